@@ -1,0 +1,176 @@
+/*
+ * hm.h — C ABI of libhm, a B200-native (sm_100a) implementation of the data-parallel
+ * hot path of Harbrecht & Zaspel, "A scalable H-matrix approach for the solution of
+ * boundary integral equations on multi-GPU clusters", arXiv 1806.11558.
+ *
+ * Citations: "P:n" = line n of the paper text (/root/reference/PAPER.md at build time);
+ * "A#" = a reading of an ambiguous passage, listed in DESIGN.md §3.
+ *
+ * The path:
+ *   hm_build_tree  panel geometry, Morton codes + stable sort, cardinality-based cluster
+ *                  tree, bounding boxes, level-wise block-cluster-tree traversal
+ *                  (Algorithm 1), leaf partition
+ *   hm_setup       batched near-field Galerkin assembly and batched
+ *                  adaptive cross approximation of the rank's leaves
+ *   hm_matvec      batched H-matrix-vector product + global sum
+ *   hm_solve       CG or GMRES(m) driving hm_matvec
+ *
+ * Conventions shared by every entry point
+ *   - Return value: hm_status.  On any non-HM_OK return, hm_last_error(ctx) holds a
+ *     one-line message; the context stays valid unless the status is HM_ERR_CUDA
+ *     (a sticky device error), after which only hm_destroy is meaningful.
+ *   - Ordering: unknown i is triangle i of the mesh passed to hm_build_tree
+ *     ("application order").  The library's internal Morton order is visible
+ *     only through hm_get_perm and the leaf quadruples of hm_get_leaves.
+ *   - Pointers: every vector argument (x, y, rhs, sol, f) may be a DEVICE pointer on the
+ *     context's device or a HOST pointer (pageable or pinned); the library detects which
+ *     with cudaPointerGetAttributes.  Host vectors are staged through library-owned
+ *     device buffers and the call returns only after the result is back in host memory.
+ *     Device vectors are read/written in stream order on the context stream.
+ *   - Ownership: all inputs are caller-owned and never retained after return; all tree,
+ *     leaf, factor and workspace storage is library-owned and released by hm_destroy.
+ *   - Precision: IEEE binary64 throughout (the paper states none; BASELINE.json fixes FP64).
+ *   - Multi-GPU: one context per process per GPU.  Calls marked COLLECTIVE
+ *     must be made by every rank of the communicator, in the same order, with identical
+ *     arguments (except the rank's own device buffers).
+ */
+#ifndef HM_H
+#define HM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hm_ctx_s* hm_ctx;
+
+typedef enum {
+  HM_OK = 0,
+  HM_ERR_ARG = 1,        /* invalid argument (see each function) */
+  HM_ERR_STATE = 2,      /* call out of order (e.g. hm_setup before hm_build_tree) */
+  HM_ERR_OOM = 3,        /* device or host allocation failed */
+  HM_ERR_CUDA = 4,       /* CUDA runtime/driver error (sticky) */
+  HM_ERR_NCCL = 5,       /* NCCL error */
+  HM_ERR_NUMERIC = 6,    /* non-finite matrix entry or vector value */
+  HM_ERR_BREAKDOWN = 7   /* Krylov breakdown (CG: p^T H p <= 0) */
+} hm_status;
+
+#define HM_NCCL_UNIQUE_ID_BYTES 128
+
+/* Surface mesh of flat triangles (nodes = element centroids).
+ * vertices: n_vertices*3 doubles, xyz row-major.  triangles: n_triangles*3 int32, 0-based
+ * vertex ids; vertices must be deduplicated (singular-entry classification compares ids).
+ * memory: 0 = both arrays in host memory, 1 = both in device memory on the ctx device. */
+typedef struct {
+  const double* vertices;
+  int64_t n_vertices;
+  const int32_t* triangles;
+  int64_t n_triangles;
+  int memory;
+} hm_mesh;
+
+/* Create a context on CUDA device `device` for rank `rank` of `world_size` ranks.
+ * nccl_unique_id: HM_NCCL_UNIQUE_ID_BYTES bytes of an ncclUniqueId made by
+ * hm_nccl_unique_id on rank 0 and broadcast by the caller; NULL iff world_size == 1.
+ * cuda_stream: a cudaStream_t on `device`, or NULL for a library-owned stream.
+ * Errors: HM_ERR_ARG (rank/world/device out of range, id NULL with world_size > 1),
+ * HM_ERR_CUDA, HM_ERR_NCCL.  COLLECTIVE when world_size > 1. */
+hm_status hm_create(hm_ctx* out, int device, int rank, int world_size,
+                    const void* nccl_unique_id, void* cuda_stream);
+/* Fill `id_out` (HM_NCCL_UNIQUE_ID_BYTES bytes) with a fresh ncclUniqueId. */
+hm_status hm_nccl_unique_id(void* id_out);
+/* Release everything owned by the context.  Safe on NULL. */
+hm_status hm_destroy(hm_ctx ctx);
+/* Message of the last failing call on ctx (valid until the next call on ctx). */
+const char* hm_last_error(hm_ctx ctx);
+
+/* Options (hm_set_option / hm_get_option), numeric values:
+ *   "k_max"        ACA rank cap per block (A11), default 64, >= 1
+ *   "solver"       0 = GMRES(restart) (BASELINE.json), 1 = CG; default 0
+ *   "restart"      GMRES restart length m, default 100
+ *   "max_iter"     Krylov iteration cap (total matvecs), default 10000
+ *   "aca_chunk_mb" ACA workspace budget per chunk in MiB, default 4096
+ *   "aca_kws"      ACA workspace columns per block before the overflow re-run, default 32
+ * Errors: HM_ERR_ARG for an unknown key or an out-of-range value. */
+hm_status hm_set_option(hm_ctx ctx, const char* key, double value);
+hm_status hm_get_option(hm_ctx ctx, const char* key, double* value);
+
+/* Build the cluster tree and block cluster tree for `mesh` with
+ * C_leaf = leaf_size and admissibility parameter eta (defaults of the paper:
+ * 32 and 1.0), then split both leaf lists into world_size contiguous
+ * cost-balanced sub-lists (A18).  The mesh is copied; the caller
+ * may free it after return.  Replicated on every rank; no communication.
+ * Re-calling invalidates a previous hm_setup.  Synchronous.
+ * Errors: HM_ERR_ARG (leaf_size < 1, eta < 0 or not finite, n_triangles < 1 or > 2^30,
+ * a vertex id out of range, a triangle of zero area), HM_ERR_OOM, HM_ERR_CUDA. */
+hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double eta);
+
+/* Assemble this rank's part of the H-matrix: every owned non-admissible leaf is evaluated
+ * densely, every owned admissible leaf is compressed by ACA with partial
+ * pivoting and the relative Frobenius stop ||u_k|| ||v_k|| <= eps_aca ||S_k||_F (A11-A12).
+ * No communication.  Synchronous.
+ * Errors: HM_ERR_STATE (no tree), HM_ERR_ARG (eps_aca <= 0 or not finite), HM_ERR_OOM,
+ * HM_ERR_NUMERIC (a non-finite entry; message names the block), HM_ERR_CUDA. */
+hm_status hm_setup(hm_ctx ctx, double eps_aca);
+
+/* y = H x, x and y of length N in application order (host or device pointers).
+ * Each rank applies its own leaves; partial products are summed over all ranks
+ * (ncclAllReduce), so every rank receives the full y.  COLLECTIVE.
+ * Stream-ordered for device pointers; synchronous for host pointers.
+ * Errors: HM_ERR_STATE (no setup), HM_ERR_ARG (NULL pointer or x == y), HM_ERR_CUDA,
+ * HM_ERR_NCCL. */
+hm_status hm_matvec(hm_ctx ctx, const double* x, double* y);
+
+/* Solve H sol = rhs with x0 = 0, stopping at ||r||_2 <= tol ||rhs||_2 or after
+ * "max_iter" matvecs.  Solver chosen by option "solver".  Vectors replicated on all ranks,
+ * one all-reduce per matvec.  COLLECTIVE.  Synchronous.
+ * iters_out: matvecs performed (may be NULL); rel_residual_out: true relative residual
+ * ||rhs - H sol|| / ||rhs|| after the last iteration (may be NULL).
+ * Non-convergence within max_iter is NOT an error: HM_OK with *rel_residual_out > tol.
+ * Errors: HM_ERR_STATE, HM_ERR_ARG (tol <= 0), HM_ERR_BREAKDOWN (CG), HM_ERR_CUDA,
+ * HM_ERR_NCCL. */
+hm_status hm_solve(hm_ctx ctx, const double* rhs, double* sol, double tol,
+                   int* iters_out, double* rel_residual_out);
+
+/* Right-hand side f_i = int_{T_i} f: kind 0 -> f = 1 (f_i = |T_i|);
+ * kind 1 -> the paper's f(x) = 4x1^2 - 3x2^2 - x3^2, edge-midpoint rule (exact for
+ * quadratics on flat triangles, A16).  f: length N, application order, host or device.
+ * Errors: HM_ERR_STATE (no tree), HM_ERR_ARG. */
+hm_status hm_assemble_rhs(hm_ctx ctx, int kind, double* f);
+
+/* ---- introspection (host buffers) ---- */
+/* perm[s] = application index of internal position s (length N). */
+hm_status hm_get_perm(hm_ctx ctx, int32_t* perm);
+/* kind 0 = admissible leaves, 1 = dense leaves, in canonical DFS order (A10).
+ * *count = number of leaves; if quads != NULL it receives 4*count int32
+ * (row_lo, row_hi, col_lo, col_hi) in internal indices, half-open.  owned_begin/end
+ * (may be NULL): this rank's sub-list [begin, end). */
+hm_status hm_get_leaves(hm_ctx ctx, int kind, int64_t* count, int32_t* quads,
+                        int64_t* owned_begin, int64_t* owned_end);
+/* Cluster tree: *count clusters; arrays (may be NULL) lo, hi (internal, half-open),
+ * depth, bbox (6 doubles: min xyz, max xyz). */
+hm_status hm_get_clusters(hm_ctx ctx, int64_t* count, int32_t* lo, int32_t* hi,
+                          int32_t* depth, double* bbox);
+/* Morton codes (application order, length N). */
+hm_status hm_get_codes(hm_ctx ctx, uint64_t* codes);
+/* Galerkin entries a_ij for n application-index pairs (2n int64, host) -> out (n, host),
+ * evaluated by the same device code as setup.  Errors: HM_ERR_STATE, HM_ERR_ARG. */
+hm_status hm_eval_entries(hm_ctx ctx, int64_t n, const int64_t* pairs, double* out);
+/* Stored dense block of owned dense leaf `leaf` (m*n doubles, row-major). */
+hm_status hm_get_dense_block(hm_ctx ctx, int64_t leaf, double* block);
+/* Rank k of owned admissible leaf `leaf`; if U/V non-NULL they receive U (m*k) and
+ * V (n*k), column-major (R = U V^T); if pivots non-NULL, 2k int32 (row, col)
+ * local pivot indices in the order chosen. */
+hm_status hm_get_lowrank(hm_ctx ctx, int64_t leaf, int32_t* k, double* U, double* V,
+                         int32_t* pivots);
+/* Gauss-Legendre table on [0,1] used by the device rules (n in 1..8). */
+hm_status hm_quadrature_table(int n, double* nodes, double* weights);
+/* JSON object with counts, bytes, per-phase device times (ms), kernel-evaluation counts,
+ * rank histogram, partition bounds.  Writes at most buf_len bytes incl. the NUL.
+ * Errors: HM_ERR_ARG if buf_len is too small (the message gives the needed size). */
+hm_status hm_get_stats(hm_ctx ctx, char* json_buf, int64_t buf_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HM_H */

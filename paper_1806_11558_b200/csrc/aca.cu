@@ -1,0 +1,460 @@
+// aca.cu — batched adaptive cross approximation of the rank's admissible leaves
+// (batching P:413-430), partial pivoting with the Frobenius stop (A11-A12).
+//
+// Design: all blocks of a chunk advance in lock-step, one ACA step per
+// round of five kernels —
+//   row   : one thread per residual-row entry  r_j = a(i,j) - sum_l U[i,l] V[j,l]
+//   pivot : one warp per block, argmax |r_j| (lowest j on ties), v = r / r_j*
+//   col   : one thread per residual-column entry u_t = a(t,j*) - sum_l U[t,l] V[j*,l]
+//   update: one warp per block, ||S_k||_F^2 update, stop test, next row = argmax unused |u_t|
+// Residual updates are sequential in l with separately rounded products and differences,
+// so r, u and therefore every pivot are bit-identical to the reading; only the norms
+// (which feed the stop test alone) are tree-reduced.  Workspace per block holds KWS
+// columns; blocks that reach KWS without stopping are re-run with k_max columns.
+// Finished blocks are packed into the factor pool as [U (m x k) | V (n x k)], col-major.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "entry.cuh"
+
+namespace hm {
+
+namespace {
+
+struct AcaBlk {
+  Quad q;
+  int32_t m, n, kmax, pad;
+  int64_t uoff, voff, boff;
+};
+
+struct AcaState {
+  int32_t i, k, js, status;   // status: 0 active, 1 done, 2 workspace overflow
+  int32_t skip, pad0;
+  double S2, vv;
+};
+
+__device__ __forceinline__ int64_t find_seg(const int64_t* __restrict__ pre, int64_t n, int64_t e) {
+  int64_t lo = 0, hi = n;   // largest c with pre[c] <= e
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (pre[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_step_sizes(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S, int64_t nb,
+                             int64_t* __restrict__ rsz, int64_t* __restrict__ csz) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > nb) return;
+  if (c == nb) { rsz[c] = 0; csz[c] = 0; return; }
+  const bool act = S[c].status == 0;
+  rsz[c] = act ? B[c].n : 0;
+  csz[c] = act ? B[c].m : 0;
+}
+
+template <bool ROW>
+__global__ void k_aca_gen(const Panel* __restrict__ P, const AcaBlk* __restrict__ B, const AcaState* __restrict__ S,
+                          const int64_t* __restrict__ pre, int64_t nb, int64_t total, double* __restrict__ Uw,
+                          double* __restrict__ Vw, unsigned long long* __restrict__ evals) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long ev = 0;
+  if (e < total) {
+    const int64_t c = find_seg(pre, nb, e);
+    const AcaBlk b = B[c];
+    const AcaState st = S[c];
+    if (ROW || !st.skip) {
+      const int idx = (int)(e - pre[c]);                   // j (row step) or t (column step)
+      const int s = ROW ? b.q.rlo + st.i : b.q.rlo + idx;
+      const int t = ROW ? b.q.clo + idx : b.q.clo + st.js;
+      const bool swap = __ldg(&P[t].app) < __ldg(&P[s].app);
+      const int xs = swap ? t : s, ys = swap ? s : t;
+      const int cls = entry_class(P[xs], P[ys]);
+      double a;
+      if (cls >= 3) {
+        double X[9], Y[9], I;
+        load_panel_vertices(P, xs, X);
+        load_panel_vertices(P, ys, Y);
+        switch (cls) {
+          case 3: I = regular_sum<3>(X, Y); break;
+          case 4: I = regular_sum<4>(X, Y); break;
+          case 5: I = regular_sum<5>(X, Y); break;
+          default: I = regular_sum<6>(X, Y); break;
+        }
+        a = dmul(dmul(I, dmul(dmul(2.0, P[xs].area), dmul(2.0, P[ys].area))), kInv4Pi);
+      } else {
+        a = entry_st(P, s, t);
+      }
+      ev = (unsigned long long)rule_evals(cls);
+      const double* U = Uw + b.uoff;
+      const double* V = Vw + b.voff;
+      if (ROW) {
+        for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[st.i + (int64_t)l * b.m], V[idx + (int64_t)l * b.n]));
+        Vw[b.voff + (int64_t)st.k * b.n + idx] = a;
+      } else {
+        for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[idx + (int64_t)l * b.m], V[st.js + (int64_t)l * b.n]));
+        Uw[b.uoff + (int64_t)st.k * b.m + idx] = a;
+      }
+    }
+  }
+  typedef cub::BlockReduce<unsigned long long, 128> BR;
+  __shared__ typename BR::TempStorage tmp;
+  unsigned long long tot = BR(tmp).Sum(ev);
+  if (threadIdx.x == 0 && tot) atomicAdd(evals, tot);
+}
+
+__device__ __forceinline__ void warp_argmax(double& v, int& idx) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ bool is_used(const uint32_t* bm, int t) { return (bm[t >> 5] >> (t & 31)) & 1u; }
+
+// smallest unused row, or -1
+__device__ int first_unused(const uint32_t* bm, int m, int lane) {
+  int words = (m + 31) >> 5;
+  int best = INT_MAX;
+  for (int w = lane; w < words; w += 32) {
+    uint32_t free_bits = ~bm[w];
+    if (w == words - 1 && (m & 31)) free_bits &= (1u << (m & 31)) - 1u;
+    if (free_bits) { best = min(best, w * 32 + __ffs(free_bits) - 1); }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  return best == INT_MAX ? -1 : best;
+}
+
+__global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, int64_t nb,
+                            double* __restrict__ Vw, uint32_t* __restrict__ bmap) {
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nb) return;
+  AcaState st = S[c];
+  if (st.status != 0) return;
+  const AcaBlk b = B[c];
+  double* r = Vw + b.voff + (int64_t)st.k * b.n;
+  uint32_t* bm = bmap + b.boff;
+  double best = -1.0;
+  int bj = INT_MAX;
+  for (int j = lane; j < b.n; j += 32) {
+    double a = fabs(r[j]);
+    if (a > best) { best = a; bj = j; }
+  }
+  warp_argmax(best, bj);
+  __syncwarp();
+  if (lane == 0) bm[st.i >> 5] |= 1u << (st.i & 31);   // row i is used (A12)
+  __syncwarp();
+  const double piv = r[bj];
+  if (piv == 0.0) {                                     // zero residual row: next unused row
+    int nx = first_unused(bm, b.m, lane);
+    if (lane == 0) {
+      if (nx < 0) st.status = 1;
+      else { st.i = nx; st.skip = 1; }
+      S[c] = st;
+    }
+    return;
+  }
+  double vv = 0.0;
+  for (int j = lane; j < b.n; j += 32) {
+    double v = ddiv(r[j], piv);
+    r[j] = v;
+    vv += v * v;
+  }
+  vv = warp_sum(vv);
+  if (lane == 0) {
+    st.js = bj;
+    st.vv = vv;
+    st.skip = 0;
+    S[c] = st;
+  }
+}
+
+__global__ void k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, int64_t nb,
+                             const double* __restrict__ Uw, const double* __restrict__ Vw,
+                             const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv, int kws, double eps) {
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nb) return;
+  AcaState st = S[c];
+  if (st.status != 0 || st.skip) return;
+  const AcaBlk b = B[c];
+  const double* U = Uw + b.uoff;
+  const double* V = Vw + b.voff;
+  const double* u = U + (int64_t)st.k * b.m;
+  const double* v = V + (int64_t)st.k * b.n;
+  double uu = 0.0;
+  for (int t = lane; t < b.m; t += 32) uu += u[t] * u[t];
+  uu = warp_sum(uu);
+  double cross = 0.0;
+  for (int l = 0; l < st.k; ++l) {
+    double du = 0.0, dv = 0.0;
+    for (int t = lane; t < b.m; t += 32) du += u[t] * U[t + (int64_t)l * b.m];
+    for (int j = lane; j < b.n; j += 32) dv += V[j + (int64_t)l * b.n] * v[j];
+    du = warp_sum(du);
+    dv = warp_sum(dv);
+    cross += du * dv;
+  }
+  st.S2 = (st.S2 + 2.0 * cross) + uu * st.vv;
+  if (lane == 0) {
+    piv[(int64_t)c * 2 * kws + 2 * st.k] = st.i;
+    piv[(int64_t)c * 2 * kws + 2 * st.k + 1] = st.js;
+  }
+  st.k += 1;
+  if (sqrt(uu) * sqrt(st.vv) <= eps * sqrt(st.S2)) st.status = 1;    // stop test (A11)
+  else if (st.k >= b.kmax) st.status = 1;                              // rank budget
+  else if (st.k >= kws) st.status = 2;                                 // workspace full: re-run
+  if (st.status == 0) {                                                // next row pivot (A12)
+    const uint32_t* bm = bmap + b.boff;
+    double best = -1.0;
+    int bt = INT_MAX;
+    for (int t = lane; t < b.m; t += 32) {
+      if (is_used(bm, t)) continue;
+      double a = fabs(u[t]);
+      if (a > best) { best = a; bt = t; }
+    }
+    warp_argmax(best, bt);
+    if (bt == INT_MAX) st.status = 1;
+    else st.i = bt;
+  }
+  if (lane == 0) S[c] = st;
+}
+
+__global__ void k_init_state(AcaState* __restrict__ S, int64_t nb) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nb) return;
+  AcaState s;
+  s.i = 0; s.k = 0; s.js = 0; s.status = 0; s.skip = 0; s.pad0 = 0; s.S2 = 0.0; s.vv = 0.0;
+  S[c] = s;
+}
+
+__global__ void k_final_sizes(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S, int64_t nb,
+                              int64_t* __restrict__ fsz) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > nb) return;
+  if (c == nb) { fsz[c] = 0; return; }
+  fsz[c] = S[c].status == 1 ? (int64_t)S[c].k * (B[c].m + B[c].n) : 0;
+}
+
+// pack finished blocks: [U (m x k) | V (n x k)] column-major, straight copies of the
+// first k workspace columns
+__global__ void k_aca_store(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S, int64_t nb,
+                            const int32_t* __restrict__ owned, const int64_t* __restrict__ fpre, int64_t base,
+                            const double* __restrict__ Uw, const double* __restrict__ Vw, double* __restrict__ pool,
+                            int64_t* __restrict__ foff, int32_t* __restrict__ frank) {
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nb) return;
+  const AcaState st = S[c];
+  if (st.status != 1) return;
+  const AcaBlk b = B[c];
+  const int64_t o = base + fpre[c];
+  const int64_t mu = (int64_t)st.k * b.m, nv = (int64_t)st.k * b.n;
+  for (int64_t x = lane; x < mu; x += 32) pool[o + x] = Uw[b.uoff + x];
+  for (int64_t x = lane; x < nv; x += 32) pool[o + mu + x] = Vw[b.voff + x];
+  if (lane == 0) {
+    foff[owned[c]] = o;
+    frank[owned[c]] = st.k;
+  }
+}
+
+template <class F>
+void cub_call(DBuf<char>& tmp, F&& f) {
+  size_t bytes = 0;
+  HM_CUDA(f(nullptr, bytes));
+  tmp.alloc(bytes);
+  HM_CUDA(f(tmp.get(), bytes));
+}
+
+struct AcaWork {
+  DBuf<AcaBlk> blk;
+  DBuf<AcaState> state;
+  DBuf<int32_t> owned, piv;
+  DBuf<int64_t> rsz, csz, rpre, cpre;
+  DBuf<double> Uw, Vw;
+  DBuf<uint32_t> bmap;
+  DBuf<unsigned long long> evals;
+  DBuf<char> tmp;
+};
+
+// Run ACA on the owned admissible leaves listed in `ids` (indices into the owned list) with
+// `kws` workspace columns; appends blocks that overflowed to `overflow`.
+void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws, std::vector<int32_t>& overflow,
+               std::vector<std::vector<int32_t>>* pivots_out) {
+  cudaStream_t st = C.stream;
+  const int64_t nb = (int64_t)ids.size();
+  std::vector<AcaBlk> hb(nb);
+  int64_t uo = 0, vo = 0, bo = 0;
+  for (int64_t c = 0; c < nb; ++c) {
+    const Quad& q = C.h_adm[C.adm_begin + ids[c]];
+    AcaBlk& b = hb[c];
+    b.q = q;
+    b.m = q.rhi - q.rlo;
+    b.n = q.chi - q.clo;
+    b.kmax = std::min(std::min(b.m, b.n), C.k_max);
+    b.pad = 0;
+    b.uoff = uo; b.voff = vo; b.boff = bo;
+    uo += (int64_t)b.m * kws;
+    vo += (int64_t)b.n * kws;
+    bo += (b.m + 31) / 32;
+  }
+  W.blk.alloc(nb); W.state.alloc(nb); W.owned.alloc(nb); W.piv.alloc(nb * 2 * kws);
+  W.rsz.alloc(nb + 1); W.csz.alloc(nb + 1); W.rpre.alloc(nb + 1); W.cpre.alloc(nb + 1);
+  W.Uw.alloc(uo); W.Vw.alloc(vo); W.bmap.alloc(bo);
+  HM_CUDA(cudaMemcpyAsync(W.blk.get(), hb.data(), nb * sizeof(AcaBlk), cudaMemcpyHostToDevice, st));
+  HM_CUDA(cudaMemcpyAsync(W.owned.get(), ids.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  HM_CUDA(cudaMemsetAsync(W.bmap.get(), 0, bo * sizeof(uint32_t), st));
+  k_init_state<<<grid_for(nb, 256), 256, 0, st>>>(W.state.get(), nb);
+  HM_CHECK_LAUNCH();
+  const Panel* P = C.panel.get();
+  for (int step = 0;; ++step) {
+    k_step_sizes<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.rsz.get(), W.csz.get());
+    HM_CHECK_LAUNCH();
+    cub_call(W.tmp, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, W.rsz.get(), W.rpre.get(), nb + 1, st);
+    });
+    cub_call(W.tmp, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, W.csz.get(), W.cpre.get(), nb + 1, st);
+    });
+    int64_t tot[2];
+    HM_CUDA(cudaMemcpyAsync(&tot[0], W.rpre.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaMemcpyAsync(&tot[1], W.cpre.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaStreamSynchronize(st));
+    if (tot[0] == 0) break;
+    C.aca_steps++;
+    C.entries_aca += (double)(tot[0] + tot[1]);
+    k_aca_gen<true><<<grid_for(tot[0], 128), 128, 0, st>>>(P, W.blk.get(), W.state.get(), W.rpre.get(), nb, tot[0],
+                                                           W.Uw.get(), W.Vw.get(), W.evals.get());
+    HM_CHECK_LAUNCH();
+    k_aca_pivot<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Vw.get(), W.bmap.get());
+    HM_CHECK_LAUNCH();
+    k_aca_gen<false><<<grid_for(tot[1], 128), 128, 0, st>>>(P, W.blk.get(), W.state.get(), W.cpre.get(), nb, tot[1],
+                                                            W.Uw.get(), W.Vw.get(), W.evals.get());
+    HM_CHECK_LAUNCH();
+    k_aca_update<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Uw.get(), W.Vw.get(),
+                                                         W.bmap.get(), W.piv.get(), kws, C.eps_aca);
+    HM_CHECK_LAUNCH();
+  }
+  // pack finished blocks into the factor pool
+  k_final_sizes<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.rsz.get());
+  HM_CHECK_LAUNCH();
+  cub_call(W.tmp, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, W.rsz.get(), W.rpre.get(), nb + 1, st);
+  });
+  int64_t add = 0;
+  HM_CUDA(cudaMemcpyAsync(&add, W.rpre.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  std::vector<AcaState> hs(nb);
+  HM_CUDA(cudaMemcpyAsync(hs.data(), W.state.get(), nb * sizeof(AcaState), cudaMemcpyDeviceToHost, st));
+  HM_CUDA(cudaStreamSynchronize(st));
+  const int64_t base = (int64_t)(C.fpool.used / sizeof(double));
+  C.fpool.ensure((base + add) * sizeof(double) + 64);
+  C.fpool.used = (base + add) * sizeof(double);
+  k_aca_store<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(),
+                                                      base, W.Uw.get(), W.Vw.get(), (double*)C.fpool.base,
+                                                      C.foff.get(), C.frank.get());
+  HM_CHECK_LAUNCH();
+  std::vector<int32_t> hp;
+  if (pivots_out) {
+    hp.resize(nb * 2 * kws);
+    HM_CUDA(cudaMemcpyAsync(hp.data(), W.piv.get(), hp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  HM_CUDA(cudaStreamSynchronize(st));
+  for (int64_t c = 0; c < nb; ++c) {
+    if (hs[c].status == 2) { overflow.push_back(ids[c]); continue; }
+    if (pivots_out)
+      (*pivots_out)[ids[c]].assign(hp.begin() + c * 2 * kws, hp.begin() + c * 2 * kws + 2 * hs[c].k);
+  }
+}
+
+}  // namespace
+
+void setup_aca(Context& C) {
+  cudaStream_t st = C.stream;
+  const int64_t nb = C.adm_end - C.adm_begin;
+  C.foff.alloc_exact(nb + 1);
+  C.frank.alloc_exact(nb + 1);
+  HM_CUDA(cudaMemsetAsync(C.frank.get(), 0, (nb + 1) * sizeof(int32_t), st));
+  C.fpool.used = 0;
+  C.aca_steps = 0; C.aca_chunks = 0; C.aca_overflow = 0;
+  C.entries_aca = 0;
+  if (nb == 0) { C.factor_doubles = 0; C.evals_aca = 0; return; }
+  if (C.h_adm.size() != (size_t)C.nadm) {
+    C.h_adm.resize(C.nadm);
+    HM_CUDA(cudaMemcpyAsync(C.h_adm.data(), C.adm.get(), C.nadm * sizeof(Quad), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaStreamSynchronize(st));
+  }
+  // reserve VA for the worst case (k_max terms per block), map on demand
+  size_t worst = 0;
+  for (int64_t b = C.adm_begin; b < C.adm_end; ++b) {
+    const Quad& q = C.h_adm[b];
+    int64_t m = q.rhi - q.rlo, n = q.chi - q.clo;
+    worst += (size_t)std::min<int64_t>(std::min(m, n), C.k_max) * (m + n);
+  }
+  C.fpool.init(C.device, worst * sizeof(double) + (64u << 20));
+  AcaWork W;
+  W.evals.alloc(1);
+  HM_CUDA(cudaMemsetAsync(W.evals.get(), 0, sizeof(unsigned long long), st));
+  const bool rec = C.N <= 400000;
+  auto& pivots = C.h_piv;
+  pivots.clear();
+  if (rec) pivots.resize(nb);
+  const int kws = std::max(1, std::min(C.k_max, (int)C.aca_kws));
+  const double budget = C.aca_chunk_mb * 1048576.0;
+  std::vector<int32_t> ids, overflow;
+  double used = 0;
+  for (int64_t b = 0; b <= nb; ++b) {
+    double need = 0;
+    if (b < nb) {
+      const Quad& q = C.h_adm[C.adm_begin + b];
+      need = 8.0 * kws * ((q.rhi - q.rlo) + (q.chi - q.clo)) + 64.0;
+    }
+    if (b == nb || (!ids.empty() && used + need > budget)) {
+      if (!ids.empty()) {
+        run_chunk(C, W, ids, kws, overflow, rec ? &pivots : nullptr);
+        C.aca_chunks++;
+      }
+      ids.clear();
+      used = 0;
+    }
+    if (b < nb) { ids.push_back((int32_t)b); used += need; }
+  }
+  C.aca_overflow = (int)overflow.size();
+  if (!overflow.empty()) {          // re-run with the full rank budget, chunked by the same budget
+    std::vector<int32_t> none, part;
+    double u2 = 0;
+    for (size_t x = 0; x <= overflow.size(); ++x) {
+      double need = 0;
+      if (x < overflow.size()) {
+        const Quad& q = C.h_adm[C.adm_begin + overflow[x]];
+        need = 8.0 * C.k_max * ((q.rhi - q.rlo) + (q.chi - q.clo)) + 64.0;
+      }
+      if (x == overflow.size() || (!part.empty() && u2 + need > budget)) {
+        if (!part.empty()) run_chunk(C, W, part, C.k_max, none, rec ? &pivots : nullptr);
+        part.clear();
+        u2 = 0;
+      }
+      if (x < overflow.size()) { part.push_back(overflow[x]); u2 += need; }
+    }
+    if (!none.empty()) fail(HM_ERR_CUDA, "ACA overflow re-run did not converge within k_max");
+  }
+  unsigned long long ev = 0;
+  HM_CUDA(cudaMemcpyAsync(&ev, W.evals.get(), sizeof(ev), cudaMemcpyDeviceToHost, st));
+  C.h_rank.resize(nb);
+  C.h_foff.resize(nb);
+  HM_CUDA(cudaMemcpyAsync(C.h_rank.data(), C.frank.get(), nb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  HM_CUDA(cudaMemcpyAsync(C.h_foff.data(), C.foff.get(), nb * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  HM_CUDA(cudaStreamSynchronize(st));
+  C.evals_aca = (double)ev;
+  C.factor_doubles = (int64_t)(C.fpool.used / sizeof(double));
+}
+
+}  // namespace hm

@@ -1,0 +1,525 @@
+// api.cu — the extern "C" boundary of libhm (include/hm.h), the VMM factor pool and the
+// NCCL plumbing.  Every entry point converts internal exceptions to an hm_status and a
+// message retrievable with hm_last_error.
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <sstream>
+
+#include "entry.cuh"
+
+using hm::Context;
+
+struct hm_ctx_s {
+  Context C;
+};
+
+namespace hm {
+
+// ---- driver entry points (no link-time dependency on libcuda: resolved through cudart) ----
+namespace {
+struct Drv {
+  PFN_cuMemGetAllocationGranularity_v10020 gran = nullptr;
+  PFN_cuMemAddressReserve_v10020 reserve = nullptr;
+  PFN_cuMemAddressFree_v10020 vfree = nullptr;
+  PFN_cuMemCreate_v10020 create = nullptr;
+  PFN_cuMemRelease_v10020 rel = nullptr;
+  PFN_cuMemMap_v10020 map = nullptr;
+  PFN_cuMemUnmap_v10020 unmap = nullptr;
+  PFN_cuMemSetAccess_v10020 access = nullptr;
+  PFN_cuGetErrorString_v6000 errstr = nullptr;
+};
+Drv& drv() {
+  static Drv d;
+  static bool loaded = false;
+  if (!loaded) {
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      HM_CUDA(cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !*fn) fail(HM_ERR_CUDA, std::string("driver symbol missing: ") + name);
+    };
+    get("cuMemGetAllocationGranularity", (void**)&d.gran);
+    get("cuMemAddressReserve", (void**)&d.reserve);
+    get("cuMemAddressFree", (void**)&d.vfree);
+    get("cuMemCreate", (void**)&d.create);
+    get("cuMemRelease", (void**)&d.rel);
+    get("cuMemMap", (void**)&d.map);
+    get("cuMemUnmap", (void**)&d.unmap);
+    get("cuMemSetAccess", (void**)&d.access);
+    get("cuGetErrorString", (void**)&d.errstr);
+    loaded = true;
+  }
+  return d;
+}
+void cu_check(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return;
+  const char* s = nullptr;
+  if (drv().errstr) drv().errstr(r, &s);
+  throw Error{r == CUDA_ERROR_OUT_OF_MEMORY ? HM_ERR_OOM : HM_ERR_CUDA, std::string(what) + ": " + (s ? s : "?")};
+}
+}  // namespace
+
+// ---- VMM pool -------------------------------------------------------------------------
+void VmmPool::init(int dev, size_t max_bytes) {
+  release();
+  device = dev;
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = dev;
+  cu_check(drv().gran(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+  if (gran == 0) gran = 2u << 20;
+  reserved = ((max_bytes + gran - 1) / gran) * gran;
+  cu_check(drv().reserve(&base, reserved, 0, 0, 0), "cuMemAddressReserve");
+  mapped = used = 0;
+}
+
+void VmmPool::ensure(size_t bytes) {
+  if (bytes <= mapped) return;
+  if (bytes > reserved) fail(HM_ERR_OOM, "factor pool exceeds its reserved range");
+  size_t chunk = std::max(((bytes - mapped + gran - 1) / gran) * gran, std::min(reserved - mapped, (size_t)256 << 20));
+  chunk = std::min(chunk, reserved - mapped);
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  CUmemGenericAllocationHandle h;
+  cu_check(drv().create(&h, chunk, &prop, 0), "cuMemCreate");
+  CUresult r = drv().map(base + mapped, chunk, 0, h, 0);
+  if (r != CUDA_SUCCESS) { drv().rel(h); cu_check(r, "cuMemMap"); }
+  CUmemAccessDesc acc = {};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  cu_check(drv().access(base + mapped, chunk, &acc, 1), "cuMemSetAccess");
+  handles.push_back(h);
+  sizes.push_back(chunk);
+  mapped += chunk;
+}
+
+void VmmPool::release() {
+  if (!base) return;
+  cudaDeviceSynchronize();
+  size_t off = 0;
+  for (size_t i = 0; i < handles.size(); ++i) {
+    drv().unmap(base + off, sizes[i]);
+    drv().rel(handles[i]);
+    off += sizes[i];
+  }
+  drv().vfree(base, reserved);
+  handles.clear(); sizes.clear();
+  base = 0; reserved = mapped = used = 0;
+}
+
+// ---- NCCL ---------------------------------------------------------------------------------
+void allreduce_sum(Context& C, double* buf, int64_t n) {
+  HM_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, C.comm, C.stream));
+}
+
+}  // namespace hm
+
+namespace {
+
+template <class F>
+hm_status guarded(hm_ctx ctx, F&& f) {
+  if (!ctx) return HM_ERR_ARG;
+  try {
+    ctx->C.err.clear();
+    HM_CUDA(cudaSetDevice(ctx->C.device));
+    f(ctx->C);
+    return HM_OK;
+  } catch (const hm::Error& e) {
+    ctx->C.err = e.msg;
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    ctx->C.err = "host allocation failed";
+    return HM_ERR_OOM;
+  } catch (const std::exception& e) {
+    ctx->C.err = e.what();
+    return HM_ERR_ARG;
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct Timer {
+  Context& C;
+  cudaEvent_t a, b;
+  explicit Timer(Context& c) : C(c) {
+    HM_CUDA(cudaEventCreate(&a));
+    HM_CUDA(cudaEventCreate(&b));
+    HM_CUDA(cudaEventRecord(a, C.stream));
+  }
+  double ms() {
+    float t = 0;
+    HM_CUDA(cudaEventRecord(b, C.stream));
+    HM_CUDA(cudaEventSynchronize(b));
+    HM_CUDA(cudaEventElapsedTime(&t, a, b));
+    return t;
+  }
+  ~Timer() { cudaEventDestroy(a); cudaEventDestroy(b); }
+};
+
+void need_tree(Context& C) { if (!C.have_tree) hm::fail(HM_ERR_STATE, "no tree: call hm_build_tree first"); }
+void need_setup(Context& C) { if (!C.have_setup) hm::fail(HM_ERR_STATE, "no H-matrix: call hm_setup first"); }
+
+// Host/device staging of an N-vector argument
+struct Vec {
+  Context& C;
+  const double* src;
+  double* dst;
+  bool host;
+  hm::DBuf<double>* buf;
+  Vec(Context& c, hm::DBuf<double>& b, const double* in, double* out) : C(c), src(in), dst(out), buf(&b) {
+    host = !is_device_ptr(in ? (const void*)in : (const void*)out);
+    if (host) {
+      buf->alloc(C.N);
+      if (in)
+        HM_CUDA(cudaMemcpyAsync(buf->get(), in, C.N * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    }
+  }
+  const double* in() const { return host ? buf->get() : src; }
+  double* out() const { return host ? buf->get() : dst; }
+  void finish() {
+    if (host && dst) {
+      HM_CUDA(cudaMemcpyAsync(dst, buf->get(), C.N * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+      HM_CUDA(cudaStreamSynchronize(C.stream));
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+hm_status hm_nccl_unique_id(void* id_out) {
+  if (!id_out) return HM_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return HM_ERR_NCCL;
+  std::memcpy(id_out, &id, sizeof(id));
+  return HM_OK;
+}
+
+hm_status hm_create(hm_ctx* out, int device, int rank, int world_size, const void* nccl_unique_id,
+                    void* cuda_stream) {
+  if (!out) return HM_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) { cudaGetLastError(); return HM_ERR_CUDA; }
+  if (device < 0 || device >= ndev || world_size < 1 || rank < 0 || rank >= world_size) return HM_ERR_ARG;
+  if (world_size > 1 && !nccl_unique_id) return HM_ERR_ARG;
+  hm_ctx ctx = new (std::nothrow) hm_ctx_s;
+  if (!ctx) return HM_ERR_OOM;
+  ctx->C.device = device;
+  ctx->C.rank = rank;
+  ctx->C.world = world_size;
+  hm_status s = guarded(ctx, [&](Context& C) {
+    if (cuda_stream) {
+      C.stream = (cudaStream_t)cuda_stream;
+    } else {
+      HM_CUDA(cudaStreamCreateWithFlags(&C.stream, cudaStreamNonBlocking));
+      C.own_stream = true;
+    }
+    if (world_size > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_unique_id, sizeof(id));
+      HM_NCCL(ncclCommInitRank(&C.comm, world_size, id, rank));
+    }
+    hm::upload_quadrature_tables();
+  });
+  if (s != HM_OK) {
+    delete ctx;
+    return s;
+  }
+  *out = ctx;
+  return HM_OK;
+}
+
+hm_status hm_destroy(hm_ctx ctx) {
+  if (!ctx) return HM_OK;
+  cudaSetDevice(ctx->C.device);
+  if (ctx->C.stream) cudaStreamSynchronize(ctx->C.stream);
+  if (ctx->C.comm) ncclCommDestroy(ctx->C.comm);
+  bool own = ctx->C.own_stream;
+  cudaStream_t st = ctx->C.stream;
+  delete ctx;
+  if (own && st) cudaStreamDestroy(st);
+  return HM_OK;
+}
+
+const char* hm_last_error(hm_ctx ctx) { return ctx ? ctx->C.err.c_str() : "null context"; }
+
+hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
+  return guarded(ctx, [&](Context& C) {
+    std::string k = key ? key : "";
+    auto bad = [&]() { hm::fail(HM_ERR_ARG, "hm_set_option: bad value for " + k); };
+    if (!std::isfinite(v)) bad();
+    if (k == "k_max") { if (v < 1 || v > 64) bad(); C.k_max = (int)v; }
+    else if (k == "solver") { if (v != 0 && v != 1) bad(); C.solver = (int)v; }
+    else if (k == "restart") { if (v < 1 || v > 1000) bad(); C.restart = (int)v; }
+    else if (k == "max_iter") { if (v < 1) bad(); C.max_iter = (int)v; }
+    else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
+    else if (k == "aca_kws") { if (v < 1 || v > 64) bad(); C.aca_kws = v; }
+    else hm::fail(HM_ERR_ARG, "hm_set_option: unknown key '" + k + "'");
+  });
+}
+
+hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
+  return guarded(ctx, [&](Context& C) {
+    std::string k = key ? key : "";
+    if (!v) hm::fail(HM_ERR_ARG, "null value pointer");
+    if (k == "k_max") *v = C.k_max;
+    else if (k == "solver") *v = C.solver;
+    else if (k == "restart") *v = C.restart;
+    else if (k == "max_iter") *v = C.max_iter;
+    else if (k == "aca_chunk_mb") *v = C.aca_chunk_mb;
+    else if (k == "aca_kws") *v = C.aca_kws;
+    else hm::fail(HM_ERR_ARG, "hm_get_option: unknown key '" + k + "'");
+  });
+}
+
+hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double eta) {
+  return guarded(ctx, [&](Context& C) {
+    if (!mesh || !mesh->vertices || !mesh->triangles) hm::fail(HM_ERR_ARG, "hm_build_tree: null mesh");
+    if (leaf_size < 1) hm::fail(HM_ERR_ARG, "hm_build_tree: leaf_size < 1");
+    if (!(eta >= 0) || !std::isfinite(eta)) hm::fail(HM_ERR_ARG, "hm_build_tree: eta must be finite and >= 0");
+    if (mesh->n_triangles < 1 || mesh->n_triangles > (1LL << 30) || mesh->n_vertices < 3)
+      hm::fail(HM_ERR_ARG, "hm_build_tree: bad mesh sizes");
+    C.have_setup = false;
+    C.fpool.release();
+    Timer t(C);
+    hm::build_tree(C, *mesh, leaf_size, eta);
+    C.times.tree_ms = t.ms();
+  });
+}
+
+hm_status hm_setup(hm_ctx ctx, double eps_aca) {
+  return guarded(ctx, [&](Context& C) {
+    need_tree(C);
+    if (!(eps_aca > 0) || !std::isfinite(eps_aca)) hm::fail(HM_ERR_ARG, "hm_setup: eps_aca must be > 0");
+    C.have_setup = false;
+    C.eps_aca = eps_aca;
+    Timer all(C);
+    {
+      Timer t(C);
+      hm::setup_nearfield(C);
+      C.times.near_ms = t.ms();
+    }
+    {
+      Timer t(C);
+      hm::setup_aca(C);
+      C.times.aca_ms = t.ms();
+    }
+    {
+      Timer t(C);
+      hm::plan_matvec(C);
+      C.times.plan_ms = t.ms();
+    }
+    C.times.setup_ms = all.ms();
+    C.have_setup = true;
+  });
+}
+
+hm_status hm_matvec(hm_ctx ctx, const double* x, double* y) {
+  return guarded(ctx, [&](Context& C) {
+    need_setup(C);
+    if (!x || !y || (const void*)x == (const void*)y) hm::fail(HM_ERR_ARG, "hm_matvec: bad x/y");
+    Vec vx(C, C.xapp, x, nullptr);
+    Vec vy(C, C.yapp, nullptr, y);
+    C.xin.alloc(C.N);
+    C.yin.alloc(C.N);
+    hm::gather_perm(C, vx.in(), C.xin.get());
+    hm::matvec_internal(C, C.xin.get(), C.yin.get());
+    hm::scatter_perm(C, C.yin.get(), vy.out());
+    vy.finish();
+  });
+}
+
+hm_status hm_solve(hm_ctx ctx, const double* rhs, double* sol, double tol, int* iters_out,
+                   double* rel_residual_out) {
+  return guarded(ctx, [&](Context& C) {
+    need_setup(C);
+    if (!rhs || !sol) hm::fail(HM_ERR_ARG, "hm_solve: null vector");
+    if (!(tol > 0) || !std::isfinite(tol)) hm::fail(HM_ERR_ARG, "hm_solve: tol must be > 0");
+    Timer t(C);
+    Vec vb(C, C.xapp, rhs, nullptr);
+    Vec vx(C, C.yapp, nullptr, sol);
+    C.xin.alloc(C.N);
+    C.yin.alloc(C.N);
+    hm::gather_perm(C, vb.in(), C.xin.get());
+    int it = 0;
+    double rr = 0;
+    hm::solve(C, C.xin.get(), C.yin.get(), tol, &it, &rr);
+    hm::scatter_perm(C, C.yin.get(), vx.out());
+    vx.finish();
+    C.times.solve_ms = t.ms();
+    C.times.solve_iters = it;
+    C.times.solve_relres = rr;
+    if (iters_out) *iters_out = it;
+    if (rel_residual_out) *rel_residual_out = rr;
+  });
+}
+
+hm_status hm_assemble_rhs(hm_ctx ctx, int kind, double* f) {
+  return guarded(ctx, [&](Context& C) {
+    need_tree(C);
+    if (!f || (kind != 0 && kind != 1)) hm::fail(HM_ERR_ARG, "hm_assemble_rhs: bad arguments");
+    Vec vf(C, C.xapp, nullptr, f);
+    hm::assemble_rhs(C, kind, vf.out());
+    vf.finish();
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+  });
+}
+
+hm_status hm_get_perm(hm_ctx ctx, int32_t* perm) {
+  return guarded(ctx, [&](Context& C) {
+    need_tree(C);
+    if (!perm) hm::fail(HM_ERR_ARG, "null perm");
+    HM_CUDA(cudaMemcpyAsync(perm, C.perm.get(), C.N * sizeof(int32_t), cudaMemcpyDeviceToHost, C.stream));
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+  });
+}
+
+hm_status hm_get_codes(hm_ctx ctx, uint64_t* codes) {
+  return guarded(ctx, [&](Context& C) {
+    need_tree(C);
+    if (!codes) hm::fail(HM_ERR_ARG, "null codes");
+    HM_CUDA(cudaMemcpyAsync(codes, C.codes_app.get(), C.N * sizeof(uint64_t), cudaMemcpyDeviceToHost, C.stream));
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+  });
+}
+
+hm_status hm_get_leaves(hm_ctx ctx, int kind, int64_t* count, int32_t* quads, int64_t* ob, int64_t* oe) {
+  return guarded(ctx, [&](Context& C) {
+    need_tree(C);
+    if (kind != 0 && kind != 1) hm::fail(HM_ERR_ARG, "kind must be 0 or 1");
+    int64_t n = kind == 0 ? C.nadm : C.ndense;
+    if (count) *count = n;
+    if (ob) *ob = kind == 0 ? C.adm_begin : C.dense_begin;
+    if (oe) *oe = kind == 0 ? C.adm_end : C.dense_end;
+    if (quads && n) {
+      HM_CUDA(cudaMemcpyAsync(quads, kind == 0 ? C.adm.get() : C.dense.get(), n * sizeof(hm::Quad),
+                              cudaMemcpyDeviceToHost, C.stream));
+      HM_CUDA(cudaStreamSynchronize(C.stream));
+    }
+  });
+}
+
+hm_status hm_get_clusters(hm_ctx ctx, int64_t* count, int32_t* lo, int32_t* hi, int32_t* depth, double* bbox) {
+  return guarded(ctx, [&](Context& C) {
+    need_tree(C);
+    if (count) *count = C.ncl;
+    auto cp = [&](void* dst, const void* src, size_t b) {
+      if (dst) HM_CUDA(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToHost, C.stream));
+    };
+    cp(lo, C.cl_lo.get(), C.ncl * 4);
+    cp(hi, C.cl_hi.get(), C.ncl * 4);
+    cp(depth, C.cl_depth.get(), C.ncl * 4);
+    cp(bbox, C.cl_box.get(), C.ncl * 48);
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+  });
+}
+
+hm_status hm_eval_entries(hm_ctx ctx, int64_t n, const int64_t* pairs, double* out) {
+  return guarded(ctx, [&](Context& C) {
+    need_tree(C);
+    if (n < 0 || (n > 0 && (!pairs || !out))) hm::fail(HM_ERR_ARG, "hm_eval_entries: bad arguments");
+    for (int64_t e = 0; e < 2 * n; ++e)
+      if (pairs[e] < 0 || pairs[e] >= C.N) hm::fail(HM_ERR_ARG, "hm_eval_entries: index out of range");
+    if (n == 0) return;
+    hm::DBuf<int64_t> dp;
+    hm::DBuf<double> dout;
+    dp.alloc(2 * n);
+    dout.alloc(n);
+    HM_CUDA(cudaMemcpyAsync(dp.get(), pairs, 2 * n * sizeof(int64_t), cudaMemcpyHostToDevice, C.stream));
+    hm::eval_entries(C, n, dp.get(), dout.get());
+    HM_CUDA(cudaMemcpyAsync(out, dout.get(), n * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+  });
+}
+
+hm_status hm_get_dense_block(hm_ctx ctx, int64_t leaf, double* block) {
+  return guarded(ctx, [&](Context& C) {
+    need_setup(C);
+    if (leaf < C.dense_begin || leaf >= C.dense_end || !block) hm::fail(HM_ERR_ARG, "leaf not owned by this rank");
+    int64_t off[2];
+    HM_CUDA(cudaMemcpyAsync(off, C.doff.get() + (leaf - C.dense_begin), 2 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            C.stream));
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+    HM_CUDA(cudaMemcpyAsync(block, C.dstore.get() + off[0], (off[1] - off[0]) * sizeof(double),
+                            cudaMemcpyDeviceToHost, C.stream));
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+  });
+}
+
+hm_status hm_get_lowrank(hm_ctx ctx, int64_t leaf, int32_t* k, double* U, double* V, int32_t* pivots) {
+  return guarded(ctx, [&](Context& C) {
+    need_setup(C);
+    if (leaf < C.adm_begin || leaf >= C.adm_end) hm::fail(HM_ERR_ARG, "leaf not owned by this rank");
+    const int64_t b = leaf - C.adm_begin;
+    if (C.h_adm.size() != (size_t)C.nadm) hm::fail(HM_ERR_STATE, "leaf list not cached");
+    const hm::Quad q = C.h_adm[leaf];
+    const int64_t m = q.rhi - q.rlo, n = q.chi - q.clo;
+    const int32_t kk = C.h_rank[b];
+    if (k) *k = kk;
+    const double* base = (const double*)C.fpool.base + C.h_foff[b];
+    if (U && kk > 0)
+      HM_CUDA(cudaMemcpyAsync(U, base, m * kk * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    if (V && kk > 0)
+      HM_CUDA(cudaMemcpyAsync(V, base + m * kk, n * kk * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    if (pivots) {
+      if (C.h_piv.size() != (size_t)(C.adm_end - C.adm_begin)) hm::fail(HM_ERR_STATE, "pivots not recorded (N > 4e5)");
+      std::memcpy(pivots, C.h_piv[b].data(), C.h_piv[b].size() * sizeof(int32_t));
+    }
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+  });
+}
+
+hm_status hm_quadrature_table(int n, double* nodes, double* weights) {
+  if (n < 1 || n > 8 || !nodes || !weights) return HM_ERR_ARG;
+  hm::quadrature_table_host(n, nodes, weights);
+  return HM_OK;
+}
+
+hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
+  return guarded(ctx, [&](Context& C) {
+    std::ostringstream o;
+    o.precision(17);
+    int64_t kmin = 0, kmax = 0;
+    double ksum = 0;
+    std::vector<int64_t> hist(65, 0);
+    for (size_t b = 0; b < C.h_rank.size() && C.have_setup; ++b) {
+      int k = C.h_rank[b];
+      ksum += k;
+      kmax = std::max<int64_t>(kmax, k);
+      kmin = b == 0 ? k : std::min<int64_t>(kmin, k);
+      hist[std::min(k, 64)]++;
+    }
+    o << "{\"N\":" << C.N << ",\"rank\":" << C.rank << ",\"world\":" << C.world << ",\"leaf_size\":" << C.leaf_size
+      << ",\"eta\":" << C.eta << ",\"clusters\":" << C.ncl << ",\"adm_leaves\":" << C.nadm
+      << ",\"dense_leaves\":" << C.ndense << ",\"adm_owned\":[" << C.adm_begin << "," << C.adm_end << "]"
+      << ",\"dense_owned\":[" << C.dense_begin << "," << C.dense_end << "]"
+      << ",\"dense_doubles\":" << C.dense_doubles << ",\"factor_doubles\":" << C.factor_doubles
+      << ",\"stored_bytes\":" << 8 * (C.dense_doubles + C.factor_doubles) << ",\"eps_aca\":" << C.eps_aca
+      << ",\"k_mean\":" << (C.h_rank.empty() ? 0.0 : ksum / C.h_rank.size()) << ",\"k_min\":" << kmin
+      << ",\"k_max_seen\":" << kmax << ",\"evals_near\":" << C.evals_near << ",\"evals_aca\":" << C.evals_aca
+      << ",\"entries_aca\":" << C.entries_aca << ",\"aca_steps\":" << C.aca_steps << ",\"aca_chunks\":" << C.aca_chunks
+      << ",\"aca_overflow\":" << C.aca_overflow << ",\"tree_ms\":" << C.times.tree_ms
+      << ",\"near_ms\":" << C.times.near_ms << ",\"aca_ms\":" << C.times.aca_ms << ",\"plan_ms\":" << C.times.plan_ms
+      << ",\"setup_ms\":" << C.times.setup_ms << ",\"solve_ms\":" << C.times.solve_ms
+      << ",\"solve_iters\":" << C.times.solve_iters << ",\"solve_relres\":" << C.times.solve_relres
+      << ",\"lr_small\":" << C.n_lr_small << ",\"lr_large\":" << C.n_lr_large << ",\"rank_hist\":[";
+    for (int k = 0; k <= 64; ++k) o << (k ? "," : "") << hist[k];
+    o << "]}";
+    std::string s = o.str();
+    if (!buf || len < (int64_t)s.size() + 1)
+      hm::fail(HM_ERR_ARG, "hm_get_stats: buffer too small, need " + std::to_string(s.size() + 1));
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+// hm_internal.cuh — libhm internals shared by the .cu translation units.
+// B200 (sm_100a) only.  Built with --fmad=false: no implicit contraction anywhere; FMAs
+// appear only where the arithmetic reading writes them (A15) via fma().
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/hm.h"
+
+namespace hm {
+
+constexpr double kInv4Pi = 0.07957747154594767;  // 1/(4 pi), correctly rounded
+
+// One panel in internal (Morton) order; 128 B, one L2 line.
+struct __align__(16) Panel {
+  double v[9];      // vertices v0, v1, v2 (xyz each)
+  double c[3];      // centroid ((v0+v1)+v2)/3
+  double area;      // |T|
+  double h;         // max edge length
+  int32_t vid[3];   // vertex ids (singular-class detection)
+  int32_t app;      // application index
+};
+static_assert(sizeof(Panel) == 128, "Panel must be one 128-B line");
+
+struct Quad { int32_t rlo, rhi, clo, chi; };   // leaf tau x sigma, internal half-open ranges
+
+// Error plumbing -------------------------------------------------------------------------
+struct Error {
+  hm_status st;
+  std::string msg;
+};
+
+#define HM_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::hm::Error{e_ == cudaErrorMemoryAllocation ? HM_ERR_OOM : HM_ERR_CUDA,       \
+                        std::string(#call) + ": " + cudaGetErrorString(e_)};              \
+  } while (0)
+
+#define HM_NCCL(call)                                                                     \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      throw ::hm::Error{HM_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+#define HM_CHECK_LAUNCH() HM_CUDA(cudaGetLastError())
+
+inline void fail(hm_status st, const std::string& m) { throw Error{st, m}; }
+
+// Device buffer (RAII) -------------------------------------------------------------------
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {  // discards contents
+    if (count <= n && p) return;
+    release();
+    size_t bytes = (count ? count : 1) * sizeof(T) + 16;   // +16: bulk-copy tail slack
+    HM_CUDA(cudaMalloc(&p, bytes));
+    n = count;
+  }
+  void alloc_exact(size_t count) {
+    release();
+    alloc(count);
+  }
+  T* get() const { return p; }
+};
+
+// Growable device pool backed by CUDA virtual memory management: one reserved VA range,
+// physical 2 MiB granules mapped on demand (no copy on growth).  Holds the ACA factors.
+struct VmmPool {
+  CUdeviceptr base = 0;
+  size_t reserved = 0, mapped = 0, used = 0, gran = 0;
+  int device = 0;
+  std::vector<CUmemGenericAllocationHandle> handles;
+  std::vector<size_t> sizes;
+  void init(int dev, size_t max_bytes);
+  void ensure(size_t bytes);   // make [0, bytes) mapped
+  void release();
+  ~VmmPool() { release(); }
+};
+
+// Timers ----------------------------------------------------------------------------------
+struct PhaseTimes {
+  double tree_ms = 0, near_ms = 0, aca_ms = 0, plan_ms = 0, setup_ms = 0;
+  double last_matvec_ms = 0, solve_ms = 0;
+  int solve_iters = 0;
+  double solve_relres = 0;
+};
+
+// Context ---------------------------------------------------------------------------------
+struct Context {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  std::string err;
+
+  // options
+  int k_max = 64, solver = 0, restart = 100, max_iter = 10000;
+  double aca_chunk_mb = 4096, aca_kws = 32;
+
+  // tree state
+  bool have_tree = false, have_setup = false;
+  int64_t N = 0, nv = 0;
+  int leaf_size = 32;
+  double eta = 1.0;
+  DBuf<Panel> panel;           // internal order
+  DBuf<int32_t> perm, iperm;   // perm[s] = app index; iperm[app] = s
+  DBuf<uint64_t> codes_app;    // Morton codes, application order
+  DBuf<double> vert;           // vertex coordinates (device copy of the mesh)
+  DBuf<int32_t> tri;
+  // cluster tree (level order)
+  int64_t ncl = 0;
+  DBuf<int32_t> cl_lo, cl_hi, cl_child, cl_depth;
+  DBuf<double> cl_box, cl_diam2;
+  // leaves (canonical DFS order)
+  int64_t nadm = 0, ndense = 0;
+  DBuf<Quad> adm, dense;
+  std::vector<Quad> h_adm, h_dense;
+  int64_t adm_begin = 0, adm_end = 0, dense_begin = 0, dense_end = 0;
+
+  // setup state
+  double eps_aca = 0;
+  DBuf<double> dstore;         // packed dense blocks (owned dense leaves), row-major each
+  DBuf<int64_t> doff;          // per owned dense leaf: offset in doubles (+1 sentinel)
+  VmmPool fpool;               // packed low-rank factors: per block [U m x k | V n x k], col-major
+  DBuf<int64_t> foff;          // per owned adm leaf: offset in doubles
+  DBuf<int32_t> frank;         // per owned adm leaf: rank k
+  DBuf<int32_t> fpiv;          // per owned adm leaf: 2*k_max pivots (row, col)
+  std::vector<int32_t> h_rank;
+  std::vector<std::vector<int32_t>> h_piv;   // per owned adm leaf (recorded when N <= 4e5)
+  std::vector<int64_t> h_foff;
+  int64_t dense_doubles = 0, factor_doubles = 0;
+  double evals_near = 0, evals_aca = 0, entries_aca = 0;
+  int aca_steps = 0, aca_chunks = 0, aca_overflow = 0;
+
+  // matvec plan: owned adm leaves split by size class
+  DBuf<int32_t> lr_small, lr_large;    // owned adm leaf indices (relative to adm_begin)
+  int64_t n_lr_small = 0, n_lr_large = 0;
+
+  // work vectors (internal order)
+  DBuf<double> xin, yin, xapp, yapp, work;
+  DBuf<double> krylov;         // GMRES basis / CG vectors
+  DBuf<double> red;            // reduction scratch
+  double* h_red = nullptr;     // pinned host scratch for scalar read-back
+
+  PhaseTimes times;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+// tree.cu
+void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta);
+// nearfield.cu
+void setup_nearfield(Context& C);
+// aca.cu
+void setup_aca(Context& C);
+// matvec.cu
+void plan_matvec(Context& C);
+void matvec_internal(Context& C, const double* x_int, double* y_int);   // y = H x (local part)
+void gather_perm(Context& C, const double* x_app, double* x_int);
+void scatter_perm(Context& C, const double* y_int, double* y_app);
+// solver.cu
+void solve(Context& C, const double* rhs_int, double* sol_int, double tol, int* iters,
+           double* relres);
+// comm
+void allreduce_sum(Context& C, double* buf, int64_t n);
+// entries (entry.cu)
+void eval_entries(Context& C, int64_t n, const int64_t* d_pairs, double* d_out);
+void assemble_rhs(Context& C, int kind, double* f_app);
+void upload_quadrature_tables();
+void quadrature_table_host(int n, double* nodes, double* weights);
+
+// Utilities
+inline unsigned grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 2147483647LL) g = 2147483647LL;
+  return (unsigned)g;
+}
+
+}  // namespace hm

@@ -1,0 +1,257 @@
+// solver.cu — Krylov solvers driving the batched H-matvec (A17):
+//   CG (the paper's solver) and GMRES(m) with classical Gram-Schmidt + one
+//   re-orthogonalisation (CGS2) and Givens rotations (BASELINE.json's solver).
+// Vectors live in internal (Morton) order on the device and are replicated on every rank
+// (P:578-582); the only collective per iteration is the all-reduce inside the matvec.
+// Reductions use a fixed grid and a fixed tree, so every rank computes bit-identical
+// scalars and takes identical convergence decisions.  x0 = 0; stop at ||r|| <= tol ||b||.
+#include <cub/cub.cuh>
+
+#include <cmath>
+
+#include "entry.cuh"
+
+namespace hm {
+
+namespace {
+
+constexpr int kRedBlocks = 296;
+constexpr int kRedThreads = 256;
+
+// partial dot products of w against nv vectors V[i] (stride ld), for i < nv; partial[b*nv + i]
+__global__ void k_mdot(const double* __restrict__ Vb, int64_t ld, int nv, const double* __restrict__ w, int64_t n,
+                       double* __restrict__ partial) {
+  __shared__ double sh[kRedThreads / 32][33];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (int i0 = 0; i0 < nv; i0 += 32) {
+    const int cnt = min(32, nv - i0);
+    double acc[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q] = 0.0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+      const double wt = w[t];
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < cnt) acc[q] += Vb[(int64_t)(i0 + q) * ld + t] * wt;
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      double a = acc[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) sh[wib][q] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      double s = 0.0;
+      for (int w2 = 0; w2 < kRedThreads / 32; ++w2) s += sh[w2][threadIdx.x];
+      partial[(int64_t)blockIdx.x * nv + i0 + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_mdot_final(const double* __restrict__ partial, int nb, int nv, double* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * nv + i];
+  out[i] = s;
+}
+
+// w -= sum_i h[i] V[i]  (i ascending)
+__global__ void k_msub(const double* __restrict__ Vb, int64_t ld, int nv, const double* __restrict__ h,
+                       double* __restrict__ w, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    double x = w[t];
+    for (int i = 0; i < nv; ++i) x -= h[i] * Vb[(int64_t)i * ld + t];
+    w[t] = x;
+  }
+}
+
+// y += sum_i c[i] V[i]
+__global__ void k_madd(const double* __restrict__ Vb, int64_t ld, int nv, const double* __restrict__ c,
+                       double* __restrict__ y, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    double x = y[t];
+    for (int i = 0; i < nv; ++i) x += c[i] * Vb[(int64_t)i * ld + t];
+    y[t] = x;
+  }
+}
+
+__global__ void k_scale_to(const double* __restrict__ a, const double* __restrict__ s, bool recip,
+                           double* __restrict__ out, int64_t n) {
+  const double f = recip ? 1.0 / *s : *s;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = a[t] * f;
+}
+
+__global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = a[t] - b[t];
+}
+
+// CG update: x += a p; r -= a Ap
+__global__ void k_cg_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                        const double* __restrict__ Ap, double a, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    x[t] += a * p[t];
+    r[t] -= a * Ap[t];
+  }
+}
+
+__global__ void k_cg_p(double* __restrict__ p, const double* __restrict__ r, double beta, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    p[t] = r[t] + beta * p[t];
+}
+
+struct Red {
+  Context& C;
+  DBuf<double> part, out;
+  explicit Red(Context& c) : C(c) {}
+  // out[0..nv) = V[i]^T w on the device; returns device pointer
+  double* mdot(const double* Vb, int64_t ld, int nv, const double* w) {
+    part.alloc((size_t)kRedBlocks * nv);
+    out.alloc(nv + 8);
+    k_mdot<<<kRedBlocks, kRedThreads, 0, C.stream>>>(Vb, ld, nv, w, C.N, part.get());
+    k_mdot_final<<<(nv + 127) / 128, 128, 0, C.stream>>>(part.get(), kRedBlocks, nv, out.get());
+    HM_CHECK_LAUNCH();
+    return out.get();
+  }
+  double dot(const double* a, const double* b) {
+    double* d = mdot(a, 0, 1, b);
+    double h;
+    HM_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+    return h;
+  }
+};
+
+unsigned vgrid(int64_t n) { return std::min<unsigned>(grid_for(n, 256), 148 * 16); }
+
+void apply(Context& C, const double* x, double* y) { matvec_internal(C, x, y); }
+
+double true_relres(Context& C, Red& R, const double* b, const double* x, double bn, double* tmp) {
+  apply(C, x, tmp);
+  k_sub<<<vgrid(C.N), 256, 0, C.stream>>>(b, tmp, tmp, C.N);
+  HM_CHECK_LAUNCH();
+  double rr = R.dot(tmp, tmp);
+  return bn > 0 ? std::sqrt(rr) / bn : 0.0;
+}
+
+void cg(Context& C, const double* b, double* x, double tol, int* iters, double* relres) {
+  const int64_t N = C.N;
+  cudaStream_t st = C.stream;
+  C.krylov.alloc(3 * N);
+  double *r = C.krylov.get(), *p = r + N, *Ap = p + N;
+  Red R(C);
+  HM_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st));
+  HM_CUDA(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  HM_CUDA(cudaMemcpyAsync(p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  const double bn = std::sqrt(R.dot(b, b));
+  double rr = R.dot(r, r);
+  int it = 0;
+  if (bn == 0.0) { *iters = 0; *relres = 0.0; return; }
+  while (it < C.max_iter && std::sqrt(rr) > tol * bn) {
+    apply(C, p, Ap);
+    const double pAp = R.dot(p, Ap);
+    if (!(pAp > 0.0)) fail(HM_ERR_BREAKDOWN, "CG breakdown: p^T H p <= 0 at iteration " + std::to_string(it));
+    const double alpha = rr / pAp;
+    k_cg_xr<<<vgrid(N), 256, 0, st>>>(x, r, p, Ap, alpha, N);
+    HM_CHECK_LAUNCH();
+    const double rr1 = R.dot(r, r);
+    const double beta = rr1 / rr;
+    rr = rr1;
+    k_cg_p<<<vgrid(N), 256, 0, st>>>(p, r, beta, N);
+    HM_CHECK_LAUNCH();
+    ++it;
+  }
+  *iters = it;
+  *relres = true_relres(C, R, b, x, bn, Ap);
+}
+
+void gmres(Context& C, const double* b, double* x, double tol, int* iters, double* relres) {
+  const int64_t N = C.N;
+  const int m = std::max(1, C.restart);
+  cudaStream_t st = C.stream;
+  C.krylov.alloc((size_t)(m + 2) * N);
+  double* Vb = C.krylov.get();
+  double* w = Vb + (int64_t)(m + 1) * N;
+  Red R(C);
+  DBuf<double> hdev, hsum;
+  hdev.alloc(m + 8);
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), h(m + 1), h2(m + 1), y(m);
+  HM_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st));
+  const double bn = std::sqrt(R.dot(b, b));
+  int total = 0;
+  if (bn == 0.0) { *iters = 0; *relres = 0.0; return; }
+  for (;;) {
+    apply(C, x, w);
+    k_sub<<<vgrid(N), 256, 0, st>>>(b, w, w, N);
+    HM_CHECK_LAUNCH();
+    const double beta = std::sqrt(R.dot(w, w));
+    if (beta <= tol * bn || total >= C.max_iter) break;
+    HM_CUDA(cudaMemcpyAsync(hdev.get(), &beta, sizeof(double), cudaMemcpyHostToDevice, st));
+    k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb, N);
+    HM_CHECK_LAUNCH();
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int jend = 0;
+    bool conv = false;
+    for (int j = 0; j < m; ++j) {
+      apply(C, Vb + (int64_t)j * N, w);
+      ++total;
+      // CGS2
+      double* d1 = R.mdot(Vb, N, j + 1, w);
+      k_msub<<<vgrid(N), 256, 0, st>>>(Vb, N, j + 1, d1, w, N);
+      HM_CHECK_LAUNCH();
+      HM_CUDA(cudaMemcpyAsync(h.data(), d1, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+      double* d2 = R.mdot(Vb, N, j + 1, w);
+      k_msub<<<vgrid(N), 256, 0, st>>>(Vb, N, j + 1, d2, w, N);
+      HM_CHECK_LAUNCH();
+      HM_CUDA(cudaMemcpyAsync(h2.data(), d2, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+      HM_CUDA(cudaStreamSynchronize(st));
+      for (int i = 0; i <= j; ++i) h[i] += h2[i];
+      const double hn = std::sqrt(R.dot(w, w));
+      for (int i = 0; i < j; ++i) {
+        const double t1 = cs[i] * h[i] + sn[i] * h[i + 1];
+        const double t2 = -sn[i] * h[i] + cs[i] * h[i + 1];
+        h[i] = t1; h[i + 1] = t2;
+      }
+      const double den = std::sqrt(h[j] * h[j] + hn * hn);
+      if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; }
+      else { cs[j] = h[j] / den; sn[j] = hn / den; }
+      h[j] = cs[j] * h[j] + sn[j] * hn;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      for (int i = 0; i <= j; ++i) H[i + (size_t)j * (m + 1)] = h[i];
+      jend = j + 1;
+      if (std::fabs(g[j + 1]) <= tol * bn || total >= C.max_iter || hn == 0.0) { conv = true; break; }
+      HM_CUDA(cudaMemcpyAsync(hdev.get(), &hn, sizeof(double), cudaMemcpyHostToDevice, st));
+      k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb + (int64_t)(j + 1) * N, N);
+      HM_CHECK_LAUNCH();
+    }
+    for (int i = jend - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int l = i + 1; l < jend; ++l) s -= H[i + (size_t)l * (m + 1)] * y[l];
+      y[i] = s / H[i + (size_t)i * (m + 1)];
+    }
+    HM_CUDA(cudaMemcpyAsync(hdev.get(), y.data(), jend * sizeof(double), cudaMemcpyHostToDevice, st));
+    k_madd<<<vgrid(N), 256, 0, st>>>(Vb, N, jend, hdev.get(), x, N);
+    HM_CHECK_LAUNCH();
+    HM_CUDA(cudaStreamSynchronize(st));
+    if (conv && (std::fabs(g[jend]) <= tol * bn || total >= C.max_iter)) break;
+    if (total >= C.max_iter) break;
+  }
+  *iters = total;
+  *relres = true_relres(C, R, b, x, bn, w);
+}
+
+}  // namespace
+
+void solve(Context& C, const double* rhs_int, double* sol_int, double tol, int* iters, double* relres) {
+  if (C.solver == 1) cg(C, rhs_int, sol_int, tol, iters, relres);
+  else gmres(C, rhs_int, sol_int, tol, iters, relres);
+}
+
+}  // namespace hm

@@ -1,0 +1,439 @@
+// tree.cu — hm_build_tree on the device:
+//   a1 panel geometry, a2 Morton codes + stable radix sort, a3 cardinality-based cluster
+//   tree + bounding boxes (level-wise), a4 level-wise block-cluster-tree traversal with
+//   admissibility (Algorithm 1) and canonical DFS leaf order, plus the leaf partition
+//   (A18).
+// All floating-point decisions use explicitly rounded intrinsics so that codes, clusters and
+// leaf lists are bit-identical to the definition (A4-A10).
+#include <cub/cub.cuh>
+
+#include "entry.cuh"
+
+namespace hm {
+
+namespace {
+
+
+__global__ void k_geometry(const double* __restrict__ V, const int32_t* __restrict__ T, int64_t N,
+                           int64_t nv, double* __restrict__ cen, double* __restrict__ area,
+                           double* __restrict__ hh, unsigned int* bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int32_t a = T[3 * i], b = T[3 * i + 1], c = T[3 * i + 2];
+  if (a < 0 || b < 0 || c < 0 || a >= nv || b >= nv || c >= nv) { atomicOr(bad, 1u); return; }
+  double v0[3], v1[3], v2[3];
+  for (int k = 0; k < 3; ++k) { v0[k] = V[3 * (int64_t)a + k]; v1[k] = V[3 * (int64_t)b + k]; v2[k] = V[3 * (int64_t)c + k]; }
+  for (int k = 0; k < 3; ++k) cen[3 * i + k] = ddiv(dadd(dadd(v0[k], v1[k]), v2[k]), 3.0);
+  double e01[3], e02[3];
+  for (int k = 0; k < 3; ++k) { e01[k] = dsub(v1[k], v0[k]); e02[k] = dsub(v2[k], v0[k]); }
+  const double cx = dsub(dmul(e01[1], e02[2]), dmul(e01[2], e02[1]));
+  const double cy = dsub(dmul(e01[2], e02[0]), dmul(e01[0], e02[2]));
+  const double cz = dsub(dmul(e01[0], e02[1]), dmul(e01[1], e02[0]));
+  const double ar = dmul(0.5, __dsqrt_rn(dadd(dadd(dmul(cx, cx), dmul(cy, cy)), dmul(cz, cz))));
+  area[i] = ar;
+  if (!(ar > 0.0)) atomicOr(bad, 2u);
+  const double l0 = edge_length(v0, v1), l1 = edge_length(v1, v2), l2 = edge_length(v2, v0);
+  const double m = l0 > l1 ? l0 : l1;
+  hh[i] = m > l2 ? m : l2;
+}
+
+// global centroid box: per-block partial min/max, then one block finishes
+__global__ void k_minmax(const double* __restrict__ cen, int64_t N, double* __restrict__ part) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < 3; ++k) {
+      double x = cen[3 * i + k];
+      if (x < lo[k]) lo[k] = x;
+      if (x > hi[k]) hi[k] = x;
+    }
+  __shared__ double s[6][256];
+  for (int k = 0; k < 3; ++k) { s[k][threadIdx.x] = lo[k]; s[3 + k][threadIdx.x] = hi[k]; }
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int k = 0; k < 3; ++k) {
+        double a = s[k][threadIdx.x + w], b = s[3 + k][threadIdx.x + w];
+        if (a < s[k][threadIdx.x]) s[k][threadIdx.x] = a;
+        if (b > s[3 + k][threadIdx.x]) s[3 + k][threadIdx.x] = b;
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[6 * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_minmax_final(const double* __restrict__ part, int nb, double* __restrict__ box) {
+  if (threadIdx.x >= 6) return;
+  int k = threadIdx.x;
+  double v = part[k];
+  for (int b = 1; b < nb; ++b) {
+    double x = part[6 * b + k];
+    if (k < 3 ? x < v : x > v) v = x;
+  }
+  box[k] = v;
+}
+
+__device__ __forceinline__ uint64_t quantise(double c, double lo, double hi) {
+  if (!(hi > lo)) return 0;
+  const double s = dmul(ddiv(dsub(c, lo), dsub(hi, lo)), 2097152.0);
+  uint64_t q = (uint64_t)floor(s);
+  return q > 2097151ull ? 2097151ull : q;
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {   // 21 bits -> every third bit
+  x &= 0x1fffffull;
+  x = (x | (x << 32)) & 0x1f00000000ffffull;
+  x = (x | (x << 16)) & 0x1f0000ff0000ffull;
+  x = (x | (x << 8)) & 0x100f00f00f00f00full;
+  x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+  x = (x | (x << 2)) & 0x1249249249249249ull;
+  return x;
+}
+
+__global__ void k_morton(const double* __restrict__ cen, int64_t N, const double* __restrict__ box,
+                         uint64_t* __restrict__ code, int32_t* __restrict__ idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  uint64_t q[3];
+  for (int k = 0; k < 3; ++k) q[k] = quantise(cen[3 * i + k], box[k], box[3 + k]);
+  code[i] = (spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]);
+  idx[i] = (int32_t)i;
+}
+
+__global__ void k_gather_panels(const double* __restrict__ V, const int32_t* __restrict__ T,
+                                const double* __restrict__ cen, const double* __restrict__ area,
+                                const double* __restrict__ hh, const int32_t* __restrict__ perm,
+                                int64_t N, Panel* __restrict__ P, int32_t* __restrict__ iperm) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= N) return;
+  int32_t i = perm[s];
+  Panel p;
+  for (int r = 0; r < 3; ++r) {
+    int32_t vid = T[3 * (int64_t)i + r];
+    p.vid[r] = vid;
+    for (int k = 0; k < 3; ++k) p.v[3 * r + k] = V[3 * (int64_t)vid + k];
+  }
+  for (int k = 0; k < 3; ++k) p.c[k] = cen[3 * (int64_t)i + k];
+  p.area = area[i];
+  p.h = hh[i];
+  p.app = i;
+  P[s] = p;
+  iperm[i] = (int32_t)s;
+}
+
+// ---- cluster tree (level order): node c at level l splits iff |c| > C_leaf ------------
+__global__ void k_split_flags(const int32_t* __restrict__ lo, const int32_t* __restrict__ hi, int64_t b,
+                              int64_t e, int leaf, int32_t* __restrict__ flag) {
+  int64_t c = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= e) return;
+  flag[c - b] = (hi[c] - lo[c]) > leaf ? 1 : 0;
+}
+
+__global__ void k_split_emit(int32_t* __restrict__ lo, int32_t* __restrict__ hi, int32_t* __restrict__ child,
+                             int32_t* __restrict__ depth, int64_t b, int64_t e, const int32_t* __restrict__ flag,
+                             const int32_t* __restrict__ scan, int32_t level) {
+  int64_t c = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= e) return;
+  if (!flag[c - b]) { child[c] = -1; return; }
+  int64_t k = e + 2 * (int64_t)scan[c - b];
+  int32_t l = lo[c], h = hi[c], n = h - l;
+  int32_t mid = l + (n + 1) / 2;          // |tau_1| = ceil(|tau|/2) (A8)
+  child[c] = (int32_t)k;
+  lo[k] = l; hi[k] = mid; lo[k + 1] = mid; hi[k + 1] = h;
+  depth[k] = depth[k + 1] = level + 1;
+}
+
+// boxes bottom-up: leaves from their points, inner nodes from their two children (exact)
+__global__ void k_boxes(const Panel* __restrict__ P, const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
+                        const int32_t* __restrict__ child, int64_t b, int64_t e, double* __restrict__ box,
+                        double* __restrict__ diam2) {
+  int64_t c = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= e) return;
+  double m[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  if (child[c] < 0) {
+    for (int32_t s = lo[c]; s < hi[c]; ++s)
+      for (int k = 0; k < 3; ++k) {
+        double x = P[s].c[k];
+        if (x < m[k]) m[k] = x;
+        if (x > m[3 + k]) m[3 + k] = x;
+      }
+  } else {
+    for (int ch = 0; ch < 2; ++ch) {
+      const double* cb = box + 6 * (int64_t)(child[c] + ch);
+      for (int k = 0; k < 3; ++k) {
+        if (cb[k] < m[k]) m[k] = cb[k];
+        if (cb[3 + k] > m[3 + k]) m[3 + k] = cb[3 + k];
+      }
+    }
+  }
+  for (int k = 0; k < 6; ++k) box[6 * c + k] = m[k];
+  const double dx = dsub(m[3], m[0]), dy = dsub(m[4], m[1]), dz = dsub(m[5], m[2]);
+  diam2[c] = dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
+}
+
+// ---- block cluster tree, one level of Algorithm 1 per launch --------------------------
+// adm(t,s) <=> min(D_t, D_s) <= (eta*eta) * G, G = squared box gap (A5)
+__device__ __forceinline__ bool admissible(const double* bt, const double* bs, double Dt, double Ds, double eta) {
+  double g[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double g1 = dsub(bs[a], bt[3 + a]), g2 = dsub(bt[a], bs[3 + a]);
+    const double m = g1 > g2 ? g1 : g2;
+    g[a] = m > 0.0 ? m : 0.0;
+  }
+  const double G = dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2]));
+  const double Dmin = Dt < Ds ? Dt : Ds;
+  return Dmin <= dmul(dmul(eta, eta), G);
+}
+
+__device__ __forceinline__ int64_t warp_aggregated_add(unsigned long long* ctr, int amount, bool pred) {
+  unsigned mask = __activemask();
+  unsigned take = __ballot_sync(mask, pred);
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(take) - 1;
+  unsigned long long base = 0;
+  int cnt = __popc(take) * amount;
+  if (take && lane == leader) base = atomicAdd(ctr, (unsigned long long)cnt);
+  base = __shfl_sync(mask, base, leader < 0 ? 0 : leader);
+  int rank = __popc(take & ((1u << lane) - 1));
+  return (int64_t)base + (int64_t)rank * amount;
+}
+
+__global__ void k_block_level(const int2* __restrict__ fr, const uint64_t* __restrict__ fkey, int64_t n_in,
+                              int level, const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
+                              const int32_t* __restrict__ child, const double* __restrict__ box,
+                              const double* __restrict__ diam2, double eta, int leaf,
+                              int2* __restrict__ fr_out, uint64_t* __restrict__ fkey_out,
+                              Quad* __restrict__ adm, uint64_t* __restrict__ adm_key,
+                              Quad* __restrict__ dense, uint64_t* __restrict__ dense_key,
+                              unsigned long long* __restrict__ ctr /* [next, adm, dense] */) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool valid = e < n_in;
+  int2 ts = valid ? fr[e] : make_int2(0, 0);
+  uint64_t key = valid ? fkey[e] : 0;
+  int t = ts.x, s = ts.y;
+  bool a = false, split = false;
+  if (valid) {
+    a = admissible(box + 6 * (int64_t)t, box + 6 * (int64_t)s, diam2[t], diam2[s], eta);
+    int nt = hi[t] - lo[t], ns = hi[s] - lo[s];
+    split = !a && nt > leaf && ns > leaf;
+  }
+  int64_t pos = warp_aggregated_add(&ctr[0], 4, valid && split);
+  if (valid && split) {
+    int shift = 64 - 2 * (level + 1);
+    int t0 = child[t], s0 = child[s];
+    for (int c = 0; c < 4; ++c) {
+      fr_out[pos + c] = make_int2(t0 + (c >> 1), s0 + (c & 1));
+      fkey_out[pos + c] = key | ((uint64_t)c << shift);
+    }
+  }
+  int64_t pa = warp_aggregated_add(&ctr[1], 1, valid && !split && a);
+  if (valid && !split && a) {
+    adm[pa] = Quad{lo[t], hi[t], lo[s], hi[s]};
+    adm_key[pa] = key;
+  }
+  int64_t pd = warp_aggregated_add(&ctr[2], 1, valid && !split && !a);
+  if (valid && !split && !a) {
+    dense[pd] = Quad{lo[t], hi[t], lo[s], hi[s]};
+    dense_key[pd] = key;
+  }
+}
+
+__global__ void k_leaf_cost(const Quad* __restrict__ q, int64_t n, int kind, int64_t* __restrict__ cost) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  int64_t m = q[b].rhi - q[b].rlo, nn = q[b].chi - q[b].clo;
+  cost[b] = kind == 1 ? m * nn : (m + nn) * 10;   // A18: dense |t||s|, admissible (|t|+|s|) k_est
+}
+
+template <class F>
+void cub_call(DBuf<char>& tmp, F&& f) {
+  size_t bytes = 0;
+  HM_CUDA(f(nullptr, bytes));
+  tmp.alloc(bytes);
+  HM_CUDA(f(tmp.get(), bytes));
+}
+
+void grow_copy(DBuf<Quad>& q, DBuf<uint64_t>& k, int64_t used, int64_t need, cudaStream_t st) {
+  if ((int64_t)q.n >= need) return;
+  int64_t cap = std::max<int64_t>(need, 2 * (int64_t)q.n);
+  Quad* nq = nullptr;
+  uint64_t* nk = nullptr;
+  HM_CUDA(cudaMalloc(&nq, cap * sizeof(Quad) + 16));
+  HM_CUDA(cudaMalloc(&nk, cap * sizeof(uint64_t) + 16));
+  if (used > 0) {
+    HM_CUDA(cudaMemcpyAsync(nq, q.p, used * sizeof(Quad), cudaMemcpyDeviceToDevice, st));
+    HM_CUDA(cudaMemcpyAsync(nk, k.p, used * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+  }
+  HM_CUDA(cudaStreamSynchronize(st));
+  q.release(); k.release();
+  q.p = nq; q.n = cap; k.p = nk; k.n = cap;
+}
+
+void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_t& begin, int64_t& end,
+                    DBuf<char>& tmp) {
+  if (C.world == 1 || n == 0) { begin = 0; end = n; return; }
+  DBuf<int64_t> cost, pref;
+  cost.alloc(n); pref.alloc(n);
+  k_leaf_cost<<<grid_for(n, 256), 256, 0, C.stream>>>(q.get(), n, kind, cost.get());
+  HM_CHECK_LAUNCH();
+  cub_call(tmp, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, cost.get(), pref.get(), n, C.stream);
+  });
+  std::vector<int64_t> hp(n), hc(1);
+  HM_CUDA(cudaMemcpyAsync(hp.data(), pref.get(), n * sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
+  HM_CUDA(cudaMemcpyAsync(hc.data(), cost.get() + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
+  HM_CUDA(cudaStreamSynchronize(C.stream));
+  const int64_t total = hp[n - 1] + hc[0];
+  auto first_at = [&](int r) -> int64_t {   // first leaf whose exclusive prefix >= floor(rC/p)
+    if (r >= C.world) return n;
+    int64_t bound = (int64_t)(((__int128)r * total) / C.world);
+    return std::lower_bound(hp.begin(), hp.end(), bound) - hp.begin();
+  };
+  begin = C.rank == 0 ? 0 : first_at(C.rank);
+  end = C.rank + 1 >= C.world ? n : first_at(C.rank + 1);
+}
+
+}  // namespace
+
+void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
+  cudaStream_t st = C.stream;
+  const int64_t N = mesh.n_triangles, nv = mesh.n_vertices;
+  C.have_tree = C.have_setup = false;
+  C.N = N; C.nv = nv; C.leaf_size = leaf_size; C.eta = eta;
+  upload_quadrature_tables();
+  // ---- a1: mesh upload + panel geometry
+  C.vert.alloc_exact(nv * 3);
+  C.tri.alloc_exact(N * 3);
+  cudaMemcpyKind kind = mesh.memory ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  HM_CUDA(cudaMemcpyAsync(C.vert.get(), mesh.vertices, nv * 3 * sizeof(double), kind, st));
+  HM_CUDA(cudaMemcpyAsync(C.tri.get(), mesh.triangles, N * 3 * sizeof(int32_t), kind, st));
+  DBuf<double> cen, area, hh;
+  cen.alloc(N * 3); area.alloc(N); hh.alloc(N);
+  DBuf<unsigned int> bad;
+  bad.alloc(1);
+  HM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned int), st));
+  k_geometry<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), N, nv, cen.get(), area.get(),
+                                                 hh.get(), bad.get());
+  HM_CHECK_LAUNCH();
+  unsigned int hbad = 0;
+  HM_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+  // ---- a2: Morton codes + stable sort
+  const int nb = 148;
+  DBuf<double> part, gbox;
+  part.alloc(6 * nb); gbox.alloc(6);
+  k_minmax<<<nb, 256, 0, st>>>(cen.get(), N, part.get());
+  k_minmax_final<<<1, 32, 0, st>>>(part.get(), nb, gbox.get());
+  HM_CHECK_LAUNCH();
+  HM_CUDA(cudaStreamSynchronize(st));
+  if (hbad & 1u) fail(HM_ERR_ARG, "hm_build_tree: a triangle references a vertex id out of range");
+  if (hbad & 2u) fail(HM_ERR_ARG, "hm_build_tree: a triangle has zero area (degenerate)");
+  DBuf<uint64_t> code_sorted;
+  DBuf<int32_t> idx;
+  C.codes_app.alloc_exact(N);
+  code_sorted.alloc(N); idx.alloc(N);
+  C.perm.alloc_exact(N); C.iperm.alloc_exact(N);
+  k_morton<<<grid_for(N, 256), 256, 0, st>>>(cen.get(), N, gbox.get(), C.codes_app.get(), idx.get());
+  HM_CHECK_LAUNCH();
+  DBuf<char> tmp;
+  cub_call(tmp, [&](void* t, size_t& b) {   // LSD radix sort: stable, ties keep ascending index (A7)
+    return cub::DeviceRadixSort::SortPairs(t, b, C.codes_app.get(), code_sorted.get(), idx.get(),
+                                           C.perm.get(), (int)N, 0, 63, st);
+  });
+  C.panel.alloc_exact(N);
+  k_gather_panels<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), cen.get(), area.get(), hh.get(),
+                                                     C.perm.get(), N, C.panel.get(), C.iperm.get());
+  HM_CHECK_LAUNCH();
+  // ---- a3: cluster tree, level order
+  int64_t leaf_min = std::max<int64_t>(1, (leaf_size + 1) / 2);
+  int64_t cap = 2 * (N / leaf_min + 2) + 4;
+  C.cl_lo.alloc_exact(cap); C.cl_hi.alloc_exact(cap); C.cl_child.alloc_exact(cap); C.cl_depth.alloc_exact(cap);
+  int32_t root[2] = {0, (int32_t)N}, zero = 0;
+  HM_CUDA(cudaMemcpyAsync(C.cl_lo.get(), &root[0], sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  HM_CUDA(cudaMemcpyAsync(C.cl_hi.get(), &root[1], sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  HM_CUDA(cudaMemcpyAsync(C.cl_depth.get(), &zero, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  std::vector<int64_t> lev = {0, 1};
+  DBuf<int32_t> flag, scan;
+  flag.alloc(cap); scan.alloc(cap);
+  for (int level = 0;; ++level) {
+    int64_t b = lev[level], e = lev[level + 1], n = e - b;
+    k_split_flags<<<grid_for(n, 256), 256, 0, st>>>(C.cl_lo.get(), C.cl_hi.get(), b, e, leaf_size, flag.get());
+    HM_CHECK_LAUNCH();
+    cub_call(tmp, [&](void* t, size_t& bytes) {
+      return cub::DeviceScan::ExclusiveSum(t, bytes, flag.get(), scan.get(), (int)n, st);
+    });
+    k_split_emit<<<grid_for(n, 256), 256, 0, st>>>(C.cl_lo.get(), C.cl_hi.get(), C.cl_child.get(),
+                                                    C.cl_depth.get(), b, e, flag.get(), scan.get(), level);
+    HM_CHECK_LAUNCH();
+    int32_t hs[2];
+    HM_CUDA(cudaMemcpyAsync(&hs[0], scan.get() + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaMemcpyAsync(&hs[1], flag.get() + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaStreamSynchronize(st));
+    int64_t nsplit = hs[0] + hs[1];
+    if (nsplit == 0) break;
+    if (e + 2 * nsplit > cap) fail(HM_ERR_CUDA, "cluster tree capacity exceeded");
+    lev.push_back(e + 2 * nsplit);
+  }
+  C.ncl = lev.back();
+  int nlev = (int)lev.size() - 1;
+  C.cl_box.alloc_exact(6 * C.ncl); C.cl_diam2.alloc_exact(C.ncl);
+  for (int level = nlev - 1; level >= 0; --level) {
+    int64_t b = lev[level], e = lev[level + 1];
+    k_boxes<<<grid_for(e - b, 128), 128, 0, st>>>(C.panel.get(), C.cl_lo.get(), C.cl_hi.get(), C.cl_child.get(),
+                                                   b, e, C.cl_box.get(), C.cl_diam2.get());
+    HM_CHECK_LAUNCH();
+  }
+  // ---- a4: block cluster tree, level-wise
+  DBuf<int2> fr[2];
+  DBuf<uint64_t> fk[2];
+  fr[0].alloc(1024); fk[0].alloc(1024);
+  int2 r2 = make_int2(0, 0);
+  uint64_t k0 = 0;
+  HM_CUDA(cudaMemcpyAsync(fr[0].get(), &r2, sizeof(int2), cudaMemcpyHostToDevice, st));
+  HM_CUDA(cudaMemcpyAsync(fk[0].get(), &k0, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  DBuf<Quad> admq, denq;
+  DBuf<uint64_t> admk, denk;
+  DBuf<unsigned long long> ctr;
+  ctr.alloc(3);
+  int64_t n_in = 1, nadm = 0, nden = 0;
+  int cur = 0;
+  for (int level = 0; n_in > 0; ++level) {
+    fr[1 - cur].alloc(4 * n_in); fk[1 - cur].alloc(4 * n_in);
+    grow_copy(admq, admk, nadm, nadm + n_in, st);
+    grow_copy(denq, denk, nden, nden + n_in, st);
+    unsigned long long hc[3] = {0, (unsigned long long)nadm, (unsigned long long)nden};
+    HM_CUDA(cudaMemcpyAsync(ctr.get(), hc, sizeof(hc), cudaMemcpyHostToDevice, st));
+    k_block_level<<<grid_for(n_in, 256), 256, 0, st>>>(
+        fr[cur].get(), fk[cur].get(), n_in, level, C.cl_lo.get(), C.cl_hi.get(), C.cl_child.get(), C.cl_box.get(),
+        C.cl_diam2.get(), eta, leaf_size, fr[1 - cur].get(), fk[1 - cur].get(), admq.get(), admk.get(),
+        denq.get(), denk.get(), ctr.get());
+    HM_CHECK_LAUNCH();
+    HM_CUDA(cudaMemcpyAsync(hc, ctr.get(), sizeof(hc), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaStreamSynchronize(st));
+    n_in = (int64_t)hc[0]; nadm = (int64_t)hc[1]; nden = (int64_t)hc[2];
+    cur = 1 - cur;
+    if (level > 62) fail(HM_ERR_ARG, "block tree deeper than 31 levels");
+  }
+  // canonical DFS order = ascending left-aligned path key (A10)
+  C.nadm = nadm; C.ndense = nden;
+  C.adm.alloc_exact(nadm); C.dense.alloc_exact(nden);
+  DBuf<uint64_t> ksorted;
+  ksorted.alloc(std::max(nadm, nden));
+  if (nadm)
+    cub_call(tmp, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, admk.get(), ksorted.get(), admq.get(), C.adm.get(), (int)nadm,
+                                             0, 64, st);
+    });
+  if (nden)
+    cub_call(tmp, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, denk.get(), ksorted.get(), denq.get(), C.dense.get(), (int)nden,
+                                             0, 64, st);
+    });
+  // ---- leaf partition over ranks (A18)
+  partition_list(C, C.adm, nadm, 0, C.adm_begin, C.adm_end, tmp);
+  partition_list(C, C.dense, nden, 1, C.dense_begin, C.dense_end, tmp);
+  HM_CUDA(cudaStreamSynchronize(st));
+  C.h_adm.clear(); C.h_dense.clear();
+  C.have_tree = true;
+}
+
+}  // namespace hm

@@ -1,0 +1,222 @@
+"""GPU-vs-oracle parity of the whole hot path, through the C ABI (libhm.so).
+
+Bars: tree, Morton codes, perm and leaf lists bit-exact; regular entries
+bit-exact, singular entries <= 1e-14 relative; ACA ranks and pivot sequences identical on
+>= 99.9% of blocks; H-matvec <= 10*eps_aca against the oracle's exact Galerkin product and
+<= 1e-12 against the oracle's own H-matvec; solutions <= 1e-5 relative to the oracle's.
+"""
+import numpy as np
+import pytest
+
+from inputs.meshes import geodesic, icosphere, lobed, seeded_vector
+
+pytestmark = pytest.mark.gpu
+
+EPS = 1e-6
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return torch
+
+
+def _gpu(V, T, leaf=32, eta=1.0):
+    from paper_1806_11558_b200 import HMatrix
+    H = HMatrix(device=0)
+    H.build_tree(V, T, leaf_size=leaf, eta=eta)
+    return H
+
+
+def _compare_tree(O, H, V, T, leaf=32, eta=1.0):
+    R = O.Problem(V, T, leaf_size=leaf, eta=eta)
+    assert np.array_equal(H.codes(), R.codes())
+    assert np.array_equal(H.perm(), R.perm())
+    for kind in (0, 1):
+        assert np.array_equal(H.leaves(kind)[0], R.leaves(kind)), f"leaf list {kind}"
+    cg, cr = H.clusters(), R.clusters()
+    kg = sorted(zip(cg["lo"], cg["hi"], map(tuple, cg["bbox"])))
+    kr = sorted(zip(cr["lo"], cr["hi"], map(tuple, cr["bbox"])))
+    assert kg == kr
+    return R
+
+
+@pytest.mark.parametrize("mesh", ["ico2", "ico3", "ico5", "geo8", "geo33", "lobed20", "ico5_leaf7", "ico4_eta0"])
+def test_tree_bit_exact(O, torch_cuda, mesh):
+    V, T = {"ico2": lambda: icosphere(2), "ico3": lambda: icosphere(3), "ico5": lambda: icosphere(5),
+            "geo8": lambda: geodesic(8), "geo33": lambda: geodesic(33), "lobed20": lambda: lobed(20),
+            "ico5_leaf7": lambda: icosphere(5), "ico4_eta0": lambda: icosphere(4)}[mesh]()
+    leaf = 7 if mesh.endswith("leaf7") else 32
+    eta = 0.0 if mesh.endswith("eta0") else 1.0
+    H = _gpu(V, T, leaf, eta)
+    _compare_tree(O, H, V, T, leaf, eta)
+
+
+def test_tree_bit_exact_full_sizes(O, torch_cuda):
+    # BASELINE configs[2] (327,680) and configs[3] (1,568,000): the bench's trees
+    for V, T in (icosphere(7), geodesic(280)):
+        H = _gpu(V, T)
+        R = O.Problem(V, T)
+        assert np.array_equal(H.perm(), R.perm())
+        for kind in (0, 1):
+            assert np.array_equal(H.leaves(kind)[0], R.leaves(kind))
+        H.close()
+
+
+def test_quadrature_tables_equal(O):
+    from paper_1806_11558_b200 import hm
+    for n in range(1, 9):
+        xg, wg = hm.hm_quadrature_table(n)
+        xo, wo = O.gauss_legendre01(n)
+        assert np.array_equal(xg, xo) and np.array_equal(wg, wo)
+
+
+def test_entries_all_classes(O, torch_cuda):
+    V, T = icosphere(4)
+    N = T.shape[0]
+    H = _gpu(V, T)
+    R = O.Problem(V, T)
+    rng = np.random.default_rng(1)
+    pairs = [rng.integers(0, N, size=2) for _ in range(4000)]
+    # every touching neighbour of 40 panels (identical, edge, vertex) + near regular pairs
+    c, _, _ = R.geometry()
+    for i in rng.integers(0, N, size=40):
+        ti = set(T[i])
+        near = np.argsort(np.linalg.norm(c - c[i], axis=1))[:40]
+        for j in near:
+            pairs.append((i, j))
+            pairs.append((j, i))
+    pairs = np.array(pairs, dtype=np.int64)
+    g = H.entries(pairs)
+    o = R.entries(pairs)
+    cls = np.array([R.entry_class(i, j) for i, j in pairs])
+    reg = cls >= 3
+    assert np.array_equal(g[reg], o[reg]), "regular entries must be bit-identical (A15)"
+    rel = np.abs(g[~reg] - o[~reg]) / np.abs(o[~reg])
+    assert (~reg).sum() > 100 and rel.max() <= 1e-14
+    assert set(cls) == {0, 1, 2, 3, 4, 5, 6}
+
+
+@pytest.fixture(scope="module")
+def c1(O, torch_cuda):
+    V, T = icosphere(3)
+    H = _gpu(V, T)
+    H.setup(EPS)
+    R = O.Problem(V, T)
+    R.assemble(EPS)
+    return V, T, H, R, R.dense()
+
+
+def _check_blocks(H, R, tol_pivots=0.999):
+    adm, _ = H.leaves(0)
+    dense, _ = H.leaves(1)
+    same = 0
+    for b, q in enumerate(dense):
+        Bg = H.dense_block(b, (q[1] - q[0], q[3] - q[2]))
+        Bo = R.dense_block(b)
+        ok = np.abs(Bg - Bo) <= 1e-14 * np.abs(Bo)
+        assert ok.all(), f"dense block {b}"
+    for b, q in enumerate(adm):
+        m, n = q[1] - q[0], q[3] - q[2]
+        U, W, pv = H.lowrank(b, m, n, pivots=True)
+        if U.shape[1] == R.rank(b) and np.array_equal(pv, R.pivots(b)):
+            same += 1
+            Uo, Wo = R.factors(b)
+            np.testing.assert_allclose(U @ W.T, Uo @ Wo.T, rtol=0, atol=1e-12 * np.abs(Uo @ Wo.T).max())
+    assert same >= tol_pivots * len(adm), f"identical pivots on {same}/{len(adm)} blocks"
+
+
+def test_c1_blocks_pivots_and_matvec(c1):
+    V, T, H, R, A = c1
+    _check_blocks(H, R)
+    import torch
+    N = T.shape[0]
+    xs = [np.ones(N), R.rhs(1)] + [seeded_vector(N, s) for s in range(5)]
+    for x in xs:
+        yg = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        ye = A @ x
+        assert np.linalg.norm(yg - ye) <= 10 * EPS * np.linalg.norm(ye)
+        yo = R.matvec(x)
+        assert np.linalg.norm(yg - yo) <= 1e-12 * np.linalg.norm(yo)
+    # host-pointer path of the same ABI call
+    yh = H.matvec(xs[2].copy())
+    assert np.linalg.norm(yh - R.matvec(xs[2])) <= 1e-12 * np.linalg.norm(yh)
+
+
+@pytest.mark.parametrize("solver", [0, 1])
+def test_c1_solve_vs_oracle(c1, solver):
+    V, T, H, R, A = c1
+    import torch
+    H.set_option("solver", solver)
+    for kind in (0, 1):
+        f = R.rhs(kind)
+        fg = H.assemble_rhs(kind)
+        assert np.abs(fg - f).max() <= 1e-15 * np.abs(f).max()
+        sol, it, rr = H.solve(torch.from_numpy(f).cuda(), tol=1e-10)
+        sol = sol.cpu().numpy()
+        xo = (R.gmres(f, tol=1e-10) if solver == 0 else R.cg(f, tol=1e-10))[0]
+        assert np.linalg.norm(sol - xo) <= 1e-5 * np.linalg.norm(xo)
+        assert rr <= 1e-9
+        xd = np.linalg.solve(A, f)
+        assert np.linalg.norm(sol - xd) <= 1e-5 * np.linalg.norm(xd)
+        if kind == 0:
+            assert abs(sol.mean() - 1.0) < 1e-2              # V u = 1 on the unit sphere
+    H.set_option("solver", 0)
+
+
+@pytest.fixture(scope="module")
+def c2(O, torch_cuda):
+    V, T = icosphere(5)
+    H = _gpu(V, T)
+    H.setup(EPS)
+    R = O.Problem(V, T)
+    R.assemble(EPS)
+    return V, T, H, R
+
+
+def test_c2_blocks_and_pivots(c2):
+    V, T, H, R = c2
+    _check_blocks(H, R)
+
+
+def test_c2_matvec_vs_exact_rows_and_oracle(c2):
+    V, T, H, R = c2
+    import torch
+    N = T.shape[0]
+    rows = np.random.default_rng(7).permutation(N)[:256]
+    Arows = R.dense_rows(rows)
+    for x in [np.ones(N), R.rhs(1), seeded_vector(N, 0), seeded_vector(N, 1)]:
+        yg = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        ye = Arows @ x
+        assert np.linalg.norm(yg[rows] - ye) <= 10 * EPS * np.linalg.norm(ye)
+        yo = R.matvec(x)
+        assert np.linalg.norm(yg - yo) <= 1e-12 * np.linalg.norm(yo)
+
+
+def test_c2_solve_vs_oracle(c2):
+    V, T, H, R = c2
+    import torch
+    f = R.rhs(1)
+    sol, it, rr = H.solve(torch.from_numpy(f).cuda(), tol=1e-10)
+    xo = R.gmres(f, tol=1e-10)[0]
+    assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-5 * np.linalg.norm(xo)
+
+
+def test_c3_full_size_sampled_rows(O, torch_cuda):
+    # configs[2] at full size, in the launch configuration bench.py times
+    import torch
+    V, T = icosphere(7)
+    N = T.shape[0]
+    H = _gpu(V, T)
+    H.setup(EPS)
+    R = O.Problem(V, T)
+    rows = np.random.default_rng(7).permutation(N)[:48]
+    Arows = R.dense_rows(rows)
+    for x in [np.ones(N), seeded_vector(N, 0)]:
+        yg = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        ye = Arows @ x
+        assert np.linalg.norm(yg[rows] - ye) <= 10 * EPS * np.linalg.norm(ye)
+    st = H.stats()
+    assert st["aca_overflow"] == 0 or st["k_max_seen"] <= 64
+    H.close()
