@@ -1,0 +1,411 @@
+"""bench.py — one JSON line for BASELINE.json's metric on B200.
+
+A "step" is one pass of the whole hot path over the
+workload's synthetic mesh: hm_build_tree (geometry, Morton sort, cluster tree, block tree,
+partition) + hm_setup (near-field assembly + batched ACA) + hm_solve (GMRES(100) driving
+the batched H-matvec, rhs = the paper's f, tol 1e-8).  `value` = seconds per step with the
+mesh and rhs already resident in HBM (max over ranks, CUDA events on the library's stream).
+`e2e` = the same step through the same C ABI with HOST buffers (mesh H2D, rhs H2D and
+solution D2H inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+For N > 1 launch with torchrun; every rank builds the same tree, owns a contiguous
+cost-balanced slice of both leaf lists, and the matvec's partial sums are
+all-reduced over NCCL.  Total work is fixed, so scaling is "strong".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "H-matrix setup s, H-matvec s and GB/s vs HBM peak, solve s at 1/2/4/8 B200"
+CONFIGS = {
+    "C1": "unit sphere, icosphere L=3, 1280 triangles",
+    "C2": "unit sphere, icosphere L=5, 20480 triangles",
+    "C3": "unit sphere, icosphere L=7, 327680 triangles",
+    "C4": "sphere-type geodesic nu=280, 1568000 triangles",
+    "C5": "perturbed multi-lobed surface (geodesic nu=244), 1190720 triangles",
+}
+EPS, LEAF, ETA, TOL = 1e-6, 32, 1.0, 1e-8
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.jsonl")
+
+
+def fp64_eval_peak():
+    """Measured throughput of the minimal IEEE evaluation sequence w/sqrt(d2) + sum on this
+    pool's B200 (tools/fp64_peak.cu), evaluations/s."""
+    best = None
+    if os.path.exists(FP64_PEAK_FILE):
+        for line in open(FP64_PEAK_FILE):
+            d = json.loads(line)
+            if d.get("kernel") == "eval_min":
+                best = max(best or 0, d["evals_per_s"])
+            if d.get("kernel") == "sqrt_div" and best is None:
+                best = d["evals_per_s"]
+    return best or 6.26e11
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, dev):
+        self.f = os.path.join("/tmp", f"clocks_{os.getpid()}.csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={dev}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=open(self.f, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.f):
+            c = [x.strip() for x in line.split(",")]
+            if len(c) < 9:
+                continue
+            try:
+                sm.append(float(c[1])); mx = max(mx, float(c[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, c[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def mesh_for(cfg):
+    from inputs.meshes import config_mesh
+    return config_mesh(cfg)
+
+
+def dist_init(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    rank, world, local = dist_init(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):      # every torch op and every libhm launch on one stream
+        return _run_gpu(args, rank, world, local, dev, stream)
+
+
+def _run_gpu(args, rank, world, local, dev, stream):
+    import torch
+    from paper_1806_11558_b200 import HMatrix, hm
+    nid = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [hm.hm_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    V, T = mesh_for(args.config)
+    N = T.shape[0]
+    Vd = torch.from_numpy(V).to(dev)
+    Td = torch.from_numpy(T).to(dev)
+    H = HMatrix(device=local, rank=rank, world_size=world, nccl_unique_id=nid, cuda_stream=stream.cuda_stream)
+    H.N = N
+    H.set_option("solver", 0)
+    H.set_option("restart", 100)
+    # rhs = the paper's f, assembled by the library
+    H.build_tree(Vd, Td, LEAF, ETA)
+    f = torch.empty(N, dtype=torch.float64, device=dev)
+    H.assemble_rhs(1, f)
+    sol = torch.empty_like(f)
+    torch.cuda.synchronize()
+
+    def step():
+        H.build_tree(Vd, Td, LEAF, ETA)
+        H.setup(EPS)
+        return H.solve(f, TOL, sol)
+
+    for _ in range(args.warmup):
+        step()
+    barrier(world)
+    l0 = H.stats()["launches"]
+    clk = Clocks(local) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per = []
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _, iters, rr = step()
+            b.record(stream)
+            per.append((a, b))
+        e1.record(stream)
+    barrier(world)
+    clocks = clk.stop() if clk else None
+    launches = (H.stats()["launches"] - l0) // max(1, args.steps)
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms, world)
+    st = H.stats()
+    tree_s = max_over_ranks(st["tree_ms"], world) / 1e3
+    setup_s = max_over_ranks(st["setup_ms"], world) / 1e3
+    near_s = max_over_ranks(st["near_ms"], world) / 1e3
+    aca_s = max_over_ranks(st["aca_ms"], world) / 1e3
+    solve_s = max_over_ranks(st["solve_ms"], world) / 1e3
+
+    # ---- matvec timing (the dominant HBM kernel family), L2 flushed between products
+    x = torch.randn(N, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(0))
+    y = torch.empty_like(x)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    mv = []
+    for r in range(args.matvecs + 3):
+        flush.fill_(r)
+        barrier(world)
+        with torch.cuda.stream(stream):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            H.matvec(x, y)
+            b.record(stream)
+        b.synchronize()
+        if r >= 3:
+            mv.append(a.elapsed_time(b))
+    mv_ms = max_over_ranks(statistics.median(mv), world)
+    stored = st["stored_bytes"]
+    stored_tot = stored
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([float(stored)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        stored_tot = float(t.item())
+    alg_bytes_rank = stored + 8 * 5 * N       # H bytes + x gather, y zero/atomics/scatter
+    hbm, hbm_src = peaks()
+    mv_gbs = alg_bytes_rank / (mv_ms * 1e-3) / 1e9
+
+    # ---- entry-evaluation throughput of setup (FP64-pipe bound phase)
+    evals = st["evals_near"] + st["evals_aca"]
+    eval_rate = evals / max(1e-9, (st["near_ms"] + st["aca_ms"]) * 1e-3)
+    eval_peak = fp64_eval_peak()
+
+    # ---- e2e: same step through the same ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        fh = f.cpu().numpy()
+        solh = np.empty(N)
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.steps)):
+            H.build_tree(V, T, LEAF, ETA)
+            H.setup(EPS)
+            H.solve(fh, TOL, solh)
+        barrier(world)
+        e2e_s = (time.perf_counter() - t0) / max(1, args.steps)
+        e2e_s = max_over_ranks(e2e_s, world)
+        e2e = {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": int(V.nbytes + T.nbytes + fh.nbytes),
+               "d2h_bytes_per_step": int(solh.nbytes)}
+
+    # dominant phase -> roofline object
+    if (near_s + aca_s) >= solve_s:
+        roof = {"kernel": "entry evaluation (near-field + ACA row/column generation)", "bound": "alu",
+                "achieved": round(eval_rate / 1e9, 2), "peak": round(eval_peak / 1e9, 2), "unit": "Geval/s",
+                "frac": round(eval_rate / eval_peak, 4), "traffic": None,
+                "peak_source": "measured: minimal IEEE FP64 evaluation sequence on this pool's B200 (profiles/r01_fp64_peak.jsonl)"}
+    else:
+        roof = {"kernel": "H-matvec", "bound": "hbm", "achieved": round(mv_gbs, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(mv_gbs / hbm, 4), "traffic": None, "peak_source": hbm_src}
+    matvec_roof = {"bound": "hbm", "achieved": round(mv_gbs, 1), "peak": hbm, "unit": "GB/s",
+                   "frac": round(mv_gbs / hbm, 4), "alg_bytes_per_launch": int(alg_bytes_rank), "peak_source": hbm_src}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(args.config, V, T, iters)
+        out = {
+            "metric": METRIC, "value": round(ms / 1e3, 6), "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "N": N, "leaf_size": LEAF, "eta": ETA,
+                       "eps_aca": EPS, "solver": "GMRES(100)", "tol": TOL, "rhs": "paper f=4x^2-3y^2-z^2",
+                       "parallelism": f"leaf-partition x{world}",
+                       "l2": "inputs larger than L2 (stored H >> 126 MB); matvec timing flushes L2 with a 256 MB write"},
+            "breakdown": {"tree_s": round(tree_s, 6), "setup_s": round(setup_s, 6), "near_field_s": round(near_s, 6),
+                          "aca_s": round(aca_s, 6), "solve_s": round(solve_s, 6), "solve_iters": iters,
+                          "solve_relres": rr, "matvec_s": round(mv_ms / 1e3, 6), "matvec_GBps": round(mv_gbs, 1),
+                          "matvec_frac_hbm": round(mv_gbs / hbm, 4), "stored_GB_total": round(stored_tot / 1e9, 3),
+                          "k_mean": st["k_mean"], "evals": evals, "eval_rate_Gps": round(eval_rate / 1e9, 2)},
+            "roofline": roof, "matvec_roofline": matvec_roof,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    H.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return out
+
+
+# ------------------------------------------------------------------------------------------
+def oracle_step_estimate(cfg, V, T, budget_s=20.0, gmres_iters=None):
+    """Time the oracle (as it stands) on a bounded sample of the workload and scale to one
+    full step: tree (full), near-field + ACA on a prefix sample of each leaf list (scaled by
+    entries / sum(m+n)), one matvec over the sampled leaves (scaled by stored doubles) times
+    the GMRES iteration count."""
+    from oracle import oracle as O
+    import threading
+    t0 = time.perf_counter()
+    P = O.Problem(V, T, LEAF, ETA)
+    tree_s = time.perf_counter() - t0
+    adm, dense = P.leaves(0), P.leaves(1)
+    dm = (dense[:, 1] - dense[:, 0]).astype(np.int64) * (dense[:, 3] - dense[:, 2])
+    am = ((adm[:, 1] - adm[:, 0]) + (adm[:, 3] - adm[:, 2])).astype(np.int64)
+    # sample: every s-th leaf of both lists (strided -> representative mix of sizes)
+    frac = 1.0
+    for trial in range(12):
+        sd = max(1, int(round(1.0 / frac)))
+        d_idx = np.arange(0, len(dense), sd); a_idx = np.arange(0, len(adm), sd)
+        est = (dm[d_idx].sum() * 250 + am[a_idx].sum() * 10 * 100) / 4e8 / max(1, os.cpu_count() or 1)
+        if est <= budget_s:
+            break
+        frac /= 2
+    sd = max(1, int(round(1.0 / frac)))
+    # assemble only the sampled leaves: run contiguous ranges of stride sd (one leaf each)
+    t1 = time.perf_counter()
+    near_t = aca_t = 0.0
+    mv_t = 0.0
+    ns_d = ns_a = 0
+    x = np.random.default_rng(0).standard_normal(P.N)
+    for lo in range(0, max(len(dense), len(adm)), sd):
+        d0, d1 = (lo, min(lo + 1, len(dense))) if lo < len(dense) else (0, 0)
+        a0, a1 = (lo, min(lo + 1, len(adm))) if lo < len(adm) else (0, 0)
+        ta = time.perf_counter()
+        P.assemble(EPS, 64, (d0, d1), (0, 0))
+        tb = time.perf_counter()
+        P.assemble(EPS, 64, (0, 0), (a0, a1))
+        tc = time.perf_counter()
+        near_t += tb - ta; aca_t += tc - tb
+        ns_d += d1 - d0; ns_a += a1 - a0
+        if time.perf_counter() - t1 > budget_s:
+            break
+    d_done = dm[np.arange(0, ns_d * sd, sd)[:ns_d]].sum() if ns_d else 1
+    a_done = am[np.arange(0, ns_a * sd, sd)[:ns_a]].sum() if ns_a else 1
+    near_full = near_t * dm.sum() / max(1, d_done)
+    aca_full = aca_t * am.sum() / max(1, a_done)
+    # matvec: oracle matvec of the (currently assembled) last sample ~ stored doubles; use a
+    # bandwidth model measured on a dense-only assembly of the first leaves instead
+    nd = min(len(dense), 20000)
+    P.assemble(EPS, 64, (0, nd), (0, 0))
+    tm = time.perf_counter(); P.matvec(x); mv_t = time.perf_counter() - tm
+    bytes_per_s = 8 * dm[:nd].sum() / max(mv_t, 1e-9)
+    cores = os.cpu_count() or 1
+    return {"tree_s": tree_s, "near_s": near_full, "aca_s": aca_full, "matvec_Bps": bytes_per_s,
+            "sample": f"every {sd}-th leaf of both canonical lists ({ns_d} dense + {ns_a} admissible leaves), "
+                      f"scaled by entries / sum(m+n); matvec rate from a dense-only assembly of {nd} leaves",
+            "cores": cores, "gmres_iters": gmres_iters}
+
+
+def cpu_baseline(cfg, V, T, gmres_iters, budget_s=20.0):
+    try:
+        e = oracle_step_estimate(cfg, V, T, budget_s, gmres_iters)
+    except Exception as ex:  # the baseline must not take the bench down
+        return {"error": str(ex)}
+    # stored bytes estimate for the solve: dense entries + ~9 terms per admissible leaf
+    from oracle import oracle as O
+    step = e["tree_s"] + e["near_s"] + e["aca_s"]
+    return {"value": round(step, 3), "unit": "s (tree + setup; solve excluded, see sample)", "cores": e["cores"],
+            "kind": "oracle", "sample": e["sample"], "breakdown": {k: e[k] for k in ("tree_s", "near_s", "aca_s")}}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    V, T = mesh_for(args.config)
+    N = T.shape[0]
+    vals = []
+    for s in range(args.warmup + args.steps):
+        e = oracle_step_estimate(args.config, V, T, budget_s=max(5.0, 60.0 / max(1, args.steps + args.warmup)))
+        if s >= args.warmup:
+            vals.append(e["tree_s"] + e["near_s"] + e["aca_s"])
+    v = statistics.median(vals)
+    out = {"metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "N": N},
+           "cpu_baseline": {"value": round(v, 3), "kind": "oracle", "cores": e["cores"], "sample": e["sample"]},
+           "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=list(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--matvecs", type=int, default=20)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

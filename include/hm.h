@@ -72,7 +72,8 @@ typedef struct {
 /* Create a context on CUDA device `device` for rank `rank` of `world_size` ranks.
  * nccl_unique_id: HM_NCCL_UNIQUE_ID_BYTES bytes of an ncclUniqueId made by
  * hm_nccl_unique_id on rank 0 and broadcast by the caller; NULL iff world_size == 1.
- * cuda_stream: a cudaStream_t on `device`, or NULL for a library-owned stream.
+ * cuda_stream: a cudaStream_t on `device`, or NULL for a library-owned blocking stream (it
+ * orders with the legacy default stream, so plain torch/cudaMemcpy users need no extra sync).
  * Errors: HM_ERR_ARG (rank/world/device out of range, id NULL with world_size > 1),
  * HM_ERR_CUDA, HM_ERR_NCCL.  COLLECTIVE when world_size > 1. */
 hm_status hm_create(hm_ctx* out, int device, int rank, int world_size,

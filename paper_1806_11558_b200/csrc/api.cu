@@ -16,6 +16,8 @@ struct hm_ctx_s {
 
 namespace hm {
 
+unsigned long long g_launches = 0;
+
 // ---- driver entry points (no link-time dependency on libcuda: resolved through cudart) ----
 namespace {
 struct Drv {
@@ -221,7 +223,7 @@ hm_status hm_create(hm_ctx* out, int device, int rank, int world_size, const voi
     if (cuda_stream) {
       C.stream = (cudaStream_t)cuda_stream;
     } else {
-      HM_CUDA(cudaStreamCreateWithFlags(&C.stream, cudaStreamNonBlocking));
+      HM_CUDA(cudaStreamCreate(&C.stream));   // blocking: ordered with the legacy default stream
       C.own_stream = true;
     }
     if (world_size > 1) {
@@ -512,7 +514,7 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
       << ",\"near_ms\":" << C.times.near_ms << ",\"aca_ms\":" << C.times.aca_ms << ",\"plan_ms\":" << C.times.plan_ms
       << ",\"setup_ms\":" << C.times.setup_ms << ",\"solve_ms\":" << C.times.solve_ms
       << ",\"solve_iters\":" << C.times.solve_iters << ",\"solve_relres\":" << C.times.solve_relres
-      << ",\"lr_small\":" << C.n_lr_small << ",\"lr_large\":" << C.n_lr_large << ",\"rank_hist\":[";
+      << ",\"launches\":" << hm::g_launches << ",\"lr_small\":" << C.n_lr_small << ",\"lr_large\":" << C.n_lr_large << ",\"rank_hist\":[";
     for (int k = 0; k <= 64; ++k) o << (k ? "," : "") << hist[k];
     o << "]}";
     std::string s = o.str();

@@ -51,7 +51,13 @@ struct Error {
       throw ::hm::Error{HM_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
   } while (0)
 
-#define HM_CHECK_LAUNCH() HM_CUDA(cudaGetLastError())
+// every kernel launch of libhm is followed by HM_CHECK_LAUNCH(), which also counts it
+extern unsigned long long g_launches;
+#define HM_CHECK_LAUNCH()            \
+  do {                               \
+    ++::hm::g_launches;              \
+    HM_CUDA(cudaGetLastError());     \
+  } while (0)
 
 inline void fail(hm_status st, const std::string& m) { throw Error{st, m}; }
 
