@@ -16,7 +16,7 @@
 
 #include <algorithm>
 
-#include "entry.cuh"
+#include "entry_batch.cuh"
 
 namespace hm {
 
@@ -34,15 +34,6 @@ struct AcaState {
   double S2, vv;
 };
 
-__device__ __forceinline__ int64_t find_seg(const int64_t* __restrict__ pre, int64_t n, int64_t e) {
-  int64_t lo = 0, hi = n;   // largest c with pre[c] <= e
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (pre[mid] <= e) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 __global__ void k_step_sizes(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S, int64_t nb,
                              int64_t* __restrict__ rsz, int64_t* __restrict__ csz) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -53,55 +44,47 @@ __global__ void k_step_sizes(const AcaBlk* __restrict__ B, const AcaState* __res
   csz[c] = act ? B[c].m : 0;
 }
 
+// Residual row (ROW) or column entries of the active blocks of a chunk, as a batch mapping
+// for entry_batch.cuh.  put() applies the rank-one corrections of the previous k steps in
+// ascending l, each product and difference separately rounded (A15), and stores the residual
+// into column k of the block's V (row step) or U (column step) workspace.
 template <bool ROW>
-__global__ void k_aca_gen(const Panel* __restrict__ P, const AcaBlk* __restrict__ B, const AcaState* __restrict__ S,
-                          const int64_t* __restrict__ pre, int64_t nb, int64_t total, double* __restrict__ Uw,
-                          double* __restrict__ Vw, unsigned long long* __restrict__ evals) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  unsigned long long ev = 0;
-  if (e < total) {
-    const int64_t c = find_seg(pre, nb, e);
-    const AcaBlk b = B[c];
-    const AcaState st = S[c];
-    if (ROW || !st.skip) {
-      const int idx = (int)(e - pre[c]);                   // j (row step) or t (column step)
-      const int s = ROW ? b.q.rlo + st.i : b.q.rlo + idx;
-      const int t = ROW ? b.q.clo + idx : b.q.clo + st.js;
-      const bool swap = __ldg(&P[t].app) < __ldg(&P[s].app);
-      const int xs = swap ? t : s, ys = swap ? s : t;
-      const int cls = entry_class(P[xs], P[ys]);
-      double a;
-      if (cls >= 3) {
-        double X[9], Y[9], I;
-        load_panel_vertices(P, xs, X);
-        load_panel_vertices(P, ys, Y);
-        switch (cls) {
-          case 3: I = regular_sum<3>(X, Y); break;
-          case 4: I = regular_sum<4>(X, Y); break;
-          case 5: I = regular_sum<5>(X, Y); break;
-          default: I = regular_sum<6>(X, Y); break;
-        }
-        a = dmul(dmul(I, dmul(dmul(2.0, P[xs].area), dmul(2.0, P[ys].area))), kInv4Pi);
-      } else {
-        a = entry_st(P, s, t);
-      }
-      ev = (unsigned long long)rule_evals(cls);
-      const double* U = Uw + b.uoff;
-      const double* V = Vw + b.voff;
-      if (ROW) {
-        for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[st.i + (int64_t)l * b.m], V[idx + (int64_t)l * b.n]));
-        Vw[b.voff + (int64_t)st.k * b.n + idx] = a;
-      } else {
-        for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[idx + (int64_t)l * b.m], V[st.js + (int64_t)l * b.n]));
-        Uw[b.uoff + (int64_t)st.k * b.m + idx] = a;
-      }
+struct AcaMap {
+  const Panel* P;
+  const AcaBlk* B;
+  const AcaState* S;
+  const int64_t* pre;   // nb + 1 prefix of this step's row (or column) lengths
+  int64_t nb;
+  double* Uw;
+  double* Vw;
+  __device__ bool locate(int64_t e, bool valid, EntryRef& r) const {
+    const int64_t c = warp_find_segment(pre, nb + 1, e, valid);
+    if (!valid) return false;
+    if (!ROW && (S[c].skip || S[c].status != 0)) return false;
+    r.seg = (int32_t)c;
+    r.idx = (int32_t)(e - pre[c]);
+    return true;
+  }
+  __device__ void pair(EntryRef r, int& s, int& t) const {
+    const AcaBlk& b = B[r.seg];
+    const AcaState& st = S[r.seg];
+    s = ROW ? b.q.rlo + st.i : b.q.rlo + r.idx;
+    t = ROW ? b.q.clo + r.idx : b.q.clo + st.js;
+  }
+  __device__ void put(EntryRef r, double a) const {
+    const AcaBlk& b = B[r.seg];
+    const AcaState st = S[r.seg];
+    const double* U = Uw + b.uoff;
+    const double* V = Vw + b.voff;
+    if (ROW) {
+      for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[st.i + (int64_t)l * b.m], V[r.idx + (int64_t)l * b.n]));
+      Vw[b.voff + (int64_t)st.k * b.n + r.idx] = a;
+    } else {
+      for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[r.idx + (int64_t)l * b.m], V[st.js + (int64_t)l * b.n]));
+      Uw[b.uoff + (int64_t)st.k * b.m + r.idx] = a;
     }
   }
-  typedef cub::BlockReduce<unsigned long long, 128> BR;
-  __shared__ typename BR::TempStorage tmp;
-  unsigned long long tot = BR(tmp).Sum(ev);
-  if (threadIdx.x == 0 && tot) atomicAdd(evals, tot);
-}
+};
 
 __device__ __forceinline__ void warp_argmax(double& v, int& idx) {
 #pragma unroll
@@ -282,8 +265,9 @@ struct AcaWork {
   DBuf<int64_t> rsz, csz, rpre, cpre;
   DBuf<double> Uw, Vw;
   DBuf<uint32_t> bmap;
-  DBuf<unsigned long long> evals;
   DBuf<char> tmp;
+  EntryBatchWork batch;
+  double evals = 0;
 };
 
 // Run ACA on the owned admissible leaves listed in `ids` (indices into the owned list) with
@@ -332,14 +316,12 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     if (tot[0] == 0) break;
     C.aca_steps++;
     C.entries_aca += (double)(tot[0] + tot[1]);
-    k_aca_gen<true><<<grid_for(tot[0], 128), 128, 0, st>>>(P, W.blk.get(), W.state.get(), W.rpre.get(), nb, tot[0],
-                                                           W.Uw.get(), W.Vw.get(), W.evals.get());
-    HM_CHECK_LAUNCH();
+    W.evals += eval_batched(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), nb, W.Uw.get(), W.Vw.get()},
+                            tot[0], W.batch);
     k_aca_pivot<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Vw.get(), W.bmap.get());
     HM_CHECK_LAUNCH();
-    k_aca_gen<false><<<grid_for(tot[1], 128), 128, 0, st>>>(P, W.blk.get(), W.state.get(), W.cpre.get(), nb, tot[1],
-                                                            W.Uw.get(), W.Vw.get(), W.evals.get());
-    HM_CHECK_LAUNCH();
+    W.evals += eval_batched(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), nb, W.Uw.get(), W.Vw.get()},
+                            tot[1], W.batch);
     k_aca_update<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Uw.get(), W.Vw.get(),
                                                          W.bmap.get(), W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();
@@ -401,8 +383,6 @@ void setup_aca(Context& C) {
   }
   C.fpool.init(C.device, worst * sizeof(double) + (64u << 20));
   AcaWork W;
-  W.evals.alloc(1);
-  HM_CUDA(cudaMemsetAsync(W.evals.get(), 0, sizeof(unsigned long long), st));
   const bool rec = C.N <= 400000;
   auto& pivots = C.h_piv;
   pivots.clear();
@@ -446,14 +426,12 @@ void setup_aca(Context& C) {
     }
     if (!none.empty()) fail(HM_ERR_CUDA, "ACA overflow re-run did not converge within k_max");
   }
-  unsigned long long ev = 0;
-  HM_CUDA(cudaMemcpyAsync(&ev, W.evals.get(), sizeof(ev), cudaMemcpyDeviceToHost, st));
   C.h_rank.resize(nb);
   C.h_foff.resize(nb);
   HM_CUDA(cudaMemcpyAsync(C.h_rank.data(), C.frank.get(), nb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaMemcpyAsync(C.h_foff.data(), C.foff.get(), nb * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
-  C.evals_aca = (double)ev;
+  C.evals_aca = W.evals;
   C.factor_doubles = (int64_t)(C.fpool.used / sizeof(double));
 }
 

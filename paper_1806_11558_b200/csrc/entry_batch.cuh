@@ -1,0 +1,147 @@
+// entry_batch.cuh — batched evaluation of many Galerkin entries, bucketed by quadrature class
+// so that every warp runs one rule (the paper's "batching of many small similar tasks",
+// P:413-438, applied at the level of single entries).
+//
+//   pass 1  k_class_count    classify every entry of the batch, count per class
+//   pass 2  k_class_scatter  write (segment, index) references into per-class lists
+//   pass 3  one kernel per class: regular orders 3/4/5/6 (thread per entry), common edge,
+//           common vertex (Sauter-Schwab), identical panel (closed form)
+//
+// A batch is described by a mapping M (device-side functor, passed by value):
+//   bool locate(int64_t e, bool valid, EntryRef& r)  flattened entry -> reference (warp-collective)
+//   void pair(EntryRef r, int& s, int& t)            internal row / column indices of the entry
+//   void put(EntryRef r, double a)                   consume the value (store / residual update)
+#pragma once
+#include "entry.cuh"
+
+namespace hm {
+
+constexpr int kNumClass = 7;   // 0 identical, 1 edge, 2 vertex, 3..6 regular order n
+
+struct EntryRef {
+  int32_t seg, idx;
+};
+
+__device__ __forceinline__ int canonical_class(const Panel* __restrict__ P, int s, int t, int& xs, int& ys) {
+  const bool swap = __ldg(&P[t].app) < __ldg(&P[s].app);
+  xs = swap ? t : s;
+  ys = swap ? s : t;
+  return entry_class(P[xs], P[ys]);
+}
+
+template <class M>
+__global__ void k_class_count(M m, int64_t total, unsigned long long* __restrict__ cnt) {
+  __shared__ unsigned int sc[kNumClass];
+  if (threadIdx.x < kNumClass) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  EntryRef r;
+  if (m.locate(e, e < total, r)) {
+    int s, t, xs, ys;
+    m.pair(r, s, t);
+    atomicAdd(&sc[canonical_class(m.P, s, t, xs, ys)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumClass && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
+}
+
+template <class M>
+__global__ void k_class_scatter(M m, int64_t total, unsigned long long* __restrict__ cursor,
+                                EntryRef* __restrict__ lists) {
+  __shared__ unsigned int sc[kNumClass];
+  __shared__ unsigned long long base[kNumClass];
+  if (threadIdx.x < kNumClass) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  EntryRef r;
+  int cls = -1;
+  unsigned int pos = 0;
+  if (m.locate(e, e < total, r)) {
+    int s, t, xs, ys;
+    m.pair(r, s, t);
+    cls = canonical_class(m.P, s, t, xs, ys);
+    pos = atomicAdd(&sc[cls], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumClass) base[threadIdx.x] = sc[threadIdx.x] ? atomicAdd(&cursor[threadIdx.x], (unsigned long long)sc[threadIdx.x]) : 0;
+  __syncthreads();
+  if (cls >= 0) lists[base[cls] + pos] = r;
+}
+
+template <int n, class M>
+__global__ void __launch_bounds__(128) k_eval_regular(M m, const EntryRef* __restrict__ list, int64_t cnt) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  const EntryRef r = list[k];
+  int s, t, xs, ys;
+  m.pair(r, s, t);
+  canonical_class(m.P, s, t, xs, ys);
+  double X[9], Y[9];
+  load_panel_vertices(m.P, xs, X);
+  load_panel_vertices(m.P, ys, Y);
+  const double I = regular_sum<n>(X, Y);
+  m.put(r, dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi));
+}
+
+template <int KIND, class M>
+__global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __restrict__ list, int64_t cnt) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  const EntryRef r = list[k];
+  int s, t, xs, ys;
+  m.pair(r, s, t);
+  canonical_class(m.P, s, t, xs, ys);
+  const Panel& A = m.P[xs];
+  const Panel& B = m.P[ys];
+  double X[9], Y[9], v;
+  if (KIND == 0) {
+    load_panel_vertices(m.P, xs, X);
+    v = dmul(selfterm_closed(X, A.area), kInv4Pi);
+  } else {
+    orient_touching(KIND, A, B, X, Y);
+    const double I = ss_sum_t<KIND>(X, Y);
+    v = dmul(dmul(I, dmul(dmul(2.0, A.area), dmul(2.0, B.area))), kInv4Pi);
+  }
+  m.put(r, v);
+}
+
+struct EntryBatchWork {
+  DBuf<unsigned long long> cnt, cursor;
+  DBuf<EntryRef> list;
+  unsigned long long hcnt[kNumClass];
+};
+
+// Evaluate all `total` entries of mapping m; returns the number of kernel evaluations.
+template <class M>
+double eval_batched(Context& C, const M& m, int64_t total, EntryBatchWork& W) {
+  if (total <= 0) return 0.0;
+  cudaStream_t st = C.stream;
+  W.cnt.alloc(kNumClass);
+  W.cursor.alloc(kNumClass);
+  HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, kNumClass * sizeof(unsigned long long), st));
+  k_class_count<M><<<grid_for(total, 256), 256, 0, st>>>(m, total, W.cnt.get());
+  HM_CHECK_LAUNCH();
+  HM_CUDA(cudaMemcpyAsync(W.hcnt, W.cnt.get(), sizeof(W.hcnt), cudaMemcpyDeviceToHost, st));
+  HM_CUDA(cudaStreamSynchronize(st));
+  unsigned long long base[kNumClass], acc = 0;
+  for (int c = 0; c < kNumClass; ++c) { base[c] = acc; acc += W.hcnt[c]; }
+  W.list.alloc(acc);
+  HM_CUDA(cudaMemcpyAsync(W.cursor.get(), base, sizeof(base), cudaMemcpyHostToDevice, st));
+  k_class_scatter<M><<<grid_for(total, 256), 256, 0, st>>>(m, total, W.cursor.get(), W.list.get());
+  HM_CHECK_LAUNCH();
+  const EntryRef* L = W.list.get();
+  double evals = 0;
+  // heavy classes first so that the light ones fill the tail
+  if (W.hcnt[1]) { k_eval_touching<1, M><<<grid_for(W.hcnt[1], 64), 64, 0, st>>>(m, L + base[1], W.hcnt[1]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[2]) { k_eval_touching<2, M><<<grid_for(W.hcnt[2], 64), 64, 0, st>>>(m, L + base[2], W.hcnt[2]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[6]) { k_eval_regular<6, M><<<grid_for(W.hcnt[6], 128), 128, 0, st>>>(m, L + base[6], W.hcnt[6]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[5]) { k_eval_regular<5, M><<<grid_for(W.hcnt[5], 128), 128, 0, st>>>(m, L + base[5], W.hcnt[5]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[4]) { k_eval_regular<4, M><<<grid_for(W.hcnt[4], 128), 128, 0, st>>>(m, L + base[4], W.hcnt[4]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[3]) { k_eval_regular<3, M><<<grid_for(W.hcnt[3], 128), 128, 0, st>>>(m, L + base[3], W.hcnt[3]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[0]) { k_eval_touching<0, M><<<grid_for(W.hcnt[0], 64), 64, 0, st>>>(m, L + base[0], W.hcnt[0]); HM_CHECK_LAUNCH(); }
+  const double per[kNumClass] = {0, 6480, 2592, 81, 256, 625, 1296};
+  for (int c = 0; c < kNumClass; ++c) evals += per[c] * (double)W.hcnt[c];
+  return evals;
+}
+
+}  // namespace hm

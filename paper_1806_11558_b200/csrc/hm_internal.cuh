@@ -106,6 +106,7 @@ struct VmmPool {
 // Timers ----------------------------------------------------------------------------------
 struct PhaseTimes {
   double tree_ms = 0, near_ms = 0, aca_ms = 0, plan_ms = 0, setup_ms = 0;
+  double tree_phase_ms[6] = {0, 0, 0, 0, 0, 0};   // geometry, morton+sort, cluster, block, leafsort, partition
   double last_matvec_ms = 0, solve_ms = 0;
   int solve_iters = 0;
   double solve_relres = 0;
@@ -195,6 +196,31 @@ void upload_quadrature_tables();
 void quadrature_table_host(int n, double* nodes, double* weights);
 
 // Utilities
+// Segment lookup for flattened work: largest c with pre[c] <= e (pre ascending, nseg entries).
+// One binary search per warp (for the warp's smallest e), then a short forward walk per lane:
+// consecutive lanes hold consecutive e, so each lane walks over at most a few short segments.
+template <class I>
+__device__ __forceinline__ int64_t warp_find_segment(const I* __restrict__ pre, int64_t nseg, int64_t e, bool valid) {
+  const unsigned mask = __activemask();
+  int64_t emin = valid ? e : INT64_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t other = __shfl_xor_sync(mask, emin, o);
+    emin = other < emin ? other : emin;
+  }
+  int64_t lo = 0;
+  if (emin != INT64_MAX) {
+    int64_t hi = nseg;
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)__ldg(pre + mid) <= emin) lo = mid; else hi = mid;
+    }
+  }
+  if (valid)
+    while (lo + 1 < nseg && (int64_t)__ldg(pre + lo + 1) <= e) ++lo;
+  return lo;
+}
+
 inline unsigned grid_for(int64_t n, int block) {
   int64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;

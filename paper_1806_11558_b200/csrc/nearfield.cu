@@ -1,13 +1,12 @@
 // nearfield.cu — batched dense assembly of the rank's non-admissible leaves:
 // every entry of every owned dense leaf, stored contiguously without padding, row-major per
-// block, offsets = exclusive scan of |tau||sigma|.
-//
-// Two passes keep warps uniform: pass 1 (one thread per entry, consecutive entries of a
-// block row share the row panel) evaluates all regular entries and queues the ~1% touching
-// entries; pass 2 evaluates the queued singular entries (Sauter-Schwab / closed form).
+// block, offsets = exclusive scan of |tau||sigma|.  Entries are evaluated by the
+// class-bucketed batch machinery (entry_batch.cuh) in chunks of at most 2^26 entries.
 #include <cub/cub.cuh>
 
-#include "entry.cuh"
+#include <algorithm>
+
+#include "entry_batch.cuh"
 
 namespace hm {
 
@@ -19,71 +18,33 @@ __global__ void k_dense_sizes(const Quad* __restrict__ q, int64_t n, int64_t* __
   sz[b] = (int64_t)(q[b].rhi - q[b].rlo) * (q[b].chi - q[b].clo);
 }
 
-__device__ __forceinline__ int64_t find_block(const int64_t* __restrict__ off, int64_t nb, int64_t e) {
-  int64_t lo = 0, hi = nb;   // largest b with off[b] <= e
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (__ldg(off + mid) <= e) lo = mid; else hi = mid;
+// leaves [b0, b0 + nseg) of the owned dense list; flattened entry e counts from off[b0]
+struct NearMap {
+  const Panel* P;
+  const Quad* q;
+  const int64_t* off;    // owned-list offsets (nb + 1)
+  int64_t b0, nseg;      // first leaf of the chunk, leaves in the chunk
+  int64_t e0;            // off[b0]
+  double* store;
+  __device__ bool locate(int64_t e, bool valid, EntryRef& r) const {
+    const int64_t b = b0 + warp_find_segment(off + b0, nseg, e + e0, valid);
+    if (!valid) return false;
+    r.seg = (int32_t)b;
+    r.idx = (int32_t)(e + e0 - off[b]);
+    return true;
   }
-  return lo;
-}
-
-__global__ void k_near_regular(const Panel* __restrict__ P, const Quad* __restrict__ q, const int64_t* __restrict__ off,
-                               int64_t nb, int64_t total, double* __restrict__ store,
-                               int64_t* __restrict__ sing, int64_t sing_cap,
-                               unsigned long long* __restrict__ ctr /*[nsing, evals, bad]*/) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  unsigned long long ev = 0;
-  if (e < total) {
-    int64_t b = find_block(off, nb, e);
-    const Quad Q = q[b];
-    int64_t loc = e - off[b];
-    int ncol = Q.chi - Q.clo;
-    int s = Q.rlo + (int)(loc / ncol), t = Q.clo + (int)(loc % ncol);
-    const bool swap = __ldg(&P[t].app) < __ldg(&P[s].app);
-    const int xs = swap ? t : s, ys = swap ? s : t;
-    const int cls = entry_class(P[xs], P[ys]);
-    if (cls >= 3) {
-      double X[9], Y[9], I;
-      load_panel_vertices(P, xs, X);
-      load_panel_vertices(P, ys, Y);
-      switch (cls) {
-        case 3: I = regular_sum<3>(X, Y); break;
-        case 4: I = regular_sum<4>(X, Y); break;
-        case 5: I = regular_sum<5>(X, Y); break;
-        default: I = regular_sum<6>(X, Y); break;
-      }
-      const double v = dmul(dmul(I, dmul(dmul(2.0, P[xs].area), dmul(2.0, P[ys].area))), kInv4Pi);
-      store[e] = v;
-      if (!isfinite(v)) atomicAdd(&ctr[2], 1ull);
-      ev = (unsigned long long)(cls * cls * cls * cls);
-    } else {
-      unsigned long long slot = atomicAdd(&ctr[0], 1ull);
-      if ((int64_t)slot < sing_cap) sing[slot] = e;
-      ev = (unsigned long long)rule_evals(cls);
-    }
+  __device__ void pair(EntryRef r, int& s, int& t) const {
+    const Quad Q = q[r.seg];
+    const int ncol = Q.chi - Q.clo;
+    s = Q.rlo + r.idx / ncol;
+    t = Q.clo + r.idx % ncol;
   }
-  // block-aggregated evaluation count
-  typedef cub::BlockReduce<unsigned long long, 128> BR;
-  __shared__ typename BR::TempStorage tmp;
-  unsigned long long tot = BR(tmp).Sum(ev);
-  if (threadIdx.x == 0 && tot) atomicAdd(&ctr[1], tot);
-}
+  __device__ void put(EntryRef r, double a) const { store[off[r.seg] + r.idx] = a; }
+};
 
-__global__ void k_near_singular(const Panel* __restrict__ P, const Quad* __restrict__ q, const int64_t* __restrict__ off,
-                                int64_t nb, const int64_t* __restrict__ sing, const unsigned long long* __restrict__ nsing,
-                                double* __restrict__ store, unsigned long long* __restrict__ ctr) {
-  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= (int64_t)*nsing) return;
-  int64_t e = sing[k];
-  int64_t b = find_block(off, nb, e);
-  const Quad Q = q[b];
-  int64_t loc = e - off[b];
-  int ncol = Q.chi - Q.clo;
-  int s = Q.rlo + (int)(loc / ncol), t = Q.clo + (int)(loc % ncol);
-  const double v = entry_st(P, s, t);
-  store[e] = v;
-  if (!isfinite(v)) atomicAdd(&ctr[2], 1ull);
+__global__ void k_check_finite(const double* __restrict__ a, int64_t n, unsigned long long* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(a[i])) atomicAdd(bad, 1ull);
 }
 
 }  // namespace
@@ -105,40 +66,33 @@ void setup_nearfield(Context& C) {
   HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sz.get(), C.doff.get(), nb + 1, st));
   tmp.alloc(bytes);
   HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, sz.get(), C.doff.get(), nb + 1, st));
-  int64_t total = 0;
-  HM_CUDA(cudaMemcpyAsync(&total, C.doff.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  std::vector<int64_t> hoff(nb + 1);
+  HM_CUDA(cudaMemcpyAsync(hoff.data(), C.doff.get(), (nb + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
+  const int64_t total = hoff[nb];
   C.dense_doubles = total;
   C.dstore.alloc_exact(total);
-  if (total == 0) { C.evals_near = 0; return; }
-  DBuf<unsigned long long> ctr;
-  ctr.alloc(3);
-  HM_CUDA(cudaMemsetAsync(ctr.get(), 0, 3 * sizeof(unsigned long long), st));
-  // touching pairs are ~13 per row panel on the paper-type meshes; the queue is re-sized and
-  // the pass repeated if a mesh has more
-  int64_t sing_cap = std::min<int64_t>(total, 16 * (C.N + 1) + 1024);
-  DBuf<int64_t> sing;
-  unsigned long long hc[3];
-  for (;;) {
-    sing.alloc(sing_cap);
-    HM_CUDA(cudaMemsetAsync(ctr.get(), 0, 3 * sizeof(unsigned long long), st));
-    k_near_regular<<<grid_for(total, 128), 128, 0, st>>>(C.panel.get(), q, C.doff.get(), nb, total, C.dstore.get(),
-                                                          sing.get(), sing_cap, ctr.get());
-    HM_CHECK_LAUNCH();
-    HM_CUDA(cudaMemcpyAsync(hc, ctr.get(), sizeof(hc), cudaMemcpyDeviceToHost, st));
-    HM_CUDA(cudaStreamSynchronize(st));
-    if ((int64_t)hc[0] <= sing_cap) break;
-    sing_cap = (int64_t)hc[0];
+  C.evals_near = 0;
+  if (total == 0) return;
+  EntryBatchWork W;
+  const int64_t chunk = 1LL << 26;
+  for (int64_t b0 = 0; b0 < nb;) {
+    // leaves [b0, b1) with at most `chunk` entries (at least one leaf)
+    int64_t b1 = std::upper_bound(hoff.begin() + b0 + 1, hoff.begin() + nb + 1, hoff[b0] + chunk) - hoff.begin() - 1;
+    b1 = std::max(b1, b0 + 1);
+    NearMap m{C.panel.get(), q, C.doff.get(), b0, b1 - b0, hoff[b0], C.dstore.get()};
+    C.evals_near += eval_batched(C, m, hoff[b1] - hoff[b0], W);
+    b0 = b1;
   }
-  if (hc[0]) {
-    k_near_singular<<<grid_for((int64_t)hc[0], 64), 64, 0, st>>>(C.panel.get(), q, C.doff.get(), nb, sing.get(),
-                                                                  ctr.get(), C.dstore.get(), ctr.get());
-    HM_CHECK_LAUNCH();
-  }
-  HM_CUDA(cudaMemcpyAsync(hc, ctr.get(), sizeof(hc), cudaMemcpyDeviceToHost, st));
+  DBuf<unsigned long long> bad;
+  bad.alloc(1);
+  HM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), st));
+  k_check_finite<<<148 * 4, 256, 0, st>>>(C.dstore.get(), total, bad.get());
+  HM_CHECK_LAUNCH();
+  unsigned long long hb = 0;
+  HM_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
-  C.evals_near = (double)hc[1];
-  if (hc[2]) fail(HM_ERR_NUMERIC, "hm_setup: non-finite near-field entry (" + std::to_string(hc[2]) + " entries)");
+  if (hb) fail(HM_ERR_NUMERIC, "hm_setup: " + std::to_string(hb) + " non-finite near-field entries");
 }
 
 }  // namespace hm

@@ -297,6 +297,9 @@ void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_
 
 void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   cudaStream_t st = C.stream;
+  cudaEvent_t ev[7];
+  for (auto& e : ev) HM_CUDA(cudaEventCreate(&e));
+  HM_CUDA(cudaEventRecord(ev[0], st));
   const int64_t N = mesh.n_triangles, nv = mesh.n_vertices;
   C.have_tree = C.have_setup = false;
   C.N = N; C.nv = nv; C.leaf_size = leaf_size; C.eta = eta;
@@ -317,6 +320,7 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   HM_CHECK_LAUNCH();
   unsigned int hbad = 0;
   HM_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+  HM_CUDA(cudaEventRecord(ev[1], st));
   // ---- a2: Morton codes + stable sort
   const int nb = 148;
   DBuf<double> part, gbox;
@@ -343,6 +347,7 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   k_gather_panels<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), cen.get(), area.get(), hh.get(),
                                                      C.perm.get(), N, C.panel.get(), C.iperm.get());
   HM_CHECK_LAUNCH();
+  HM_CUDA(cudaEventRecord(ev[2], st));
   // ---- a3: cluster tree, level order
   int64_t leaf_min = std::max<int64_t>(1, (leaf_size + 1) / 2);
   int64_t cap = 2 * (N / leaf_min + 2) + 4;
@@ -382,6 +387,7 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
                                                    b, e, C.cl_box.get(), C.cl_diam2.get());
     HM_CHECK_LAUNCH();
   }
+  HM_CUDA(cudaEventRecord(ev[3], st));
   // ---- a4: block cluster tree, level-wise
   DBuf<int2> fr[2];
   DBuf<uint64_t> fk[2];
@@ -413,6 +419,7 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
     cur = 1 - cur;
     if (level > 62) fail(HM_ERR_ARG, "block tree deeper than 31 levels");
   }
+  HM_CUDA(cudaEventRecord(ev[4], st));
   // canonical DFS order = ascending left-aligned path key (A10)
   C.nadm = nadm; C.ndense = nden;
   C.adm.alloc_exact(nadm); C.dense.alloc_exact(nden);
@@ -428,10 +435,18 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
       return cub::DeviceRadixSort::SortPairs(t, b, denk.get(), ksorted.get(), denq.get(), C.dense.get(), (int)nden,
                                              0, 64, st);
     });
+  HM_CUDA(cudaEventRecord(ev[5], st));
   // ---- leaf partition over ranks (A18)
   partition_list(C, C.adm, nadm, 0, C.adm_begin, C.adm_end, tmp);
   partition_list(C, C.dense, nden, 1, C.dense_begin, C.dense_end, tmp);
+  HM_CUDA(cudaEventRecord(ev[6], st));
   HM_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k < 6; ++k) {
+    float ms = 0;
+    HM_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+    C.times.tree_phase_ms[k] = ms;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
   C.h_adm.clear(); C.h_dense.clear();
   C.have_tree = true;
 }
