@@ -90,8 +90,9 @@ const char* hm_last_error(hm_ctx ctx);
  *   "solver"       0 = GMRES(restart) (BASELINE.json), 1 = CG; default 0
  *   "restart"      GMRES restart length m, default 100
  *   "max_iter"     Krylov iteration cap (total matvecs), default 10000
- *   "aca_chunk_mb" ACA workspace budget per chunk in MiB, default 4096
- *   "aca_kws"      ACA workspace columns per block before the overflow re-run, default 32
+ *   "aca_chunk_mb" ACA workspace budget per chunk in MiB, default 16384, capped at 1/4 of the
+ *                  free device memory at hm_setup
+ *   "aca_kws"      ACA workspace columns per block before the overflow re-run, default 16
  * Errors: HM_ERR_ARG for an unknown key or an out-of-range value. */
 hm_status hm_set_option(hm_ctx ctx, const char* key, double value);
 hm_status hm_get_option(hm_ctx ctx, const char* key, double* value);

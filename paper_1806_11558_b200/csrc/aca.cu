@@ -266,8 +266,7 @@ struct AcaWork {
   DBuf<double> Uw, Vw;
   DBuf<uint32_t> bmap;
   DBuf<char> tmp;
-  EntryBatchWork batch;
-  double evals = 0;
+  DBuf<unsigned long long> ev;
 };
 
 // Run ACA on the owned admissible leaves listed in `ids` (indices into the owned list) with
@@ -316,12 +315,14 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     if (tot[0] == 0) break;
     C.aca_steps++;
     C.entries_aca += (double)(tot[0] + tot[1]);
-    W.evals += eval_batched(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), nb, W.Uw.get(), W.Vw.get()},
-                            tot[0], W.batch);
+    k_eval_fused<<<grid_for(tot[0], 256), 256, 0, st>>>(
+        AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), nb, W.Uw.get(), W.Vw.get()}, tot[0], W.ev.get());
+    HM_CHECK_LAUNCH();
     k_aca_pivot<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Vw.get(), W.bmap.get());
     HM_CHECK_LAUNCH();
-    W.evals += eval_batched(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), nb, W.Uw.get(), W.Vw.get()},
-                            tot[1], W.batch);
+    k_eval_fused<<<grid_for(tot[1], 256), 256, 0, st>>>(
+        AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), nb, W.Uw.get(), W.Vw.get()}, tot[1], W.ev.get());
+    HM_CHECK_LAUNCH();
     k_aca_update<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Uw.get(), W.Vw.get(),
                                                          W.bmap.get(), W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();
@@ -383,12 +384,17 @@ void setup_aca(Context& C) {
   }
   C.fpool.init(C.device, worst * sizeof(double) + (64u << 20));
   AcaWork W;
+  W.ev.alloc(1);
+  HM_CUDA(cudaMemsetAsync(W.ev.get(), 0, sizeof(unsigned long long), st));
   const bool rec = C.N <= 400000;
   auto& pivots = C.h_piv;
   pivots.clear();
   if (rec) pivots.resize(nb);
   const int kws = std::max(1, std::min(C.k_max, (int)C.aca_kws));
-  const double budget = C.aca_chunk_mb * 1048576.0;
+  size_t free_b = 0, total_b = 0;
+  HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  // workspace per chunk: the option, capped at a quarter of the free device memory
+  const double budget = std::min(C.aca_chunk_mb * 1048576.0, 0.25 * (double)free_b);
   std::vector<int32_t> ids, overflow;
   double used = 0;
   for (int64_t b = 0; b <= nb; ++b) {
@@ -431,7 +437,10 @@ void setup_aca(Context& C) {
   HM_CUDA(cudaMemcpyAsync(C.h_rank.data(), C.frank.get(), nb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaMemcpyAsync(C.h_foff.data(), C.foff.get(), nb * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
-  C.evals_aca = W.evals;
+  unsigned long long hev = 0;
+  HM_CUDA(cudaMemcpyAsync(&hev, W.ev.get(), sizeof(hev), cudaMemcpyDeviceToHost, st));
+  HM_CUDA(cudaStreamSynchronize(st));
+  C.evals_aca = (double)hev;
   C.factor_doubles = (int64_t)(C.fpool.used / sizeof(double));
 }
 

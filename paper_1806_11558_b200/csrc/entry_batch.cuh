@@ -105,6 +105,69 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
   m.put(r, v);
 }
 
+// Fused single-pass variant for batches dominated by cheap regular classes (ACA rows and
+// columns: admissible blocks are far apart, so nearly every entry is order 3 or 4): a CTA of
+// 256 threads classifies its 256 entries, counting-sorts them by class in shared memory and
+// then evaluates in sorted order, so warps are uniform except at class boundaries.  No
+// global lists, no host round trip.
+template <class M>
+__global__ void __launch_bounds__(256) k_eval_fused(M m, int64_t total, unsigned long long* __restrict__ evals) {
+  __shared__ unsigned int cnt[kNumClass + 1];
+  __shared__ EntryRef sref[256];
+  __shared__ unsigned char scls[256];
+  if (threadIdx.x <= kNumClass) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  EntryRef r;
+  int cls = kNumClass;                       // kNumClass = no work
+  if (m.locate(e, e < total, r)) {
+    int s, t, xs, ys;
+    m.pair(r, s, t);
+    cls = canonical_class(m.P, s, t, xs, ys);
+  }
+  // counting sort of (cls, ref), heavy classes first: order 6,5,4,3, edge, vertex, identical, none
+  const int key = cls == kNumClass ? 7 : cls >= 3 ? 6 - cls : cls == 1 ? 4 : cls == 2 ? 5 : 6;
+  const unsigned pos = atomicAdd(&cnt[key], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned acc = 0;
+    for (int k = 0; k <= kNumClass; ++k) { unsigned c = cnt[k]; cnt[k] = acc; acc += c; }
+  }
+  __syncthreads();
+  sref[cnt[key] + pos] = r;
+  scls[cnt[key] + pos] = (unsigned char)cls;
+  __syncthreads();
+  const int my = scls[threadIdx.x];
+  unsigned long long ev = 0;
+  if (my < kNumClass) {
+    const EntryRef rr = sref[threadIdx.x];
+    int s, t, xs, ys;
+    m.pair(rr, s, t);
+    canonical_class(m.P, s, t, xs, ys);
+    double v;
+    if (my >= 3) {
+      double X[9], Y[9], I;
+      load_panel_vertices(m.P, xs, X);
+      load_panel_vertices(m.P, ys, Y);
+      switch (my) {
+        case 3: I = regular_sum<3>(X, Y); break;
+        case 4: I = regular_sum<4>(X, Y); break;
+        case 5: I = regular_sum<5>(X, Y); break;
+        default: I = regular_sum<6>(X, Y); break;
+      }
+      v = dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi);
+    } else {
+      v = entry_st(m.P, s, t);
+    }
+    ev = (unsigned long long)rule_evals(my);
+    m.put(rr, v);
+  }
+  // evaluation count, one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+  if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
+}
+
 struct EntryBatchWork {
   DBuf<unsigned long long> cnt, cursor;
   DBuf<EntryRef> list;

@@ -103,6 +103,26 @@ struct VmmPool {
   ~VmmPool() { release(); }
 };
 
+// matvec plan records (matvec.cu)
+struct MvTask {
+  int32_t rlo, clo, loff;   // loff: offset in doubles from the batch's staged start
+  uint32_t mnk;             // m | n << 11 | k << 22 (k == 0: dense m x n row-major)
+};
+struct MvBatch {
+  int64_t src;              // byte offset (16-B aligned) from the base pointer
+  int32_t bytes;            // multiple of 16
+  int32_t first, count;
+  int32_t base;             // 0 dense store, 1 factor pool
+  int32_t pad[2];
+};
+struct MvLarge {
+  int32_t rlo, clo, m, n, k, pad;
+  int64_t off;              // doubles from the factor pool base
+  int64_t toff;             // offset into the t buffer
+};
+struct MvTileV { int32_t blk, l, j0, j1; };
+struct MvTileU { int32_t blk, t0, t1, pad; };
+
 // Timers ----------------------------------------------------------------------------------
 struct PhaseTimes {
   double tree_ms = 0, near_ms = 0, aca_ms = 0, plan_ms = 0, setup_ms = 0;
@@ -122,7 +142,7 @@ struct Context {
 
   // options
   int k_max = 64, solver = 0, restart = 100, max_iter = 10000;
-  double aca_chunk_mb = 4096, aca_kws = 32;
+  double aca_chunk_mb = 16384, aca_kws = 16;
 
   // tree state
   bool have_tree = false, have_setup = false;
@@ -159,8 +179,16 @@ struct Context {
   double evals_near = 0, evals_aca = 0, entries_aca = 0;
   int aca_steps = 0, aca_chunks = 0, aca_overflow = 0;
 
-  // matvec plan: owned adm leaves split by size class
-  DBuf<int32_t> lr_small, lr_large;    // owned adm leaf indices (relative to adm_begin)
+  // matvec plan (matvec.cu)
+  DBuf<MvBatch> mv_batches;
+  DBuf<MvTask> mv_tasks;
+  DBuf<int32_t> mv_cta;
+  DBuf<MvLarge> mv_large, mv_dense_big;
+  DBuf<MvTileV> mv_tiles_v;
+  DBuf<MvTileU> mv_tiles_u;
+  DBuf<double> mv_tbuf;
+  int mv_grid = 0;
+  int64_t mv_nbatches = 0, mv_tlen = 0;
   int64_t n_lr_small = 0, n_lr_large = 0;
 
   // work vectors (internal order)

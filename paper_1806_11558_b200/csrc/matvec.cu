@@ -1,20 +1,33 @@
 // matvec.cu — batched H-matrix-vector product: non-admissible leaves apply their
-// stored dense block, admissible leaves apply U (V^T x) ("two matrix-vector products
-// of skinny matrices"); application<->internal permutations at entry and exit.
+// stored dense block, admissible leaves apply U (V^T x) ("two matrix-vector
+// products of skinny matrices"); application <-> internal permutation at the ends.
 //
-// Memory-bound (0.25 flop/B).  Storage is streamed once per product in storage order:
-//   dense leaves   one warp per leaf; s lanes per row (s = pow2 ~ n/4) so each load
-//                  instruction touches whole 32-B sectors; per-row shuffle reduction, one
-//                  FP64 atomic per row into the L2-resident y.
-//   low-rank       [U m x k | V n x k] col-major, contiguous per block: t = V^T x_sigma as k
-//                  coalesced dot products, then y_tau += U t with lanes over rows (coalesced
-//                  along each u_l), one atomic per row.  Warp per block when m+n <= 1024,
-//                  CTA (256 threads) per block above.
+// Memory-bound (0.25 flop/B): the stored H is streamed from HBM exactly once per product.
+//
+//   small leaves   (dense blocks and low-rank blocks with (m+n)k*8 <= 16 KiB, ~all leaves):
+//                  k_mv_batched — one persistent CTA per SM walks a contiguous, byte-balanced
+//                  range of "batches" (runs of consecutive leaves whose storage is contiguous,
+//                  <= 40 KiB).  One elected thread streams each batch into shared memory with a
+//                  single cp.async.bulk (TMA bulk copy, mbarrier completion), 4 stages deep, so
+//                  ~160 KiB per SM are in flight while the 12 warps compute the previous
+//                  batches out of shared memory: dense rows with s lanes per row, low-rank
+//                  t = V^T x then y += U t.  One FP64 atomic per row into the L2-resident y.
+//   large low-rank (the few blocks above 16 KiB): two tiled kernels with direct coalesced
+//                  loads, k_mv_large_v (t += V^T x per column tile, atomics into t) then
+//                  k_mv_large_u (y += U t, k independent loads per row).
+//   dense blocks too big for a stage (only with large leaf_size): k_mv_dense_direct.
 #include <cub/cub.cuh>
+
+#include <algorithm>
 
 #include "entry.cuh"
 
 namespace hm {
+
+constexpr int kMvStages = 4;
+constexpr int kMvStageBytes = 40 * 1024;
+constexpr int kMvThreads = 384;
+constexpr int kMvSmallMax = 16 * 1024;
 
 namespace {
 
@@ -30,17 +43,43 @@ __global__ void k_scatter(const double* __restrict__ y_int, const int32_t* __res
   if (s < N) y_app[perm[s]] = y_int[s];
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 template <int S>
 __device__ __forceinline__ void dense_rows(const double* __restrict__ B, int m, int n, const double* __restrict__ x,
                                            double* __restrict__ y, int lane) {
-  constexpr int RPP = 32 / S;               // rows per pass
+  constexpr int RPP = 32 / S;   // rows per pass
   const int sub = lane % S, rr = lane / S;
   for (int r0 = 0; r0 < m; r0 += RPP) {
     const int r = r0 + rr;
     double acc = 0.0;
     if (r < m) {
-      const double* row = B + (int64_t)r * n;
-      for (int c = sub; c < n; c += S) acc += __ldg(row + c) * __ldg(x + c);
+      const double* row = B + r * n;
+      for (int c = sub; c < n; c += S) acc += row[c] * __ldg(x + c);
     }
 #pragma unroll
     for (int o = S / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -48,120 +87,265 @@ __device__ __forceinline__ void dense_rows(const double* __restrict__ B, int m, 
   }
 }
 
-__global__ void k_mv_dense(const Quad* __restrict__ q, const int64_t* __restrict__ off, int64_t nb,
-                           const double* __restrict__ store, const double* __restrict__ x, double* __restrict__ y) {
+__device__ __forceinline__ void dense_any(const double* B, int m, int n, const double* x, double* y, int lane) {
+  if (n <= 8) dense_rows<2>(B, m, n, x, y, lane);
+  else if (n <= 16) dense_rows<4>(B, m, n, x, y, lane);
+  else if (n <= 48) dense_rows<8>(B, m, n, x, y, lane);
+  else if (n <= 96) dense_rows<16>(B, m, n, x, y, lane);
+  else dense_rows<32>(B, m, n, x, y, lane);
+}
+
+// low-rank block from shared memory: U (m x k) then V (n x k), column-major
+__device__ __forceinline__ void lowrank_smem(const double* __restrict__ U, int m, int n, int k,
+                                             const double* __restrict__ x, double* __restrict__ y,
+                                             double* __restrict__ tsh, int lane) {
+  const double* V = U + m * k;
+  for (int l = 0; l < k; ++l) {
+    const double* v = V + l * n;
+    double acc = 0.0;
+    for (int j = lane; j < n; j += 32) acc += v[j] * __ldg(x + j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) tsh[l] = acc;
+  }
+  __syncwarp();
+  for (int t = lane; t < m; t += 32) {
+    double acc = 0.0;
+    for (int l = 0; l < k; ++l) acc += U[t + l * m] * tsh[l];
+    atomicAdd(y + t, acc);
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kMvThreads, 1)
+    k_mv_batched(const MvBatch* __restrict__ batches, const int32_t* __restrict__ cta_first,
+                 const MvTask* __restrict__ tasks, const char* __restrict__ base0, const char* __restrict__ base1,
+                 const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  double* tsh = reinterpret_cast<double*>(smem + 128);                 // [warps][64]
+  unsigned char* buf = smem + 128 + (kMvThreads / 32) * 64 * sizeof(double);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b0 = cta_first[blockIdx.x], nb = cta_first[blockIdx.x + 1] - b0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMvStages; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int it, int stage) {
+    const MvBatch B = batches[b0 + it];
+    mbar_expect_tx(&bar[stage], (unsigned)B.bytes);
+    bulk_g2s(buf + stage * kMvStageBytes, (B.base ? base1 : base0) + B.src, (unsigned)B.bytes, &bar[stage]);
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kMvStages && s < nb; ++s) issue(s, s);
+  for (int it = 0; it < nb; ++it) {
+    const int stage = it % kMvStages;
+    mbar_wait(&bar[stage], (unsigned)((it / kMvStages) & 1));
+    const MvBatch B = batches[b0 + it];
+    const double* data = reinterpret_cast<const double*>(buf + stage * kMvStageBytes);
+    for (int t = warp; t < B.count; t += kMvThreads / 32) {
+      const MvTask T = tasks[B.first + t];
+      const int m = T.mnk & 2047, n = (T.mnk >> 11) & 2047, k = T.mnk >> 22;
+      if (k == 0) dense_any(data + T.loff, m, n, x + T.clo, y + T.rlo, lane);
+      else lowrank_smem(data + T.loff, m, n, k, x + T.clo, y + T.rlo, tsh + warp * 64, lane);
+    }
+    __syncthreads();                                   // stage fully consumed
+    if (threadIdx.x == 0 && it + kMvStages < nb) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(it + kMvStages, stage);
+    }
+  }
+}
+
+// large low-rank blocks, phase 1: t[toff + l] += sum_{j in tile} V[j, l] x[clo + j]
+__global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
+                                                    const MvLarge* __restrict__ L, const double* __restrict__ pool,
+                                                    const double* __restrict__ x, double* __restrict__ tbuf) {
+  __shared__ double part[8];
+  for (int64_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
+    const MvTileV T = tiles[i];
+    const MvLarge B = L[T.blk];
+    const double* v = pool + B.off + (int64_t)B.m * B.k + (int64_t)T.l * B.n;
+    const double* xs = x + B.clo;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = T.j0 + threadIdx.x;
+    for (; j + 768 < T.j1; j += 1024) {
+      a0 += __ldg(v + j) * __ldg(xs + j);
+      a1 += __ldg(v + j + 256) * __ldg(xs + j + 256);
+      a2 += __ldg(v + j + 512) * __ldg(xs + j + 512);
+      a3 += __ldg(v + j + 768) * __ldg(xs + j + 768);
+    }
+    for (; j < T.j1; j += 256) a0 += __ldg(v + j) * __ldg(xs + j);
+    double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += part[w];
+      atomicAdd(tbuf + B.toff + T.l, s);
+    }
+    __syncthreads();
+  }
+}
+
+// large low-rank blocks, phase 2: y[rlo + t] += sum_l U[t, l] t_l over a row tile
+__global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ tiles, int64_t ntiles,
+                                                    const MvLarge* __restrict__ L, const double* __restrict__ pool,
+                                                    const double* __restrict__ tbuf, double* __restrict__ y) {
+  __shared__ double tl[64];
+  for (int64_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
+    const MvTileU T = tiles[i];
+    const MvLarge B = L[T.blk];
+    if (threadIdx.x < B.k) tl[threadIdx.x] = tbuf[B.toff + threadIdx.x];
+    __syncthreads();
+    const double* U = pool + B.off;
+    for (int t = T.t0 + threadIdx.x; t < T.t1; t += 256) {
+      double acc = 0.0;
+      for (int l = 0; l < B.k; ++l) acc += __ldg(U + t + (int64_t)l * B.m) * tl[l];
+      atomicAdd(y + B.rlo + t, acc);
+    }
+    __syncthreads();
+  }
+}
+
+// dense blocks that do not fit a stage (large leaf_size only): warp per block, direct loads
+__global__ void k_mv_dense_direct(const MvLarge* __restrict__ L, int64_t nl, const double* __restrict__ store,
+                                  const double* __restrict__ x, double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t b = w0; b < nb; b += nw) {
-    const Quad Q = q[b];
-    const int m = Q.rhi - Q.rlo, n = Q.chi - Q.clo;
-    const double* B = store + off[b];
-    if (n <= 8) dense_rows<2>(B, m, n, x + Q.clo, y + Q.rlo, lane);
-    else if (n <= 16) dense_rows<4>(B, m, n, x + Q.clo, y + Q.rlo, lane);
-    else if (n <= 48) dense_rows<8>(B, m, n, x + Q.clo, y + Q.rlo, lane);
-    else if (n <= 96) dense_rows<16>(B, m, n, x + Q.clo, y + Q.rlo, lane);
-    else dense_rows<32>(B, m, n, x + Q.clo, y + Q.rlo, lane);
-  }
-}
-
-// warp per low-rank block (m + n <= 1024)
-__global__ void k_mv_lowrank_warp(const Quad* __restrict__ q, const int32_t* __restrict__ list, int64_t nl,
-                                  const int64_t* __restrict__ foff, const int32_t* __restrict__ frank,
-                                  const double* __restrict__ pool, const double* __restrict__ x,
-                                  double* __restrict__ y) {
-  __shared__ double tsh[8][64];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t a = w0; a < nl; a += nw) {
-    const int b = list[a];
-    const int k = frank[b];
-    if (k <= 0) continue;
-    const Quad Q = q[b];
-    const int m = Q.rhi - Q.rlo, n = Q.chi - Q.clo;
-    const double* U = pool + foff[b];
-    const double* V = U + (int64_t)m * k;
-    const double* xs = x + Q.clo;
-    for (int l = 0; l < k; ++l) {
-      const double* v = V + (int64_t)l * n;
-      double acc = 0.0;
-      for (int j = lane; j < n; j += 32) acc += __ldg(v + j) * __ldg(xs + j);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) tsh[wib][l] = acc;
-    }
-    __syncwarp();
-    for (int t = lane; t < m; t += 32) {
-      double acc = 0.0;
-      for (int l = 0; l < k; ++l) acc += __ldg(U + t + (int64_t)l * m) * tsh[wib][l];
-      atomicAdd(y + Q.rlo + t, acc);
-    }
-    __syncwarp();
-  }
-}
-
-// CTA (256 threads) per large low-rank block
-__global__ void k_mv_lowrank_cta(const Quad* __restrict__ q, const int32_t* __restrict__ list, int64_t nl,
-                                 const int64_t* __restrict__ foff, const int32_t* __restrict__ frank,
-                                 const double* __restrict__ pool, const double* __restrict__ x,
-                                 double* __restrict__ y) {
-  __shared__ double part[8][64];
-  __shared__ double tsh[64];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (int64_t a = blockIdx.x; a < nl; a += gridDim.x) {
-    const int b = list[a];
-    const int k = frank[b];
-    if (k <= 0) continue;
-    const Quad Q = q[b];
-    const int m = Q.rhi - Q.rlo, n = Q.chi - Q.clo;
-    const double* U = pool + foff[b];
-    const double* V = U + (int64_t)m * k;
-    const double* xs = x + Q.clo;
-    for (int l = 0; l < k; ++l) {
-      const double* v = V + (int64_t)l * n;
-      double acc = 0.0;
-      for (int j = threadIdx.x; j < n; j += blockDim.x) acc += __ldg(v + j) * __ldg(xs + j);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) part[wib][l] = acc;
-    }
-    __syncthreads();
-    if (threadIdx.x < k) {
-      double s = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w][threadIdx.x];
-      tsh[threadIdx.x] = s;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < m; t += blockDim.x) {
-      double acc = 0.0;
-      for (int l = 0; l < k; ++l) acc += __ldg(U + t + (int64_t)l * m) * tsh[l];
-      atomicAdd(y + Q.rlo + t, acc);
-    }
-    __syncthreads();
+  for (int64_t b = w0; b < nl; b += nw) {
+    const MvLarge B = L[b];
+    dense_any(store + B.off, B.m, B.n, x + B.clo, y + B.rlo, lane);
   }
 }
 
 }  // namespace
 
 void plan_matvec(Context& C) {
-  const int64_t nb = C.adm_end - C.adm_begin;
-  std::vector<int32_t> small, large;
-  for (int64_t b = 0; b < nb; ++b) {
-    const Quad& q = C.h_adm[C.adm_begin + b];
-    if (C.h_rank[b] <= 0) continue;
-    if ((q.rhi - q.rlo) + (q.chi - q.clo) <= 1024) small.push_back((int32_t)b);
-    else large.push_back((int32_t)b);
+  cudaStream_t st = C.stream;
+  const int64_t nd = C.dense_end - C.dense_begin, na = C.adm_end - C.adm_begin;
+  std::vector<int64_t> hoff(nd + 1);
+  HM_CUDA(cudaMemcpyAsync(hoff.data(), C.doff.get(), (nd + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (C.h_dense.size() != (size_t)C.ndense) {
+    C.h_dense.resize(C.ndense);
+    HM_CUDA(cudaMemcpyAsync(C.h_dense.data(), C.dense.get(), C.ndense * sizeof(Quad), cudaMemcpyDeviceToHost, st));
   }
-  C.n_lr_small = (int64_t)small.size();
+  HM_CUDA(cudaStreamSynchronize(st));
+  struct Item { int64_t byte0, bytes; int base; MvTask t; };
+  std::vector<Item> items;
+  items.reserve(nd + na);
+  std::vector<MvLarge> dense_big, large;
+  for (int64_t b = 0; b < nd; ++b) {
+    const Quad& q = C.h_dense[C.dense_begin + b];
+    const int m = q.rhi - q.rlo, n = q.chi - q.clo;
+    const int64_t bytes = 8 * (int64_t)m * n;
+    if (bytes + 32 > kMvStageBytes || m > 2047 || n > 2047) {
+      dense_big.push_back(MvLarge{q.rlo, q.clo, m, n, 0, 0, hoff[b], 0});
+      continue;
+    }
+    items.push_back(Item{8 * hoff[b], bytes, 0, MvTask{q.rlo, q.clo, 0, (uint32_t)m | ((uint32_t)n << 11)}});
+  }
+  std::vector<int64_t> lr_order;
+  for (int64_t b = 0; b < na; ++b)
+    if (C.h_rank[b] > 0) lr_order.push_back(b);
+  std::sort(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; });
+  int64_t tl = 0;
+  for (int64_t b : lr_order) {
+    const Quad& q = C.h_adm[C.adm_begin + b];
+    const int m = q.rhi - q.rlo, n = q.chi - q.clo, k = C.h_rank[b];
+    const int64_t bytes = 8 * (int64_t)k * (m + n);
+    if (bytes <= kMvSmallMax && m <= 2047 && n <= 2047) {
+      items.push_back(Item{8 * C.h_foff[b], bytes, 1,
+                           MvTask{q.rlo, q.clo, 0, (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)}});
+    } else {
+      large.push_back(MvLarge{q.rlo, q.clo, m, n, k, 0, C.h_foff[b], tl});
+      tl += k;
+    }
+  }
+  // batches of consecutive, contiguous items within one stage
+  std::vector<MvBatch> batches;
+  std::vector<MvTask> tasks;
+  tasks.reserve(items.size());
+  for (size_t i = 0; i < items.size();) {
+    const int64_t a0 = items[i].byte0 & ~int64_t(15);
+    int64_t end = items[i].byte0 + items[i].bytes;
+    size_t j = i + 1;
+    while (j < items.size() && items[j].base == items[i].base && items[j].byte0 == items[j - 1].byte0 + items[j - 1].bytes &&
+           ((items[j].byte0 + items[j].bytes + 15) & ~int64_t(15)) - a0 <= kMvStageBytes) {
+      end = items[j].byte0 + items[j].bytes;
+      ++j;
+    }
+    const int64_t a1 = (end + 15) & ~int64_t(15);
+    MvBatch B{};
+    B.src = a0;
+    B.bytes = (int32_t)(a1 - a0);
+    B.first = (int32_t)tasks.size();
+    B.count = (int32_t)(j - i);
+    B.base = items[i].base;
+    for (size_t k = i; k < j; ++k) {
+      MvTask t = items[k].t;
+      t.loff = (int32_t)((items[k].byte0 - a0) / 8);
+      tasks.push_back(t);
+    }
+    batches.push_back(B);
+    i = j;
+  }
+  // byte-balanced contiguous batch ranges, one persistent CTA per SM
+  int sms = 148;
+  HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, C.device));
+  const int G = std::max(1, std::min<int>(sms, (int)batches.size()));
+  std::vector<int32_t> cta_first(G + 1, (int32_t)batches.size());
+  {
+    double total = 0;
+    for (auto& B : batches) total += B.bytes;
+    double acc = 0;
+    int g = 0;
+    cta_first[0] = 0;
+    for (size_t b = 0; b < batches.size() && g + 1 < G; ++b) {
+      while (g + 1 < G && acc >= total * (g + 1) / G) cta_first[++g] = (int32_t)b;
+      acc += batches[b].bytes;
+    }
+    while (g + 1 < G) cta_first[++g] = (int32_t)batches.size();
+  }
+  // tiles of the large low-rank blocks
+  std::vector<MvTileV> tv;
+  std::vector<MvTileU> tu;
+  for (size_t i = 0; i < large.size(); ++i) {
+    const MvLarge& B = large[i];
+    for (int l = 0; l < B.k; ++l)
+      for (int j0 = 0; j0 < B.n; j0 += 4096) tv.push_back(MvTileV{(int32_t)i, l, j0, std::min(B.n, j0 + 4096)});
+    const int rows = std::max(32, 4096 / B.k);
+    for (int t0 = 0; t0 < B.m; t0 += rows) tu.push_back(MvTileU{(int32_t)i, t0, std::min(B.m, t0 + rows), 0});
+  }
+  auto up = [&](auto& dbuf, const auto& v) {
+    dbuf.alloc_exact(v.size());
+    if (!v.empty())
+      HM_CUDA(cudaMemcpyAsync(dbuf.get(), v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, st));
+  };
+  up(C.mv_batches, batches);
+  up(C.mv_tasks, tasks);
+  up(C.mv_cta, cta_first);
+  up(C.mv_large, large);
+  up(C.mv_dense_big, dense_big);
+  up(C.mv_tiles_v, tv);
+  up(C.mv_tiles_u, tu);
+  C.mv_grid = G;
+  C.mv_nbatches = (int64_t)batches.size();
+  C.mv_tbuf.alloc_exact(tl + 1);
+  C.mv_tlen = tl;
+  C.n_lr_small = (int64_t)(lr_order.size() - large.size());
   C.n_lr_large = (int64_t)large.size();
-  C.lr_small.alloc_exact(C.n_lr_small);
-  C.lr_large.alloc_exact(C.n_lr_large);
-  if (C.n_lr_small)
-    HM_CUDA(cudaMemcpyAsync(C.lr_small.get(), small.data(), small.size() * 4, cudaMemcpyHostToDevice, C.stream));
-  if (C.n_lr_large)
-    HM_CUDA(cudaMemcpyAsync(C.lr_large.get(), large.data(), large.size() * 4, cudaMemcpyHostToDevice, C.stream));
-  HM_CUDA(cudaStreamSynchronize(C.stream));
+  HM_CUDA(cudaStreamSynchronize(st));
+  static bool attr = false;
+  if (!attr) {
+    const int smem = 128 + (kMvThreads / 32) * 64 * 8 + kMvStages * kMvStageBytes;
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
 }
 
 void gather_perm(Context& C, const double* x_app, double* x_int) {
@@ -174,25 +358,29 @@ void scatter_perm(Context& C, const double* y_int, double* y_app) {
   HM_CHECK_LAUNCH();
 }
 
-// y_int = (local leaves of H) x_int, then summed over ranks
+// y_int = (local leaves of H) x_int, then summed over ranks (P:578-587)
 void matvec_internal(Context& C, const double* x_int, double* y_int) {
   cudaStream_t st = C.stream;
   HM_CUDA(cudaMemsetAsync(y_int, 0, C.N * sizeof(double), st));
-  const int64_t nd = C.dense_end - C.dense_begin;
-  const int sms = 148;
-  if (nd) {
-    k_mv_dense<<<sms * 8, 256, 0, st>>>(C.dense.get() + C.dense_begin, C.doff.get(), nd, C.dstore.get(), x_int, y_int);
+  if (C.mv_tlen) HM_CUDA(cudaMemsetAsync(C.mv_tbuf.get(), 0, C.mv_tlen * sizeof(double), st));
+  const double* pool = (const double*)C.fpool.base;
+  if (C.mv_nbatches) {
+    const int smem = 128 + (kMvThreads / 32) * 64 * 8 + kMvStages * kMvStageBytes;
+    k_mv_batched<<<C.mv_grid, kMvThreads, smem, st>>>(C.mv_batches.get(), C.mv_cta.get(), C.mv_tasks.get(),
+                                                       (const char*)C.dstore.get(), (const char*)pool, x_int, y_int);
     HM_CHECK_LAUNCH();
   }
-  const Quad* qa = C.adm.get() + C.adm_begin;
-  if (C.n_lr_small) {
-    k_mv_lowrank_warp<<<sms * 8, 256, 0, st>>>(qa, C.lr_small.get(), C.n_lr_small, C.foff.get(), C.frank.get(),
-                                               (const double*)C.fpool.base, x_int, y_int);
+  if (C.mv_dense_big.n) {
+    k_mv_dense_direct<<<148 * 8, 256, 0, st>>>(C.mv_dense_big.get(), (int64_t)C.mv_dense_big.n, C.dstore.get(),
+                                               x_int, y_int);
     HM_CHECK_LAUNCH();
   }
-  if (C.n_lr_large) {
-    k_mv_lowrank_cta<<<sms * 4, 256, 0, st>>>(qa, C.lr_large.get(), C.n_lr_large, C.foff.get(), C.frank.get(),
-                                              (const double*)C.fpool.base, x_int, y_int);
+  if (C.mv_tiles_v.n) {
+    k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), (int64_t)C.mv_tiles_v.n, C.mv_large.get(), pool, x_int,
+                                          C.mv_tbuf.get());
+    HM_CHECK_LAUNCH();
+    k_mv_large_u<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), (int64_t)C.mv_tiles_u.n, C.mv_large.get(), pool,
+                                          C.mv_tbuf.get(), y_int);
     HM_CHECK_LAUNCH();
   }
   if (C.world > 1) allreduce_sum(C, y_int, C.N);
