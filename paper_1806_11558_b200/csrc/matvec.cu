@@ -7,9 +7,9 @@
 //   small leaves   (dense blocks and low-rank blocks with (m+n)k*8 <= 16 KiB, ~all leaves):
 //                  k_mv_batched — one persistent CTA per SM walks a contiguous, byte-balanced
 //                  range of "batches" (runs of consecutive leaves whose storage is contiguous,
-//                  <= 40 KiB).  One elected thread streams each batch into shared memory with a
+//                  <= 44 KiB).  One elected thread streams each batch into shared memory with a
 //                  single cp.async.bulk (TMA bulk copy, mbarrier completion), 4 stages deep, so
-//                  ~160 KiB per SM are in flight while the 12 warps compute the previous
+//                  ~176 KiB per SM are in flight while the 16 warps compute the previous
 //                  batches out of shared memory: dense rows with s lanes per row, low-rank
 //                  t = V^T x then y += U t.  One FP64 atomic per row into the L2-resident y.
 //   large low-rank (the few blocks above 16 KiB): two tiled kernels with direct coalesced
@@ -25,8 +25,8 @@
 namespace hm {
 
 constexpr int kMvStages = 4;
-constexpr int kMvStageBytes = 40 * 1024;
-constexpr int kMvThreads = 384;
+constexpr int kMvStageBytes = 44 * 1024;
+constexpr int kMvThreads = 512;
 constexpr int kMvSmallMax = 16 * 1024;
 
 namespace {
@@ -69,52 +69,83 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
-template <int S>
-__device__ __forceinline__ void dense_rows(const double* __restrict__ B, int m, int n, const double* __restrict__ x,
-                                           double* __restrict__ y, int lane) {
-  constexpr int RPP = 32 / S;   // rows per pass
+// Dense m x n row-major block: S lanes per row (consecutive columns -> conflict-free shared
+// loads for the leaf widths of CBC), 32/S rows per pass, P passes held in registers so the
+// P shuffle reductions are independent (ILP instead of P serial reduction chains).
+template <int S, int P>
+__device__ __forceinline__ void dense_block(const double* __restrict__ B, int m, int n, const double* __restrict__ x,
+                                            double* __restrict__ y, int lane) {
+  constexpr int RPP = 32 / S;
   const int sub = lane % S, rr = lane / S;
-  for (int r0 = 0; r0 < m; r0 += RPP) {
-    const int r = r0 + rr;
-    double acc = 0.0;
-    if (r < m) {
-      const double* row = B + r * n;
-      for (int c = sub; c < n; c += S) acc += row[c] * __ldg(x + c);
+  for (int r0 = 0; r0 < m; r0 += RPP * P) {
+    double acc[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) acc[p] = 0.0;
+    for (int c = sub; c < n; c += S) {
+      const double xc = __ldg(x + c);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int r = r0 + rr + p * RPP;
+        if (r < m) acc[p] += B[r * n + c] * xc;
+      }
     }
 #pragma unroll
-    for (int o = S / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (sub == 0 && r < m) atomicAdd(y + r, acc);
+    for (int o = S / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int p = 0; p < P; ++p) acc[p] += __shfl_xor_sync(0xffffffffu, acc[p], o);
+    if (sub == 0)
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int r = r0 + rr + p * RPP;
+        if (r < m) atomicAdd(y + r, acc[p]);
+      }
   }
 }
 
 __device__ __forceinline__ void dense_any(const double* B, int m, int n, const double* x, double* y, int lane) {
-  if (n <= 8) dense_rows<2>(B, m, n, x, y, lane);
-  else if (n <= 16) dense_rows<4>(B, m, n, x, y, lane);
-  else if (n <= 48) dense_rows<8>(B, m, n, x, y, lane);
-  else if (n <= 96) dense_rows<16>(B, m, n, x, y, lane);
-  else dense_rows<32>(B, m, n, x, y, lane);
+  if (n <= 16) dense_block<2, 4>(B, m, n, x, y, lane);
+  else if (n <= 48) dense_block<4, 4>(B, m, n, x, y, lane);
+  else if (n <= 96) dense_block<8, 4>(B, m, n, x, y, lane);
+  else dense_block<32, 2>(B, m, n, x, y, lane);
 }
 
-// low-rank block from shared memory: U (m x k) then V (n x k), column-major
-__device__ __forceinline__ void lowrank_smem(const double* __restrict__ U, int m, int n, int k,
-                                             const double* __restrict__ x, double* __restrict__ y,
-                                             double* __restrict__ tsh, int lane) {
-  const double* V = U + m * k;
-  for (int l = 0; l < k; ++l) {
-    const double* v = V + l * n;
-    double acc = 0.0;
-    for (int j = lane; j < n; j += 32) acc += v[j] * __ldg(x + j);
+// Low-rank block U (m x k) | V (n x k), column-major: t = V^T x with all k column sums in
+// registers (x_j loaded once, k independent loads per row j), one butterfly reduction over
+// the k sums at once, then y += U t (k independent loads per row).
+// columns [l0, l0 + kc) of the block (kc <= KB); k > 32 is processed in column groups
+template <int KB>
+__device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int m, int n, int k, int l0, int kc,
+                                              const double* __restrict__ x, double* __restrict__ y, int lane) {
+  const double* V = U0 + (int64_t)m * k + (int64_t)l0 * n;
+  const double* U = U0 + (int64_t)l0 * m;
+  double acc[KB];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) tsh[l] = acc;
+  for (int l = 0; l < KB; ++l) acc[l] = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    const double xj = __ldg(x + j);
+#pragma unroll
+    for (int l = 0; l < KB; ++l)
+      if (l < kc) acc[l] += V[j + (int64_t)l * n] * xj;
   }
-  __syncwarp();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int l = 0; l < KB; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], o);
   for (int t = lane; t < m; t += 32) {
-    double acc = 0.0;
-    for (int l = 0; l < k; ++l) acc += U[t + l * m] * tsh[l];
-    atomicAdd(y + t, acc);
+    double s = 0.0;
+#pragma unroll
+    for (int l = 0; l < KB; ++l)
+      if (l < kc) s += U[t + (int64_t)l * m] * acc[l];
+    atomicAdd(y + t, s);
   }
-  __syncwarp();
+}
+
+__device__ __forceinline__ void lowrank_any(const double* U, int m, int n, int k, const double* x, double* y,
+                                            int lane) {
+  if (k <= 8) lowrank_block<8>(U, m, n, k, 0, k, x, y, lane);
+  else if (k <= 16) lowrank_block<16>(U, m, n, k, 0, k, x, y, lane);
+  else
+    for (int l0 = 0; l0 < k; l0 += 32) lowrank_block<32>(U, m, n, k, l0, min(32, k - l0), x, y, lane);
 }
 
 __global__ void __launch_bounds__(kMvThreads, 1)
@@ -123,8 +154,7 @@ __global__ void __launch_bounds__(kMvThreads, 1)
                  const double* __restrict__ x, double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  double* tsh = reinterpret_cast<double*>(smem + 128);                 // [warps][64]
-  unsigned char* buf = smem + 128 + (kMvThreads / 32) * 64 * sizeof(double);
+  unsigned char* buf = smem + 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = cta_first[blockIdx.x], nb = cta_first[blockIdx.x + 1] - b0;
   if (threadIdx.x == 0) {
@@ -148,7 +178,7 @@ __global__ void __launch_bounds__(kMvThreads, 1)
       const MvTask T = tasks[B.first + t];
       const int m = T.mnk & 2047, n = (T.mnk >> 11) & 2047, k = T.mnk >> 22;
       if (k == 0) dense_any(data + T.loff, m, n, x + T.clo, y + T.rlo, lane);
-      else lowrank_smem(data + T.loff, m, n, k, x + T.clo, y + T.rlo, tsh + warp * 64, lane);
+      else lowrank_any(data + T.loff, m, n, k, x + T.clo, y + T.rlo, lane);
     }
     __syncthreads();                                   // stage fully consumed
     if (threadIdx.x == 0 && it + kMvStages < nb) {
@@ -158,36 +188,50 @@ __global__ void __launch_bounds__(kMvThreads, 1)
   }
 }
 
-// large low-rank blocks, phase 1: t[toff + l] += sum_{j in tile} V[j, l] x[clo + j]
+// large low-rank blocks, phase 1: t[toff + l] += sum_{j in tile} V[j, l] x[clo + j] for all l
+// (tile = 1024 consecutive rows j of V, every column; x_j loaded once per row)
+template <int KB>
+__device__ __forceinline__ void large_v_tile(const MvLarge& B, const MvTileV& T, const double* __restrict__ pool,
+                                             const double* __restrict__ x, double* __restrict__ tbuf,
+                                             double (*part)[64]) {
+  const int l0 = T.l, kc = min(KB, B.k - T.l);
+  const double* V = pool + B.off + (int64_t)B.m * B.k + (int64_t)l0 * B.n;
+  double acc[KB];
+#pragma unroll
+  for (int l = 0; l < KB; ++l) acc[l] = 0.0;
+  for (int j = T.j0 + threadIdx.x; j < T.j1; j += 256) {
+    const double xj = __ldg(x + B.clo + j);
+#pragma unroll
+    for (int l = 0; l < KB; ++l)
+      if (l < kc) acc[l] += __ldg(V + j + (int64_t)l * B.n) * xj;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int l = 0; l < KB; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int l = 0; l < KB; ++l) part[w][l] = acc[l];
+  __syncthreads();
+  if (threadIdx.x < kc) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += part[q][threadIdx.x];
+    atomicAdd(tbuf + B.toff + l0 + threadIdx.x, s);
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
                                                     const MvLarge* __restrict__ L, const double* __restrict__ pool,
                                                     const double* __restrict__ x, double* __restrict__ tbuf) {
-  __shared__ double part[8];
+  __shared__ double part[8][64];
   for (int64_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
     const MvTileV T = tiles[i];
     const MvLarge B = L[T.blk];
-    const double* v = pool + B.off + (int64_t)B.m * B.k + (int64_t)T.l * B.n;
-    const double* xs = x + B.clo;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int j = T.j0 + threadIdx.x;
-    for (; j + 768 < T.j1; j += 1024) {
-      a0 += __ldg(v + j) * __ldg(xs + j);
-      a1 += __ldg(v + j + 256) * __ldg(xs + j + 256);
-      a2 += __ldg(v + j + 512) * __ldg(xs + j + 512);
-      a3 += __ldg(v + j + 768) * __ldg(xs + j + 768);
-    }
-    for (; j < T.j1; j += 256) a0 += __ldg(v + j) * __ldg(xs + j);
-    double acc = (a0 + a1) + (a2 + a3);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < 8; ++w) s += part[w];
-      atomicAdd(tbuf + B.toff + T.l, s);
-    }
-    __syncthreads();
+    if (B.k <= 8) large_v_tile<8>(B, T, pool, x, tbuf, part);
+    else if (B.k <= 16) large_v_tile<16>(B, T, pool, x, tbuf, part);
+    else large_v_tile<32>(B, T, pool, x, tbuf, part);
   }
 }
 
@@ -203,9 +247,14 @@ __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ 
     __syncthreads();
     const double* U = pool + B.off;
     for (int t = T.t0 + threadIdx.x; t < T.t1; t += 256) {
-      double acc = 0.0;
-      for (int l = 0; l < B.k; ++l) acc += __ldg(U + t + (int64_t)l * B.m) * tl[l];
-      atomicAdd(y + B.rlo + t, acc);
+      double s0 = 0.0, s1 = 0.0;
+      int l = 0;
+      for (; l + 1 < B.k; l += 2) {
+        s0 += __ldg(U + t + (int64_t)l * B.m) * tl[l];
+        s1 += __ldg(U + t + (int64_t)(l + 1) * B.m) * tl[l + 1];
+      }
+      if (l < B.k) s0 += __ldg(U + t + (int64_t)l * B.m) * tl[l];
+      atomicAdd(y + B.rlo + t, s0 + s1);
     }
     __syncthreads();
   }
@@ -316,9 +365,9 @@ void plan_matvec(Context& C) {
   std::vector<MvTileU> tu;
   for (size_t i = 0; i < large.size(); ++i) {
     const MvLarge& B = large[i];
-    for (int l = 0; l < B.k; ++l)
-      for (int j0 = 0; j0 < B.n; j0 += 4096) tv.push_back(MvTileV{(int32_t)i, l, j0, std::min(B.n, j0 + 4096)});
-    const int rows = std::max(32, 4096 / B.k);
+    for (int l0 = 0; l0 < B.k; l0 += (B.k <= 16 ? 16 : 32))
+      for (int j0 = 0; j0 < B.n; j0 += 1024) tv.push_back(MvTileV{(int32_t)i, l0, j0, std::min(B.n, j0 + 1024)});
+    const int rows = 1024;
     for (int t0 = 0; t0 < B.m; t0 += rows) tu.push_back(MvTileU{(int32_t)i, t0, std::min(B.m, t0 + rows), 0});
   }
   auto up = [&](auto& dbuf, const auto& v) {
@@ -342,7 +391,7 @@ void plan_matvec(Context& C) {
   HM_CUDA(cudaStreamSynchronize(st));
   static bool attr = false;
   if (!attr) {
-    const int smem = 128 + (kMvThreads / 32) * 64 * 8 + kMvStages * kMvStageBytes;
+    const int smem = 128 + kMvStages * kMvStageBytes;
     HM_CUDA(cudaFuncSetAttribute(k_mv_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
@@ -365,7 +414,7 @@ void matvec_internal(Context& C, const double* x_int, double* y_int) {
   if (C.mv_tlen) HM_CUDA(cudaMemsetAsync(C.mv_tbuf.get(), 0, C.mv_tlen * sizeof(double), st));
   const double* pool = (const double*)C.fpool.base;
   if (C.mv_nbatches) {
-    const int smem = 128 + (kMvThreads / 32) * 64 * 8 + kMvStages * kMvStageBytes;
+    const int smem = 128 + kMvStages * kMvStageBytes;
     k_mv_batched<<<C.mv_grid, kMvThreads, smem, st>>>(C.mv_batches.get(), C.mv_cta.get(), C.mv_tasks.get(),
                                                        (const char*)C.dstore.get(), (const char*)pool, x_int, y_int);
     HM_CHECK_LAUNCH();

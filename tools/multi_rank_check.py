@@ -1,0 +1,80 @@
+"""Multi-GPU parity check (run with torchrun, one process per GPU, NCCL).
+
+Every rank builds the same tree and owns a contiguous cost-balanced slice of both leaf
+lists; the matvec's partial products are all-reduced.  Checks:
+  * owned ranges of all ranks are disjoint and cover both lists (gathered to rank 0);
+  * the p-rank H-matvec equals a 1-rank H-matvec built on rank 0's GPU to 1e-13 relative
+    (same leaves, same factors; only the summation order of the global sum differs, A19);
+  * the p-rank GMRES solution equals the 1-rank solution to 1e-10 relative.
+Prints one JSON line on rank 0 and exits non-zero on failure.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from inputs.meshes import config_mesh, seeded_vector
+from paper_1806_11558_b200 import HMatrix, hm
+
+
+def main():
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = [hm.hm_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    V, T = config_mesh(cfg)
+    N = T.shape[0]
+    H = HMatrix(device=local, rank=rank, world_size=world, nccl_unique_id=obj[0])
+    H.build_tree(V, T)
+    H.setup(1e-6)
+    st = H.stats()
+    x = torch.from_numpy(seeded_vector(N, 3)).cuda()
+    y = H.matvec(x)
+    f = torch.from_numpy(H.assemble_rhs(1)).cuda()
+    sol, it, rr = H.solve(f, 1e-10)
+    torch.cuda.synchronize()
+    own = torch.tensor(st["adm_owned"] + st["dense_owned"], dtype=torch.int64, device="cuda")
+    allown = [torch.zeros_like(own) for _ in range(world)]
+    dist.all_gather(allown, own)
+    setup_ms = torch.tensor([st["setup_ms"]], dtype=torch.float64, device="cuda")
+    dist.all_reduce(setup_ms, op=dist.ReduceOp.MAX)
+    ok = True
+    res = {"config": cfg, "world": world, "N": N}
+    if rank == 0:
+        ranges = np.array([a.cpu().numpy() for a in allown])
+        for col, total in ((0, st["adm_leaves"]), (2, st["dense_leaves"])):
+            b = ranges[:, col:col + 2]
+            cover = b[0, 0] == 0 and b[-1, 1] == total and all(b[r, 1] == b[r + 1, 0] for r in range(world - 1))
+            ok &= bool(cover)
+        res["owned_ranges"] = ranges.tolist()
+        R = HMatrix(device=local)                 # 1-rank reference on the same GPU
+        R.build_tree(V, T)
+        R.setup(1e-6)
+        y1 = R.matvec(x)
+        s1, it1, rr1 = R.solve(f, 1e-10)
+        torch.cuda.synchronize()
+        dy = (torch.linalg.norm(y - y1) / torch.linalg.norm(y1)).item()
+        ds = (torch.linalg.norm(sol - s1) / torch.linalg.norm(s1)).item()
+        res.update({"matvec_rel_diff": dy, "solve_rel_diff": ds, "iters": it, "iters_1rank": it1,
+                    "setup_ms_max": setup_ms.item(), "setup_ms_1rank": R.stats()["setup_ms"]})
+        ok &= dy <= 1e-13 and ds <= 1e-10
+        res["ok"] = bool(ok)
+        print(json.dumps(res), flush=True)
+        R.close()
+    H.close()
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.broadcast(flag, 0)
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() else 1)
+
+
+if __name__ == "__main__":
+    main()
