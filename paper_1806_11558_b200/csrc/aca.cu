@@ -266,8 +266,25 @@ struct AcaWork {
   DBuf<double> Uw, Vw;
   DBuf<uint32_t> bmap;
   DBuf<char> tmp;
-  DBuf<unsigned long long> ev;
+  DBuf<unsigned long long> ev, cnt;
+  DBuf<EntryRef> lists;
 };
+
+// one batch of residual entries: order-3 in place, then the order-4 list, then the rest
+template <class M>
+void aca_eval(Context& C, const M& m, int64_t total, AcaWork& W) {
+  if (total <= 0) return;
+  cudaStream_t st = C.stream;
+  W.cnt.alloc(2);
+  HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 2 * sizeof(unsigned long long), st));
+  k_eval_class3<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.lists.get(), W.cnt.get(), W.ev.get());
+  HM_CHECK_LAUNCH();
+  const unsigned g = (unsigned)std::min<int64_t>(grid_for(total, 128), 148 * 16);
+  k_eval_list<4, M><<<g, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
+  HM_CHECK_LAUNCH();
+  k_eval_rest<M><<<std::min<unsigned>(g, 148 * 4), 128, 0, st>>>(m, W.lists.get(), total, W.cnt.get(), W.ev.get());
+  HM_CHECK_LAUNCH();
+}
 
 // Run ACA on the owned admissible leaves listed in `ids` (indices into the owned list) with
 // `kws` workspace columns; appends blocks that overflowed to `overflow`.
@@ -315,14 +332,11 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     if (tot[0] == 0) break;
     C.aca_steps++;
     C.entries_aca += (double)(tot[0] + tot[1]);
-    k_eval_fused<<<grid_for(tot[0], 256), 256, 0, st>>>(
-        AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), nb, W.Uw.get(), W.Vw.get()}, tot[0], W.ev.get());
-    HM_CHECK_LAUNCH();
+    W.lists.alloc(std::max(tot[0], tot[1]));
+    aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), nb, W.Uw.get(), W.Vw.get()}, tot[0], W);
     k_aca_pivot<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Vw.get(), W.bmap.get());
     HM_CHECK_LAUNCH();
-    k_eval_fused<<<grid_for(tot[1], 256), 256, 0, st>>>(
-        AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), nb, W.Uw.get(), W.Vw.get()}, tot[1], W.ev.get());
-    HM_CHECK_LAUNCH();
+    aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), nb, W.Uw.get(), W.Vw.get()}, tot[1], W);
     k_aca_update<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Uw.get(), W.Vw.get(),
                                                          W.bmap.get(), W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();

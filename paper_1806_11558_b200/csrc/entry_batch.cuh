@@ -168,6 +168,89 @@ __global__ void __launch_bounds__(256) k_eval_fused(M m, int64_t total, unsigned
   if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
 }
 
+// Three-kernel, host-sync-free variant for ACA rows / columns (nearly all entries are order 3,
+// most of the rest order 4):
+//   k_eval_class3   evaluates the order-3 entries in place (others exit at once) and appends
+//                   order-4 references to the front of `lists`, all other classes to the back;
+//   k_eval_list<4>  persistent grid-stride over the order-4 list (count read on the device);
+//   k_eval_rest     persistent, in-CTA class sort of the remaining few.
+template <class M>
+__global__ void __launch_bounds__(128) k_eval_class3(M m, int64_t total, EntryRef* __restrict__ lists,
+                                                     unsigned long long* __restrict__ cnt /* [n4, nrest] */,
+                                                     unsigned long long* __restrict__ evals) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  EntryRef r;
+  int cls = -1, xs = 0, ys = 0;
+  if (m.locate(e, e < total, r)) {
+    int s, t;
+    m.pair(r, s, t);
+    cls = canonical_class(m.P, s, t, xs, ys);
+  }
+  const unsigned mask = __activemask();
+  const int lane = threadIdx.x & 31;
+  // warp-aggregated appends: order 4 at the front, everything else (not 3) at the back
+  const unsigned b4 = __ballot_sync(mask, cls == 4), br = __ballot_sync(mask, cls >= 0 && cls != 3 && cls != 4);
+  unsigned long long base4 = 0, baser = 0;
+  if (lane == 0) {
+    if (b4) base4 = atomicAdd(&cnt[0], (unsigned long long)__popc(b4));
+    if (br) baser = atomicAdd(&cnt[1], (unsigned long long)__popc(br));
+  }
+  base4 = __shfl_sync(mask, base4, 0);
+  baser = __shfl_sync(mask, baser, 0);
+  const unsigned below = (1u << lane) - 1u;
+  if (cls == 4) lists[base4 + __popc(b4 & below)] = r;
+  else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
+  unsigned long long ev = 0;
+  if (cls == 3) {
+    double X[9], Y[9];
+    load_panel_vertices(m.P, xs, X);
+    load_panel_vertices(m.P, ys, Y);
+    const double I = regular_sum<3>(X, Y);
+    m.put(r, dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi));
+    ev = 81;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(mask, ev, o);
+  if (lane == 0 && ev) atomicAdd(evals, ev);
+}
+
+template <int n, class M>
+__global__ void __launch_bounds__(128) k_eval_list(M m, const EntryRef* __restrict__ list,
+                                                   const unsigned long long* __restrict__ cnt,
+                                                   unsigned long long* __restrict__ evals) {
+  const int64_t c = (int64_t)*cnt;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < c; k += (int64_t)gridDim.x * blockDim.x) {
+    const EntryRef r = list[k];
+    int s, t, xs, ys;
+    m.pair(r, s, t);
+    canonical_class(m.P, s, t, xs, ys);
+    double X[9], Y[9];
+    load_panel_vertices(m.P, xs, X);
+    load_panel_vertices(m.P, ys, Y);
+    const double I = regular_sum<n>(X, Y);
+    m.put(r, dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(evals, (unsigned long long)(n * n * n * n) * (unsigned long long)c);
+}
+
+// the rare rest (orders 5, 6 and touching pairs), read from the back of `lists`
+template <class M>
+__global__ void __launch_bounds__(128) k_eval_rest(M m, const EntryRef* __restrict__ lists, int64_t total,
+                                                   const unsigned long long* __restrict__ cnt,
+                                                   unsigned long long* __restrict__ evals) {
+  const int64_t c = (int64_t)cnt[1];
+  unsigned long long ev = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < c; k += (int64_t)gridDim.x * blockDim.x) {
+    const EntryRef r = lists[total - 1 - k];
+    int s, t, xs, ys;
+    m.pair(r, s, t);
+    const int cls = canonical_class(m.P, s, t, xs, ys);
+    m.put(r, entry_st(m.P, s, t));
+    ev += (unsigned long long)rule_evals(cls);
+  }
+  if (ev) atomicAdd(evals, ev);
+}
+
 struct EntryBatchWork {
   DBuf<unsigned long long> cnt, cursor;
   DBuf<EntryRef> list;

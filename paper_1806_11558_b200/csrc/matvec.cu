@@ -8,13 +8,14 @@
 //                  k_mv_batched — one persistent CTA per SM walks a contiguous, byte-balanced
 //                  range of "batches" (runs of consecutive leaves whose storage is contiguous,
 //                  <= 44 KiB).  One elected thread streams each batch into shared memory with a
-//                  single cp.async.bulk (TMA bulk copy, mbarrier completion), 4 stages deep, so
-//                  ~176 KiB per SM are in flight while the 16 warps compute the previous
-//                  batches out of shared memory: dense rows with s lanes per row, low-rank
-//                  t = V^T x then y += U t.  One FP64 atomic per row into the L2-resident y.
-//   large low-rank (the few blocks above 16 KiB): two tiled kernels with direct coalesced
-//                  loads, k_mv_large_v (t += V^T x per column tile, atomics into t) then
-//                  k_mv_large_u (y += U t, k independent loads per row).
+//                  single cp.async.bulk (TMA bulk copy, mbarrier completion), 4 stages deep
+//                  (~176 KiB per SM in flight); warp 0 produces, 15 consumer warps compute
+//                  the staged batches out of shared memory (dense rows with s lanes per row,
+//                  low-rank t = V^T x then y += U t), releasing each stage through an "empty"
+//                  mbarrier.  One FP64 atomic per row into the L2-resident y.
+//   large low-rank (blocks above 16 KiB): two barrier-free warp-task kernels with direct
+//                  coalesced loads, k_mv_large_v (t += V^T x over 8-column x 2048-row tiles,
+//                  atomics into t) then k_mv_large_u (y += U t, k independent loads per row).
 //   dense blocks too big for a stage (only with large leaf_size): k_mv_dense_direct.
 #include <cub/cub.cuh>
 
@@ -148,115 +149,118 @@ __device__ __forceinline__ void lowrank_any(const double* U, int m, int n, int k
     for (int l0 = 0; l0 < k; l0 += 32) lowrank_block<32>(U, m, n, k, l0, min(32, k - l0), x, y, lane);
 }
 
+// Warp-specialised pipeline: warp 0 is the producer (one lane issues the bulk copies, waits
+// on the per-stage "empty" barrier before reusing a stage); warps 1..NW-1 consume every stage
+// (tasks round-robin), then arrive on its "empty" barrier.  A slow task delays only the refill
+// of its own stage, not the other consumers.
 __global__ void __launch_bounds__(kMvThreads, 1)
     k_mv_batched(const MvBatch* __restrict__ batches, const int32_t* __restrict__ cta_first,
                  const MvTask* __restrict__ tasks, const char* __restrict__ base0, const char* __restrict__ base1,
                  const double* __restrict__ x, double* __restrict__ y) {
+  constexpr int NW = kMvThreads / 32, NC = NW - 1;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMvStages;
   unsigned char* buf = smem + 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = cta_first[blockIdx.x], nb = cta_first[blockIdx.x + 1] - b0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kMvStages; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < kMvStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NC);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](int it, int stage) {
-    const MvBatch B = batches[b0 + it];
-    mbar_expect_tx(&bar[stage], (unsigned)B.bytes);
-    bulk_g2s(buf + stage * kMvStageBytes, (B.base ? base1 : base0) + B.src, (unsigned)B.bytes, &bar[stage]);
-  };
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kMvStages && s < nb; ++s) issue(s, s);
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int it = 0; it < nb; ++it) {
+        const int stage = it % kMvStages;
+        if (it >= kMvStages) mbar_wait(&empty[stage], (unsigned)(((it / kMvStages) - 1) & 1));
+        const MvBatch B = batches[b0 + it];
+        mbar_expect_tx(&full[stage], (unsigned)B.bytes);
+        bulk_g2s(buf + stage * kMvStageBytes, (B.base ? base1 : base0) + B.src, (unsigned)B.bytes, &full[stage]);
+      }
+    }
+    return;
+  }
   for (int it = 0; it < nb; ++it) {
     const int stage = it % kMvStages;
-    mbar_wait(&bar[stage], (unsigned)((it / kMvStages) & 1));
+    mbar_wait(&full[stage], (unsigned)((it / kMvStages) & 1));
     const MvBatch B = batches[b0 + it];
     const double* data = reinterpret_cast<const double*>(buf + stage * kMvStageBytes);
-    for (int t = warp; t < B.count; t += kMvThreads / 32) {
+    for (int t = warp - 1; t < B.count; t += NC) {
       const MvTask T = tasks[B.first + t];
       const int m = T.mnk & 2047, n = (T.mnk >> 11) & 2047, k = T.mnk >> 22;
       if (k == 0) dense_any(data + T.loff, m, n, x + T.clo, y + T.rlo, lane);
       else lowrank_any(data + T.loff, m, n, k, x + T.clo, y + T.rlo, lane);
     }
-    __syncthreads();                                   // stage fully consumed
-    if (threadIdx.x == 0 && it + kMvStages < nb) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(it + kMvStages, stage);
-    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[stage])) : "memory");
   }
 }
 
-// large low-rank blocks, phase 1: t[toff + l] += sum_{j in tile} V[j, l] x[clo + j] for all l
-// (tile = 1024 consecutive rows j of V, every column; x_j loaded once per row)
-template <int KB>
-__device__ __forceinline__ void large_v_tile(const MvLarge& B, const MvTileV& T, const double* __restrict__ pool,
-                                             const double* __restrict__ x, double* __restrict__ tbuf,
-                                             double (*part)[64]) {
-  const int l0 = T.l, kc = min(KB, B.k - T.l);
-  const double* V = pool + B.off + (int64_t)B.m * B.k + (int64_t)l0 * B.n;
-  double acc[KB];
-#pragma unroll
-  for (int l = 0; l < KB; ++l) acc[l] = 0.0;
-  for (int j = T.j0 + threadIdx.x; j < T.j1; j += 256) {
-    const double xj = __ldg(x + B.clo + j);
-#pragma unroll
-    for (int l = 0; l < KB; ++l)
-      if (l < kc) acc[l] += __ldg(V + j + (int64_t)l * B.n) * xj;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int l = 0; l < KB; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], o);
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0)
-#pragma unroll
-    for (int l = 0; l < KB; ++l) part[w][l] = acc[l];
-  __syncthreads();
-  if (threadIdx.x < kc) {
-    double s = 0.0;
-    for (int q = 0; q < 8; ++q) s += part[q][threadIdx.x];
-    atomicAdd(tbuf + B.toff + l0 + threadIdx.x, s);
-  }
-  __syncthreads();
-}
-
+// Large low-rank blocks (storage > 16 KiB), barrier-free warp tasks with direct coalesced loads.
+// Phase 1, tile = (block, 8 columns l0.., 2048 rows j0..): t[l] += sum_j V[j, l] x[clo + j];
+// each lane keeps 8 column sums (x_j loaded once per row, 8 independent loads in flight).
 __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
                                                     const MvLarge* __restrict__ L, const double* __restrict__ pool,
                                                     const double* __restrict__ x, double* __restrict__ tbuf) {
-  __shared__ double part[8][64];
-  for (int64_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < ntiles; i += nw) {
     const MvTileV T = tiles[i];
     const MvLarge B = L[T.blk];
-    if (B.k <= 8) large_v_tile<8>(B, T, pool, x, tbuf, part);
-    else if (B.k <= 16) large_v_tile<16>(B, T, pool, x, tbuf, part);
-    else large_v_tile<32>(B, T, pool, x, tbuf, part);
+    const int kc = min(8, B.k - T.l);
+    const double* V = pool + B.off + (int64_t)B.m * B.k + (int64_t)T.l * B.n;
+    const double* xs = x + B.clo;
+    double acc[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) acc[l] = 0.0;
+    for (int j = T.j0 + lane; j < T.j1; j += 32) {
+      const double xj = __ldg(xs + j);
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < kc) acc[l] += __ldg(V + j + (int64_t)l * B.n) * xj;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int l = 0; l < 8; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], o);
+    if (lane < kc) {
+      double v = acc[0];
+#pragma unroll
+      for (int l = 1; l < 8; ++l) v = lane == l ? acc[l] : v;
+      atomicAdd(tbuf + B.toff + T.l + lane, v);
+    }
   }
 }
 
-// large low-rank blocks, phase 2: y[rlo + t] += sum_l U[t, l] t_l over a row tile
+// Phase 2, tile = (block, 256 rows t0..): y[rlo + t] += sum_l U[t, l] t_l (k independent loads per row)
 __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ tiles, int64_t ntiles,
                                                     const MvLarge* __restrict__ L, const double* __restrict__ pool,
                                                     const double* __restrict__ tbuf, double* __restrict__ y) {
-  __shared__ double tl[64];
-  for (int64_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < ntiles; i += nw) {
     const MvTileU T = tiles[i];
     const MvLarge B = L[T.blk];
-    if (threadIdx.x < B.k) tl[threadIdx.x] = tbuf[B.toff + threadIdx.x];
-    __syncthreads();
     const double* U = pool + B.off;
-    for (int t = T.t0 + threadIdx.x; t < T.t1; t += 256) {
-      double s0 = 0.0, s1 = 0.0;
+    const double* tl = tbuf + B.toff;
+    for (int t = T.t0 + lane; t < T.t1; t += 32) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       int l = 0;
-      for (; l + 1 < B.k; l += 2) {
-        s0 += __ldg(U + t + (int64_t)l * B.m) * tl[l];
-        s1 += __ldg(U + t + (int64_t)(l + 1) * B.m) * tl[l + 1];
+      for (; l + 3 < B.k; l += 4) {
+        s0 += __ldg(U + t + (int64_t)l * B.m) * __ldg(tl + l);
+        s1 += __ldg(U + t + (int64_t)(l + 1) * B.m) * __ldg(tl + l + 1);
+        s2 += __ldg(U + t + (int64_t)(l + 2) * B.m) * __ldg(tl + l + 2);
+        s3 += __ldg(U + t + (int64_t)(l + 3) * B.m) * __ldg(tl + l + 3);
       }
-      if (l < B.k) s0 += __ldg(U + t + (int64_t)l * B.m) * tl[l];
-      atomicAdd(y + B.rlo + t, s0 + s1);
+      for (; l < B.k; ++l) s0 += __ldg(U + t + (int64_t)l * B.m) * __ldg(tl + l);
+      atomicAdd(y + B.rlo + t, (s0 + s1) + (s2 + s3));
     }
-    __syncthreads();
   }
 }
 
@@ -365,9 +369,9 @@ void plan_matvec(Context& C) {
   std::vector<MvTileU> tu;
   for (size_t i = 0; i < large.size(); ++i) {
     const MvLarge& B = large[i];
-    for (int l0 = 0; l0 < B.k; l0 += (B.k <= 16 ? 16 : 32))
-      for (int j0 = 0; j0 < B.n; j0 += 1024) tv.push_back(MvTileV{(int32_t)i, l0, j0, std::min(B.n, j0 + 1024)});
-    const int rows = 1024;
+    for (int l0 = 0; l0 < B.k; l0 += 8)
+      for (int j0 = 0; j0 < B.n; j0 += 2048) tv.push_back(MvTileV{(int32_t)i, l0, j0, std::min(B.n, j0 + 2048)});
+    const int rows = 256;
     for (int t0 = 0; t0 < B.m; t0 += rows) tu.push_back(MvTileU{(int32_t)i, t0, std::min(B.m, t0 + rows), 0});
   }
   auto up = [&](auto& dbuf, const auto& v) {
