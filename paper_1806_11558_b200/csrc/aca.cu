@@ -20,8 +20,6 @@
 
 namespace hm {
 
-namespace {
-
 struct AcaBlk {
   Quad q;
   int32_t m, n, kmax, pad;
@@ -33,6 +31,20 @@ struct AcaState {
   int32_t skip, pad0;
   double S2, vv;
 };
+
+struct AcaWork {
+  DBuf<AcaBlk> blk;
+  DBuf<AcaState> state;
+  DBuf<int32_t> owned, piv;
+  DBuf<int64_t> rsz, csz, rpre, cpre;
+  DBuf<double> Uw, Vw;
+  DBuf<uint32_t> bmap;
+  DBuf<char> tmp;
+  DBuf<unsigned long long> ev, cnt;
+  DBuf<EntryRef> lists;
+};
+
+namespace {
 
 __global__ void k_step_sizes(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S, int64_t nb,
                              int64_t* __restrict__ rsz, int64_t* __restrict__ csz) {
@@ -258,17 +270,7 @@ void cub_call(DBuf<char>& tmp, F&& f) {
   HM_CUDA(f(tmp.get(), bytes));
 }
 
-struct AcaWork {
-  DBuf<AcaBlk> blk;
-  DBuf<AcaState> state;
-  DBuf<int32_t> owned, piv;
-  DBuf<int64_t> rsz, csz, rpre, cpre;
-  DBuf<double> Uw, Vw;
-  DBuf<uint32_t> bmap;
-  DBuf<char> tmp;
-  DBuf<unsigned long long> ev, cnt;
-  DBuf<EntryRef> lists;
-};
+
 
 // one batch of residual entries: order-3 in place, then the order-4 list, then the rest
 template <class M>
@@ -374,11 +376,13 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
 
 }  // namespace
 
+
+
 void setup_aca(Context& C) {
   cudaStream_t st = C.stream;
   const int64_t nb = C.adm_end - C.adm_begin;
-  C.foff.alloc_exact(nb + 1);
-  C.frank.alloc_exact(nb + 1);
+  C.foff.alloc(nb + 1);
+  C.frank.alloc(nb + 1);
   HM_CUDA(cudaMemsetAsync(C.frank.get(), 0, (nb + 1) * sizeof(int32_t), st));
   C.fpool.used = 0;
   C.aca_steps = 0; C.aca_chunks = 0; C.aca_overflow = 0;
@@ -396,8 +400,11 @@ void setup_aca(Context& C) {
     int64_t m = q.rhi - q.rlo, n = q.chi - q.clo;
     worst += (size_t)std::min<int64_t>(std::min(m, n), C.k_max) * (m + n);
   }
-  C.fpool.init(C.device, worst * sizeof(double) + (64u << 20));
-  AcaWork W;
+  const size_t need_va = worst * sizeof(double) + (64u << 20);
+  if (!C.fpool.base || C.fpool.reserved < need_va) C.fpool.init(C.device, need_va);   // else reuse the mapped pool
+  C.fpool.used = 0;
+  if (!C.aca_ws) C.aca_ws = std::make_shared<AcaWork>();
+  AcaWork& W = *C.aca_ws;
   W.ev.alloc(1);
   HM_CUDA(cudaMemsetAsync(W.ev.get(), 0, sizeof(unsigned long long), st));
   const bool rec = C.N <= 400000;
@@ -405,10 +412,18 @@ void setup_aca(Context& C) {
   pivots.clear();
   if (rec) pivots.resize(nb);
   const int kws = std::max(1, std::min(C.k_max, (int)C.aca_kws));
-  size_t free_b = 0, total_b = 0;
-  HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  // workspace per chunk: the option, capped at a quarter of the free device memory
-  const double budget = std::min(C.aca_chunk_mb * 1048576.0, 0.25 * (double)free_b);
+  // workspace per chunk: the option, capped by the device memory left at the start of the chunk
+  // (the factor pool grows by ~k_mean/KWS of the workspace per chunk, so 0.45 of what is free
+  // plus the current workspace leaves room for it)
+  auto chunk_budget = [&]() {
+    size_t free_b = 0, total_b = 0;
+    HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double ws = 8.0 * (double)(W.Uw.n + W.Vw.n);
+    const double b = std::min(C.aca_chunk_mb * 1048576.0, 0.45 * ((double)free_b + ws));
+    if (ws > b) { W.Uw.release(); W.Vw.release(); }
+    return std::max(b, 64.0 * 1048576.0);
+  };
+  double budget = chunk_budget();
   std::vector<int32_t> ids, overflow;
   double used = 0;
   for (int64_t b = 0; b <= nb; ++b) {
@@ -421,6 +436,7 @@ void setup_aca(Context& C) {
       if (!ids.empty()) {
         run_chunk(C, W, ids, kws, overflow, rec ? &pivots : nullptr);
         C.aca_chunks++;
+        budget = chunk_budget();
       }
       ids.clear();
       used = 0;
@@ -438,7 +454,7 @@ void setup_aca(Context& C) {
         need = 8.0 * C.k_max * ((q.rhi - q.rlo) + (q.chi - q.clo)) + 64.0;
       }
       if (x == overflow.size() || (!part.empty() && u2 + need > budget)) {
-        if (!part.empty()) run_chunk(C, W, part, C.k_max, none, rec ? &pivots : nullptr);
+        if (!part.empty()) { run_chunk(C, W, part, C.k_max, none, rec ? &pivots : nullptr); budget = chunk_budget(); }
         part.clear();
         u2 = 0;
       }

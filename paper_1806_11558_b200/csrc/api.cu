@@ -292,7 +292,6 @@ hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double e
     if (mesh->n_triangles < 1 || mesh->n_triangles > (1LL << 30) || mesh->n_vertices < 3)
       hm::fail(HM_ERR_ARG, "hm_build_tree: bad mesh sizes");
     C.have_setup = false;
-    C.fpool.release();
     Timer t(C);
     hm::build_tree(C, *mesh, leaf_size, eta);
     C.times.tree_ms = t.ms();

@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -123,6 +124,21 @@ struct MvLarge {
 struct MvTileV { int32_t blk, l, j0, j1; };
 struct MvTileU { int32_t blk, t0, t1, pad; };
 
+// Persistent scratch of hm_build_tree (grow-only: reused across calls, no allocation churn)
+struct TreeWs {
+  DBuf<double> cen, area, hh, part, gbox;
+  DBuf<uint64_t> code_sorted, ksorted, admk, denk, fk[2];
+  DBuf<int32_t> idx, flag, scan;
+  DBuf<int2> fr[2];
+  DBuf<Quad> admq, denq;
+  DBuf<unsigned long long> ctr;
+  DBuf<unsigned int> bad;
+  DBuf<int64_t> cost, pref;
+  DBuf<char> tmp;
+};
+struct EntryBatchWork;   // entry_batch.cuh
+struct AcaWork;          // aca.cu
+
 // Timers ----------------------------------------------------------------------------------
 struct PhaseTimes {
   double tree_ms = 0, near_ms = 0, aca_ms = 0, plan_ms = 0, setup_ms = 0;
@@ -196,6 +212,14 @@ struct Context {
   DBuf<double> krylov;         // GMRES basis / CG vectors
   DBuf<double> red;            // reduction scratch
   double* h_red = nullptr;     // pinned host scratch for scalar read-back
+
+  // persistent scratch (grow-only)
+  TreeWs tws;
+  DBuf<int64_t> near_sz;
+  DBuf<char> near_tmp;
+  std::shared_ptr<EntryBatchWork> near_ws;
+  std::shared_ptr<AcaWork> aca_ws;
+  int64_t mv_n_large = 0, mv_n_dense_big = 0, mv_n_tiles_v = 0, mv_n_tiles_u = 0;
 
   PhaseTimes times;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

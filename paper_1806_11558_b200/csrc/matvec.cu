@@ -375,7 +375,7 @@ void plan_matvec(Context& C) {
     for (int t0 = 0; t0 < B.m; t0 += rows) tu.push_back(MvTileU{(int32_t)i, t0, std::min(B.m, t0 + rows), 0});
   }
   auto up = [&](auto& dbuf, const auto& v) {
-    dbuf.alloc_exact(v.size());
+    dbuf.alloc(v.size());
     if (!v.empty())
       HM_CUDA(cudaMemcpyAsync(dbuf.get(), v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, st));
   };
@@ -388,7 +388,11 @@ void plan_matvec(Context& C) {
   up(C.mv_tiles_u, tu);
   C.mv_grid = G;
   C.mv_nbatches = (int64_t)batches.size();
-  C.mv_tbuf.alloc_exact(tl + 1);
+  C.mv_tbuf.alloc(tl + 1);
+  C.mv_n_large = (int64_t)large.size();
+  C.mv_n_dense_big = (int64_t)dense_big.size();
+  C.mv_n_tiles_v = (int64_t)tv.size();
+  C.mv_n_tiles_u = (int64_t)tu.size();
   C.mv_tlen = tl;
   C.n_lr_small = (int64_t)(lr_order.size() - large.size());
   C.n_lr_large = (int64_t)large.size();
@@ -423,16 +427,16 @@ void matvec_internal(Context& C, const double* x_int, double* y_int) {
                                                        (const char*)C.dstore.get(), (const char*)pool, x_int, y_int);
     HM_CHECK_LAUNCH();
   }
-  if (C.mv_dense_big.n) {
-    k_mv_dense_direct<<<148 * 8, 256, 0, st>>>(C.mv_dense_big.get(), (int64_t)C.mv_dense_big.n, C.dstore.get(),
+  if (C.mv_n_dense_big) {
+    k_mv_dense_direct<<<148 * 8, 256, 0, st>>>(C.mv_dense_big.get(), C.mv_n_dense_big, C.dstore.get(),
                                                x_int, y_int);
     HM_CHECK_LAUNCH();
   }
-  if (C.mv_tiles_v.n) {
-    k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), (int64_t)C.mv_tiles_v.n, C.mv_large.get(), pool, x_int,
+  if (C.mv_n_tiles_v) {
+    k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
                                           C.mv_tbuf.get());
     HM_CHECK_LAUNCH();
-    k_mv_large_u<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), (int64_t)C.mv_tiles_u.n, C.mv_large.get(), pool,
+    k_mv_large_u<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
                                           C.mv_tbuf.get(), y_int);
     HM_CHECK_LAUNCH();
   }

@@ -53,15 +53,15 @@ void setup_nearfield(Context& C) {
   cudaStream_t st = C.stream;
   const int64_t nb = C.dense_end - C.dense_begin;
   const Quad* q = C.dense.get() + C.dense_begin;
-  C.doff.alloc_exact(nb + 1);
-  DBuf<int64_t> sz;
+  C.doff.alloc(nb + 1);
+  DBuf<int64_t>& sz = C.near_sz;
   sz.alloc(nb + 1);
   HM_CUDA(cudaMemsetAsync(sz.get(), 0, (nb + 1) * sizeof(int64_t), st));
   if (nb) {
     k_dense_sizes<<<grid_for(nb, 256), 256, 0, st>>>(q, nb, sz.get());
     HM_CHECK_LAUNCH();
   }
-  DBuf<char> tmp;
+  DBuf<char>& tmp = C.near_tmp;
   size_t bytes = 0;
   HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sz.get(), C.doff.get(), nb + 1, st));
   tmp.alloc(bytes);
@@ -71,10 +71,11 @@ void setup_nearfield(Context& C) {
   HM_CUDA(cudaStreamSynchronize(st));
   const int64_t total = hoff[nb];
   C.dense_doubles = total;
-  C.dstore.alloc_exact(total);
+  C.dstore.alloc(total);
   C.evals_near = 0;
   if (total == 0) return;
-  EntryBatchWork W;
+  if (!C.near_ws) C.near_ws = std::make_shared<EntryBatchWork>();
+  EntryBatchWork& W = *C.near_ws;
   const int64_t chunk = 1LL << 26;
   for (int64_t b0 = 0; b0 < nb;) {
     // leaves [b0, b1) with at most `chunk` entries (at least one leaf)

@@ -272,7 +272,7 @@ void grow_copy(DBuf<Quad>& q, DBuf<uint64_t>& k, int64_t used, int64_t need, cud
 void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_t& begin, int64_t& end,
                     DBuf<char>& tmp) {
   if (C.world == 1 || n == 0) { begin = 0; end = n; return; }
-  DBuf<int64_t> cost, pref;
+  DBuf<int64_t>& cost = C.tws.cost; DBuf<int64_t>& pref = C.tws.pref;
   cost.alloc(n); pref.alloc(n);
   k_leaf_cost<<<grid_for(n, 256), 256, 0, C.stream>>>(q.get(), n, kind, cost.get());
   HM_CHECK_LAUNCH();
@@ -305,14 +305,15 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   C.N = N; C.nv = nv; C.leaf_size = leaf_size; C.eta = eta;
   upload_quadrature_tables();
   // ---- a1: mesh upload + panel geometry
-  C.vert.alloc_exact(nv * 3);
-  C.tri.alloc_exact(N * 3);
+  C.vert.alloc(nv * 3);
+  C.tri.alloc(N * 3);
   cudaMemcpyKind kind = mesh.memory ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   HM_CUDA(cudaMemcpyAsync(C.vert.get(), mesh.vertices, nv * 3 * sizeof(double), kind, st));
   HM_CUDA(cudaMemcpyAsync(C.tri.get(), mesh.triangles, N * 3 * sizeof(int32_t), kind, st));
-  DBuf<double> cen, area, hh;
+  TreeWs& ws = C.tws;
+  DBuf<double>& cen = ws.cen; DBuf<double>& area = ws.area; DBuf<double>& hh = ws.hh;
   cen.alloc(N * 3); area.alloc(N); hh.alloc(N);
-  DBuf<unsigned int> bad;
+  DBuf<unsigned int>& bad = ws.bad;
   bad.alloc(1);
   HM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned int), st));
   k_geometry<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), N, nv, cen.get(), area.get(),
@@ -323,7 +324,7 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   HM_CUDA(cudaEventRecord(ev[1], st));
   // ---- a2: Morton codes + stable sort
   const int nb = 148;
-  DBuf<double> part, gbox;
+  DBuf<double>& part = ws.part; DBuf<double>& gbox = ws.gbox;
   part.alloc(6 * nb); gbox.alloc(6);
   k_minmax<<<nb, 256, 0, st>>>(cen.get(), N, part.get());
   k_minmax_final<<<1, 32, 0, st>>>(part.get(), nb, gbox.get());
@@ -331,19 +332,19 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   HM_CUDA(cudaStreamSynchronize(st));
   if (hbad & 1u) fail(HM_ERR_ARG, "hm_build_tree: a triangle references a vertex id out of range");
   if (hbad & 2u) fail(HM_ERR_ARG, "hm_build_tree: a triangle has zero area (degenerate)");
-  DBuf<uint64_t> code_sorted;
-  DBuf<int32_t> idx;
-  C.codes_app.alloc_exact(N);
+  DBuf<uint64_t>& code_sorted = ws.code_sorted;
+  DBuf<int32_t>& idx = ws.idx;
+  C.codes_app.alloc(N);
   code_sorted.alloc(N); idx.alloc(N);
-  C.perm.alloc_exact(N); C.iperm.alloc_exact(N);
+  C.perm.alloc(N); C.iperm.alloc(N);
   k_morton<<<grid_for(N, 256), 256, 0, st>>>(cen.get(), N, gbox.get(), C.codes_app.get(), idx.get());
   HM_CHECK_LAUNCH();
-  DBuf<char> tmp;
+  DBuf<char>& tmp = ws.tmp;
   cub_call(tmp, [&](void* t, size_t& b) {   // LSD radix sort: stable, ties keep ascending index (A7)
     return cub::DeviceRadixSort::SortPairs(t, b, C.codes_app.get(), code_sorted.get(), idx.get(),
                                            C.perm.get(), (int)N, 0, 63, st);
   });
-  C.panel.alloc_exact(N);
+  C.panel.alloc(N);
   k_gather_panels<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), cen.get(), area.get(), hh.get(),
                                                      C.perm.get(), N, C.panel.get(), C.iperm.get());
   HM_CHECK_LAUNCH();
@@ -351,13 +352,13 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   // ---- a3: cluster tree, level order
   int64_t leaf_min = std::max<int64_t>(1, (leaf_size + 1) / 2);
   int64_t cap = 2 * (N / leaf_min + 2) + 4;
-  C.cl_lo.alloc_exact(cap); C.cl_hi.alloc_exact(cap); C.cl_child.alloc_exact(cap); C.cl_depth.alloc_exact(cap);
+  C.cl_lo.alloc(cap); C.cl_hi.alloc(cap); C.cl_child.alloc(cap); C.cl_depth.alloc(cap);
   int32_t root[2] = {0, (int32_t)N}, zero = 0;
   HM_CUDA(cudaMemcpyAsync(C.cl_lo.get(), &root[0], sizeof(int32_t), cudaMemcpyHostToDevice, st));
   HM_CUDA(cudaMemcpyAsync(C.cl_hi.get(), &root[1], sizeof(int32_t), cudaMemcpyHostToDevice, st));
   HM_CUDA(cudaMemcpyAsync(C.cl_depth.get(), &zero, sizeof(int32_t), cudaMemcpyHostToDevice, st));
   std::vector<int64_t> lev = {0, 1};
-  DBuf<int32_t> flag, scan;
+  DBuf<int32_t>& flag = ws.flag; DBuf<int32_t>& scan = ws.scan;
   flag.alloc(cap); scan.alloc(cap);
   for (int level = 0;; ++level) {
     int64_t b = lev[level], e = lev[level + 1], n = e - b;
@@ -380,7 +381,7 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   }
   C.ncl = lev.back();
   int nlev = (int)lev.size() - 1;
-  C.cl_box.alloc_exact(6 * C.ncl); C.cl_diam2.alloc_exact(C.ncl);
+  C.cl_box.alloc(6 * C.ncl); C.cl_diam2.alloc(C.ncl);
   for (int level = nlev - 1; level >= 0; --level) {
     int64_t b = lev[level], e = lev[level + 1];
     k_boxes<<<grid_for(e - b, 128), 128, 0, st>>>(C.panel.get(), C.cl_lo.get(), C.cl_hi.get(), C.cl_child.get(),
@@ -389,16 +390,16 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   }
   HM_CUDA(cudaEventRecord(ev[3], st));
   // ---- a4: block cluster tree, level-wise
-  DBuf<int2> fr[2];
-  DBuf<uint64_t> fk[2];
+  DBuf<int2>* fr = ws.fr;
+  DBuf<uint64_t>* fk = ws.fk;
   fr[0].alloc(1024); fk[0].alloc(1024);
   int2 r2 = make_int2(0, 0);
   uint64_t k0 = 0;
   HM_CUDA(cudaMemcpyAsync(fr[0].get(), &r2, sizeof(int2), cudaMemcpyHostToDevice, st));
   HM_CUDA(cudaMemcpyAsync(fk[0].get(), &k0, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-  DBuf<Quad> admq, denq;
-  DBuf<uint64_t> admk, denk;
-  DBuf<unsigned long long> ctr;
+  DBuf<Quad>& admq = ws.admq; DBuf<Quad>& denq = ws.denq;
+  DBuf<uint64_t>& admk = ws.admk; DBuf<uint64_t>& denk = ws.denk;
+  DBuf<unsigned long long>& ctr = ws.ctr;
   ctr.alloc(3);
   int64_t n_in = 1, nadm = 0, nden = 0;
   int cur = 0;
@@ -422,8 +423,8 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   HM_CUDA(cudaEventRecord(ev[4], st));
   // canonical DFS order = ascending left-aligned path key (A10)
   C.nadm = nadm; C.ndense = nden;
-  C.adm.alloc_exact(nadm); C.dense.alloc_exact(nden);
-  DBuf<uint64_t> ksorted;
+  C.adm.alloc(nadm); C.dense.alloc(nden);
+  DBuf<uint64_t>& ksorted = ws.ksorted;
   ksorted.alloc(std::max(nadm, nden));
   if (nadm)
     cub_call(tmp, [&](void* t, size_t& b) {
