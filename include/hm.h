@@ -93,6 +93,8 @@ const char* hm_last_error(hm_ctx ctx);
  *   "aca_chunk_mb" ACA workspace budget per chunk in MiB, default 16384, capped at 1/4 of the
  *                  free device memory at hm_setup
  *   "aca_kws"      ACA workspace columns per block before the overflow re-run, default 16
+ *   "record_pivots" keep each block's ACA pivot sequence for hm_get_lowrank: 1 on, 0 off,
+ *                  -1 (default) on iff N <= 25000
  * Errors: HM_ERR_ARG for an unknown key or an out-of-range value. */
 hm_status hm_set_option(hm_ctx ctx, const char* key, double value);
 hm_status hm_get_option(hm_ctx ctx, const char* key, double* value);

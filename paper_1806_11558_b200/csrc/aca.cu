@@ -407,7 +407,7 @@ void setup_aca(Context& C) {
   AcaWork& W = *C.aca_ws;
   W.ev.alloc(1);
   HM_CUDA(cudaMemsetAsync(W.ev.get(), 0, sizeof(unsigned long long), st));
-  const bool rec = C.N <= 400000;
+  const bool rec = C.record_pivots == 1 || (C.record_pivots < 0 && C.N <= 25000);
   auto& pivots = C.h_piv;
   pivots.clear();
   if (rec) pivots.resize(nb);

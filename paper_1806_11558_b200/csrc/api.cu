@@ -266,6 +266,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "max_iter") { if (v < 1) bad(); C.max_iter = (int)v; }
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
     else if (k == "aca_kws") { if (v < 1 || v > 64) bad(); C.aca_kws = v; }
+    else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
     else hm::fail(HM_ERR_ARG, "hm_set_option: unknown key '" + k + "'");
   });
 }
@@ -280,6 +281,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "max_iter") *v = C.max_iter;
     else if (k == "aca_chunk_mb") *v = C.aca_chunk_mb;
     else if (k == "aca_kws") *v = C.aca_kws;
+    else if (k == "record_pivots") *v = C.record_pivots;
     else hm::fail(HM_ERR_ARG, "hm_get_option: unknown key '" + k + "'");
   });
 }
@@ -473,7 +475,7 @@ hm_status hm_get_lowrank(hm_ctx ctx, int64_t leaf, int32_t* k, double* U, double
     if (V && kk > 0)
       HM_CUDA(cudaMemcpyAsync(V, base + m * kk, n * kk * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
     if (pivots) {
-      if (C.h_piv.size() != (size_t)(C.adm_end - C.adm_begin)) hm::fail(HM_ERR_STATE, "pivots not recorded (N > 4e5)");
+      if (C.h_piv.size() != (size_t)(C.adm_end - C.adm_begin)) hm::fail(HM_ERR_STATE, "pivots not recorded: set option record_pivots = 1 before hm_setup");
       std::memcpy(pivots, C.h_piv[b].data(), C.h_piv[b].size() * sizeof(int32_t));
     }
     HM_CUDA(cudaStreamSynchronize(C.stream));
@@ -515,7 +517,7 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
       << ",\"near_ms\":" << C.times.near_ms << ",\"aca_ms\":" << C.times.aca_ms << ",\"plan_ms\":" << C.times.plan_ms
       << ",\"setup_ms\":" << C.times.setup_ms << ",\"solve_ms\":" << C.times.solve_ms
       << ",\"solve_iters\":" << C.times.solve_iters << ",\"solve_relres\":" << C.times.solve_relres
-      << ",\"launches\":" << hm::g_launches << ",\"lr_small\":" << C.n_lr_small << ",\"lr_large\":" << C.n_lr_large << ",\"rank_hist\":[";
+      << ",\"launches\":" << hm::g_launches << ",\"mv_batches\":" << C.mv_nbatches << ",\"lr_small\":" << C.n_lr_small << ",\"lr_large\":" << C.n_lr_large << ",\"rank_hist\":[";
     for (int k = 0; k <= 64; ++k) o << (k ? "," : "") << hist[k];
     o << "]}";
     std::string s = o.str();

@@ -109,12 +109,15 @@ struct MvTask {
   int32_t rlo, clo, loff;   // loff: offset in doubles from the batch's staged start
   uint32_t mnk;             // m | n << 11 | k << 22 (k == 0: dense m x n row-major)
 };
-struct MvBatch {
+struct MvSeg {              // one bulk copy: [src, src + bytes) of a base -> stage offset dst
   int64_t src;              // byte offset (16-B aligned) from the base pointer
   int32_t bytes;            // multiple of 16
-  int32_t first, count;
-  int32_t base;             // 0 dense store, 1 factor pool
-  int32_t pad[2];
+  int32_t dst;              // byte offset in the stage (16-B aligned)
+};
+struct MvBatch {
+  int32_t first_seg, nseg;  // bulk copies filling one stage
+  int32_t first, count;     // tasks
+  int32_t base, bytes;      // base 0 dense store / 1 factor pool; total bytes of the stage
 };
 struct MvLarge {
   int32_t rlo, clo, m, n, k, pad;
@@ -158,6 +161,7 @@ struct Context {
 
   // options
   int k_max = 64, solver = 0, restart = 100, max_iter = 10000;
+  int record_pivots = -1;      // -1 auto (N <= 25000), 0 off, 1 on
   double aca_chunk_mb = 16384, aca_kws = 16;
 
   // tree state
@@ -197,6 +201,7 @@ struct Context {
 
   // matvec plan (matvec.cu)
   DBuf<MvBatch> mv_batches;
+  DBuf<MvSeg> mv_segs;
   DBuf<MvTask> mv_tasks;
   DBuf<int32_t> mv_cta;
   DBuf<MvLarge> mv_large, mv_dense_big;

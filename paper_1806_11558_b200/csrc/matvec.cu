@@ -6,9 +6,9 @@
 //
 //   small leaves   (dense blocks and low-rank blocks with (m+n)k*8 <= 16 KiB, ~all leaves):
 //                  k_mv_batched — one persistent CTA per SM walks a contiguous, byte-balanced
-//                  range of "batches" (runs of consecutive leaves whose storage is contiguous,
-//                  <= 44 KiB).  One elected thread streams each batch into shared memory with a
-//                  single cp.async.bulk (TMA bulk copy, mbarrier completion), 4 stages deep
+//                  range of "batches" (consecutive leaves filling <= 44 KiB).  One elected
+//                  thread streams each batch into shared memory with one cp.async.bulk (TMA
+//                  bulk copy, mbarrier completion) per contiguous run of leaves, 4 stages deep
 //                  (~176 KiB per SM in flight); warp 0 produces, 15 consumer warps compute
 //                  the staged batches out of shared memory (dense rows with s lanes per row,
 //                  low-rank t = V^T x then y += U t), releasing each stage through an "empty"
@@ -154,7 +154,7 @@ __device__ __forceinline__ void lowrank_any(const double* U, int m, int n, int k
 // (tasks round-robin), then arrive on its "empty" barrier.  A slow task delays only the refill
 // of its own stage, not the other consumers.
 __global__ void __launch_bounds__(kMvThreads, 1)
-    k_mv_batched(const MvBatch* __restrict__ batches, const int32_t* __restrict__ cta_first,
+    k_mv_batched(const MvBatch* __restrict__ batches, const MvSeg* __restrict__ segs, const int32_t* __restrict__ cta_first,
                  const MvTask* __restrict__ tasks, const char* __restrict__ base0, const char* __restrict__ base1,
                  const double* __restrict__ x, double* __restrict__ y) {
   constexpr int NW = kMvThreads / 32, NC = NW - 1;
@@ -179,7 +179,11 @@ __global__ void __launch_bounds__(kMvThreads, 1)
         if (it >= kMvStages) mbar_wait(&empty[stage], (unsigned)(((it / kMvStages) - 1) & 1));
         const MvBatch B = batches[b0 + it];
         mbar_expect_tx(&full[stage], (unsigned)B.bytes);
-        bulk_g2s(buf + stage * kMvStageBytes, (B.base ? base1 : base0) + B.src, (unsigned)B.bytes, &full[stage]);
+        const char* base = B.base ? base1 : base0;
+        for (int s = 0; s < B.nseg; ++s) {
+          const MvSeg S = segs[B.first_seg + s];
+          bulk_g2s(buf + stage * kMvStageBytes + S.dst, base + S.src, (unsigned)S.bytes, &full[stage]);
+        }
       }
     }
     return;
@@ -305,7 +309,8 @@ void plan_matvec(Context& C) {
   std::vector<int64_t> lr_order;
   for (int64_t b = 0; b < na; ++b)
     if (C.h_rank[b] > 0) lr_order.push_back(b);
-  std::sort(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; });
+  if (!std::is_sorted(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; }))
+    std::sort(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; });
   int64_t tl = 0;
   for (int64_t b : lr_order) {
     const Quad& q = C.h_adm[C.adm_begin + b];
@@ -319,31 +324,44 @@ void plan_matvec(Context& C) {
       tl += k;
     }
   }
-  // batches of consecutive, contiguous items within one stage
+  // batches: consecutive items (same base) filling one stage; each contiguous run of items
+  // becomes one bulk-copy segment (16-B aligned superset of the run)
   std::vector<MvBatch> batches;
+  std::vector<MvSeg> segs;
   std::vector<MvTask> tasks;
   tasks.reserve(items.size());
   for (size_t i = 0; i < items.size();) {
-    const int64_t a0 = items[i].byte0 & ~int64_t(15);
-    int64_t end = items[i].byte0 + items[i].bytes;
-    size_t j = i + 1;
-    while (j < items.size() && items[j].base == items[i].base && items[j].byte0 == items[j - 1].byte0 + items[j - 1].bytes &&
-           ((items[j].byte0 + items[j].bytes + 15) & ~int64_t(15)) - a0 <= kMvStageBytes) {
-      end = items[j].byte0 + items[j].bytes;
-      ++j;
-    }
-    const int64_t a1 = (end + 15) & ~int64_t(15);
     MvBatch B{};
-    B.src = a0;
-    B.bytes = (int32_t)(a1 - a0);
+    B.first_seg = (int32_t)segs.size();
     B.first = (int32_t)tasks.size();
-    B.count = (int32_t)(j - i);
     B.base = items[i].base;
-    for (size_t k = i; k < j; ++k) {
-      MvTask t = items[k].t;
-      t.loff = (int32_t)((items[k].byte0 - a0) / 8);
-      tasks.push_back(t);
+    int32_t used = 0;
+    size_t j = i;
+    while (j < items.size() && items[j].base == B.base) {
+      // the run of contiguous items starting at j
+      size_t r = j + 1;
+      int64_t end = items[j].byte0 + items[j].bytes;
+      const int64_t a0 = items[j].byte0 & ~int64_t(15);
+      while (r < items.size() && items[r].base == B.base && items[r].byte0 == end &&
+             ((items[r].byte0 + items[r].bytes + 15) & ~int64_t(15)) - a0 + used <= kMvStageBytes) {
+        end = items[r].byte0 + items[r].bytes;
+        ++r;
+      }
+      const int64_t a1 = (end + 15) & ~int64_t(15);
+      if (used + (a1 - a0) > kMvStageBytes) break;          // next run does not fit: close the batch
+      segs.push_back(MvSeg{a0, (int32_t)(a1 - a0), used});
+      for (size_t k = j; k < r; ++k) {
+        MvTask t = items[k].t;
+        t.loff = (int32_t)((used + (items[k].byte0 - a0)) / 8);
+        tasks.push_back(t);
+      }
+      used += (int32_t)(a1 - a0);
+      j = r;
     }
+    if (j == i) fail(HM_ERR_CUDA, "matvec plan: leaf larger than a pipeline stage");
+    B.nseg = (int32_t)segs.size() - B.first_seg;
+    B.count = (int32_t)(j - i);
+    B.bytes = used;
     batches.push_back(B);
     i = j;
   }
@@ -380,6 +398,7 @@ void plan_matvec(Context& C) {
       HM_CUDA(cudaMemcpyAsync(dbuf.get(), v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, st));
   };
   up(C.mv_batches, batches);
+  up(C.mv_segs, segs);
   up(C.mv_tasks, tasks);
   up(C.mv_cta, cta_first);
   up(C.mv_large, large);
@@ -423,7 +442,7 @@ void matvec_internal(Context& C, const double* x_int, double* y_int) {
   const double* pool = (const double*)C.fpool.base;
   if (C.mv_nbatches) {
     const int smem = 128 + kMvStages * kMvStageBytes;
-    k_mv_batched<<<C.mv_grid, kMvThreads, smem, st>>>(C.mv_batches.get(), C.mv_cta.get(), C.mv_tasks.get(),
+    k_mv_batched<<<C.mv_grid, kMvThreads, smem, st>>>(C.mv_batches.get(), C.mv_segs.get(), C.mv_cta.get(), C.mv_tasks.get(),
                                                        (const char*)C.dstore.get(), (const char*)pool, x_int, y_int);
     HM_CHECK_LAUNCH();
   }
