@@ -70,25 +70,50 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
+// x_sigma for a leaf, preloaded once per warp (one coalesced load per 32 columns) and handed
+// to the lane that needs column c with a shuffle: no L2 round trip inside the column loop.
+template <int NX>
+struct XReg {
+  double v[NX];
+  __device__ __forceinline__ void load(const double* __restrict__ x, int n, int lane) {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) v[i] = (i * 32 + lane < n) ? __ldg(x + i * 32 + lane) : 0.0;
+  }
+  __device__ __forceinline__ double get(int c) const {   // warp-collective, c uniform per lane group
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      const double t = __shfl_sync(0xffffffffu, v[i], c & 31);
+      r = (c >> 5) == i ? t : r;
+    }
+    return r;
+  }
+};
+
 // Dense m x n row-major block: S lanes per row (consecutive columns -> conflict-free shared
 // loads for the leaf widths of CBC), 32/S rows per pass, P passes held in registers so the
 // P shuffle reductions are independent (ILP instead of P serial reduction chains).
-template <int S, int P>
+template <int S, int P, int NX>
 __device__ __forceinline__ void dense_block(const double* __restrict__ B, int m, int n, const double* __restrict__ x,
                                             double* __restrict__ y, int lane) {
   constexpr int RPP = 32 / S;
   const int sub = lane % S, rr = lane / S;
+  XReg<NX> xr;
+  xr.load(x, n, lane);
+  const int iters = (n + S - 1) / S;
   for (int r0 = 0; r0 < m; r0 += RPP * P) {
     double acc[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) acc[p] = 0.0;
-    for (int c = sub; c < n; c += S) {
-      const double xc = __ldg(x + c);
+    for (int it = 0; it < iters; ++it) {
+      const int c = sub + it * S;
+      const double xc = xr.get(c);
+      if (c < n)
 #pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const int r = r0 + rr + p * RPP;
-        if (r < m) acc[p] += B[r * n + c] * xc;
-      }
+        for (int p = 0; p < P; ++p) {
+          const int r = r0 + rr + p * RPP;
+          if (r < m) acc[p] += B[r * n + c] * xc;
+        }
     }
 #pragma unroll
     for (int o = S / 2; o > 0; o >>= 1)
@@ -104,16 +129,24 @@ __device__ __forceinline__ void dense_block(const double* __restrict__ B, int m,
 }
 
 __device__ __forceinline__ void dense_any(const double* B, int m, int n, const double* x, double* y, int lane) {
-  if (n <= 16) dense_block<2, 4>(B, m, n, x, y, lane);
-  else if (n <= 48) dense_block<4, 4>(B, m, n, x, y, lane);
-  else if (n <= 96) dense_block<8, 4>(B, m, n, x, y, lane);
-  else dense_block<32, 2>(B, m, n, x, y, lane);
+  if (n <= 16) dense_block<2, 4, 1>(B, m, n, x, y, lane);
+  else if (n <= 32) dense_block<4, 4, 1>(B, m, n, x, y, lane);
+  else if (n <= 64) dense_block<4, 4, 2>(B, m, n, x, y, lane);
+  else if (n <= 128) dense_block<8, 4, 4>(B, m, n, x, y, lane);
+  else {   // generic (large leaf_size only): direct loads
+    for (int r = 0; r < m; ++r) {
+      double acc = 0.0;
+      for (int c = lane; c < n; c += 32) acc += B[r * n + c] * __ldg(x + c);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) atomicAdd(y + r, acc);
+    }
+  }
 }
 
-// Low-rank block U (m x k) | V (n x k), column-major: t = V^T x with all k column sums in
-// registers (x_j loaded once, k independent loads per row j), one butterfly reduction over
-// the k sums at once, then y += U t (k independent loads per row).
-// columns [l0, l0 + kc) of the block (kc <= KB); k > 32 is processed in column groups
+// Low-rank block U (m x k) | V (n x k), column-major, columns [l0, l0 + kc) (kc <= KB): t = V^T x
+// with all kc column sums in registers (x_j loaded up front, 4 rows of x per lane in flight),
+// one butterfly reduction over the kc sums at once, then y += U t (kc independent loads per row).
 template <int KB>
 __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int m, int n, int k, int l0, int kc,
                                               const double* __restrict__ x, double* __restrict__ y, int lane) {
@@ -122,11 +155,21 @@ __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int
   double acc[KB];
 #pragma unroll
   for (int l = 0; l < KB; ++l) acc[l] = 0.0;
-  for (int j = lane; j < n; j += 32) {
-    const double xj = __ldg(x + j);
+  for (int j0 = 0; j0 < n; j0 += 128) {
+    double xj[4];
 #pragma unroll
-    for (int l = 0; l < KB; ++l)
-      if (l < kc) acc[l] += V[j + (int64_t)l * n] * xj;
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q * 32 + lane;
+      xj[q] = j < n ? __ldg(x + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q * 32 + lane;
+      if (j < n)
+#pragma unroll
+        for (int l = 0; l < KB; ++l)
+          if (l < kc) acc[l] += V[j + (int64_t)l * n] * xj[q];
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
@@ -146,7 +189,7 @@ __device__ __forceinline__ void lowrank_any(const double* U, int m, int n, int k
   if (k <= 8) lowrank_block<8>(U, m, n, k, 0, k, x, y, lane);
   else if (k <= 16) lowrank_block<16>(U, m, n, k, 0, k, x, y, lane);
   else
-    for (int l0 = 0; l0 < k; l0 += 32) lowrank_block<32>(U, m, n, k, l0, min(32, k - l0), x, y, lane);
+    for (int l0 = 0; l0 < k; l0 += 16) lowrank_block<16>(U, m, n, k, l0, min(16, k - l0), x, y, lane);
 }
 
 // Warp-specialised pipeline: warp 0 is the producer (one lane issues the bulk copies, waits
@@ -193,8 +236,18 @@ __global__ void __launch_bounds__(kMvThreads, 1)
     mbar_wait(&full[stage], (unsigned)((it / kMvStages) & 1));
     const MvBatch B = batches[b0 + it];
     const double* data = reinterpret_cast<const double*>(buf + stage * kMvStageBytes);
-    for (int t = warp - 1; t < B.count; t += NC) {
-      const MvTask T = tasks[B.first + t];
+    // this warp's task descriptors for the stage, one per lane, loaded at once
+    MvTask mine = {0, 0, 0, 0};
+    {
+      const int t = warp - 1 + NC * lane;
+      if (t < B.count) mine = tasks[B.first + t];
+    }
+    for (int i = 0, t = warp - 1; t < B.count; ++i, t += NC) {
+      MvTask T;
+      T.rlo = __shfl_sync(0xffffffffu, mine.rlo, i);
+      T.clo = __shfl_sync(0xffffffffu, mine.clo, i);
+      T.loff = __shfl_sync(0xffffffffu, mine.loff, i);
+      T.mnk = __shfl_sync(0xffffffffu, mine.mnk, i);
       const int m = T.mnk & 2047, n = (T.mnk >> 11) & 2047, k = T.mnk >> 22;
       if (k == 0) dense_any(data + T.loff, m, n, x + T.clo, y + T.rlo, lane);
       else lowrank_any(data + T.loff, m, n, k, x + T.clo, y + T.rlo, lane);
@@ -222,11 +275,17 @@ __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ 
     double acc[8];
 #pragma unroll
     for (int l = 0; l < 8; ++l) acc[l] = 0.0;
-    for (int j = T.j0 + lane; j < T.j1; j += 32) {
-      const double xj = __ldg(xs + j);
+    for (int j = T.j0 + lane; j < T.j1; j += 64) {
+      const bool two = j + 32 < T.j1;
+      const double xa = __ldg(xs + j), xb = two ? __ldg(xs + j + 32) : 0.0;
+      double va[8], vb[8];
 #pragma unroll
-      for (int l = 0; l < 8; ++l)
-        if (l < kc) acc[l] += __ldg(V + j + (int64_t)l * B.n) * xj;
+      for (int l = 0; l < 8; ++l) {
+        va[l] = l < kc ? __ldg(V + j + (int64_t)l * B.n) : 0.0;
+        vb[l] = (l < kc && two) ? __ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
+      }
+#pragma unroll
+      for (int l = 0; l < 8; ++l) acc[l] += va[l] * xa + vb[l] * xb;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -253,17 +312,24 @@ __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ 
     const MvLarge B = L[T.blk];
     const double* U = pool + B.off;
     const double* tl = tbuf + B.toff;
-    for (int t = T.t0 + lane; t < T.t1; t += 32) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int t = T.t0 + lane; t < T.t1; t += 64) {
+      const bool two = t + 32 < T.t1;
+      double s0 = 0.0, s1 = 0.0, r0 = 0.0, r1 = 0.0;
       int l = 0;
-      for (; l + 3 < B.k; l += 4) {
-        s0 += __ldg(U + t + (int64_t)l * B.m) * __ldg(tl + l);
-        s1 += __ldg(U + t + (int64_t)(l + 1) * B.m) * __ldg(tl + l + 1);
-        s2 += __ldg(U + t + (int64_t)(l + 2) * B.m) * __ldg(tl + l + 2);
-        s3 += __ldg(U + t + (int64_t)(l + 3) * B.m) * __ldg(tl + l + 3);
+      for (; l + 1 < B.k; l += 2) {
+        const double ta = __ldg(tl + l), tb = __ldg(tl + l + 1);
+        const double u0 = __ldg(U + t + (int64_t)l * B.m), u1 = __ldg(U + t + (int64_t)(l + 1) * B.m);
+        const double w0 = two ? __ldg(U + t + 32 + (int64_t)l * B.m) : 0.0;
+        const double w1 = two ? __ldg(U + t + 32 + (int64_t)(l + 1) * B.m) : 0.0;
+        s0 += u0 * ta; s1 += u1 * tb; r0 += w0 * ta; r1 += w1 * tb;
       }
-      for (; l < B.k; ++l) s0 += __ldg(U + t + (int64_t)l * B.m) * __ldg(tl + l);
-      atomicAdd(y + B.rlo + t, (s0 + s1) + (s2 + s3));
+      if (l < B.k) {
+        const double ta = __ldg(tl + l);
+        s0 += __ldg(U + t + (int64_t)l * B.m) * ta;
+        if (two) r0 += __ldg(U + t + 32 + (int64_t)l * B.m) * ta;
+      }
+      atomicAdd(y + B.rlo + t, s0 + s1);
+      if (two) atomicAdd(y + B.rlo + t + 32, r0 + r1);
     }
   }
 }
