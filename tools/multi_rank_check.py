@@ -5,7 +5,9 @@ lists; the matvec's partial products are all-reduced.  C
   * owned ranges of all ranks are disjoint and cover both lists (gathered to rank 0);
   * the p-rank H-matvec equals a 1-rank H-matvec built on rank 0's GPU to 1e-13 relative
     (same leaves, same factors; only the summation order of the global sum differs, A19);
-  * the p-rank GMRES solution equals the 1-rank solution to 1e-10 relative.
+  * the p-rank GMRES solution equals the 1-rank solution to 1e-8 relative: both solves stop at
+    relres <= 1e-10 with y differing by ~1e-15 per product (A19), so they can differ by up to
+    cond(H) * 2e-10 (cond ~ 1e3 at C2, growing like 1/h); observed 4e-14 (C2), 1.3e-10 (C3).
 Prints one JSON line on rank 0 and exits non-zero on failure.
 """
 import json
@@ -65,7 +67,7 @@ def main():
         ds = (torch.linalg.norm(sol - s1) / torch.linalg.norm(s1)).item()
         res.update({"matvec_rel_diff": dy, "solve_rel_diff": ds, "iters": it, "iters_1rank": it1,
                     "setup_ms_max": setup_ms.item(), "setup_ms_1rank": R.stats()["setup_ms"]})
-        ok &= dy <= 1e-13 and ds <= 1e-10
+        ok &= dy <= 1e-13 and ds <= 1e-8
         res["ok"] = bool(ok)
         print(json.dumps(res), flush=True)
         R.close()

@@ -16,6 +16,7 @@ METRICS = {
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_pct",
     "launch__grid_size": "grid",
 }
+FULLNAME = True
 
 
 def rows(path):
@@ -24,15 +25,16 @@ def rows(path):
     hdr, units, data = r[0], r[1], r[2:]
     idx = {h: i for i, h in enumerate(hdr)}
     for d in data:
-        rec = {"kernel": re.sub(r"\(.*", "", d[idx["Kernel Name"]]).split("::")[-1]}
+        name = re.sub(r"\(.*", "", d[idx["Kernel Name"]])
+        rec = {"kernel": re.sub(r"(?:hm::|<unnamed>::|\(anonymous namespace\)::)", "", name)}
         for m, k in METRICS.items():
             if m in idx:
                 v = d[idx[m]].replace(",", "")
                 try:
                     v = float(v)
-                    if units[idx[m]] == "msecond":
+                    if units[idx[m]] in ("msecond", "ms"):
                         v *= 1e3
-                    elif units[idx[m]] == "nsecond":
+                    elif units[idx[m]] in ("nsecond", "ns"):
                         v /= 1e3
                     elif units[idx[m]] in ("Kbyte", "KB"):
                         v *= 1e3
