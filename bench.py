@@ -48,21 +48,31 @@ def peaks():
     return 6650.0, "fallback"
 
 
-FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.jsonl")
+# "alu" roofline of entry evaluation: the FP64 pipe issues 64 instructions
+# per clock per SM (B200: 148 SMs, 1965 MHz max); one quadrature evaluation of the reading's
+# arithmetic (A15) is 23.5 FP64-pipe instructions in the SASS of the evaluation loop (distance
+# 6, correctly rounded w/sqrt(d2) 16, sum 1, outer point amortised 0.5) plus one MUFU.
+FP64_LANES_PER_SM, SMS, DP_INSTR_PER_EVAL = 64, 148, 23.5
 
 
 def fp64_eval_peak():
-    """Measured throughput of the minimal IEEE evaluation sequence w/sqrt(d2) + sum on this
-    pool's B200 (tools/fp64_peak.cu), evaluations/s."""
-    best = None
-    if os.path.exists(FP64_PEAK_FILE):
-        for line in open(FP64_PEAK_FILE):
-            d = json.loads(line)
-            if d.get("kernel") == "eval_min":
-                best = max(best or 0, d["evals_per_s"])
-            if d.get("kernel") == "sqrt_div" and best is None:
-                best = d["evals_per_s"]
-    return best or 6.26e11
+    """Peak quadrature evaluations/s from unit counts and clocks (see above)."""
+    mhz = 1965.0
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        mhz = json.load(open(p)).get("sm_max_mhz", mhz)
+    return FP64_LANES_PER_SM * SMS * mhz * 1e6 / DP_INSTR_PER_EVAL
+
+
+def ncu_traffic(cfg):
+    """dram__bytes_read.sum + dram__bytes_write.sum per H-matvec from the committed ncu capture
+    of this config (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p)).get(cfg)
+        if d:
+            return d
+    return None
 
 
 class Clocks:
@@ -179,6 +189,7 @@ def _run_gpu(args, rank, world, local, dev, stream):
 
     for _ in range(args.warmup):
         step()
+    H.set_option("kernel_timing", 1)     # CUDA events around every launch family on the library stream
     barrier(world)
     l0 = H.stats()["launches"]
     clk = Clocks(local) if rank == 0 else None
@@ -199,6 +210,13 @@ def _run_gpu(args, rank, world, local, dev, stream):
     ms = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms, world)
     st = H.stats()
+    kt = st["kt"]
+    H.set_option("kernel_timing", 0)
+    K = max(1, args.steps)
+    eval_ms = max_over_ranks((kt["eval_near_ms"] + kt["eval_aca_ms"]) / K, world)
+    aca_other_ms = max_over_ranks(kt["aca_other_ms"] / K, world)
+    mv_kern_ms = max_over_ranks(kt["matvec_ms"] / max(1, kt["matvec_n"]), world)
+    mv_kern_ms_step = max_over_ranks(kt["matvec_ms"] / K, world)
     tree_s = max_over_ranks(st["tree_ms"], world) / 1e3
     setup_s = max_over_ranks(st["setup_ms"], world) / 1e3
     near_s = max_over_ranks(st["near_ms"], world) / 1e3
@@ -233,10 +251,14 @@ def _run_gpu(args, rank, world, local, dev, stream):
     hbm, hbm_src = peaks()
     mv_gbs = alg_bytes_rank / (mv_ms * 1e-3) / 1e9
 
-    # ---- entry-evaluation throughput of setup (FP64-pipe bound phase)
+    # ---- entry-evaluation throughput of setup (FP64-pipe bound kernels), per rank: evaluations
+    # of this rank's leaves / device time of its evaluation kernels (events over the timed steps)
     evals = st["evals_near"] + st["evals_aca"]
-    eval_rate = evals / max(1e-9, (st["near_ms"] + st["aca_ms"]) * 1e-3)
+    eval_ms_rank = (kt["eval_near_ms"] + kt["eval_aca_ms"]) / K
+    eval_rate = -max_over_ranks(-(evals / max(1e-9, eval_ms_rank * 1e-3)), world)   # slowest rank
+    eval_rate_phase = evals / max(1e-9, (st["near_ms"] + st["aca_ms"]) * 1e-3)
     eval_peak = fp64_eval_peak()
+    mv_gbs_live = alg_bytes_rank / (mv_kern_ms * 1e-3) / 1e9
 
     # ---- e2e: same step through the same ABI with host buffers
     e2e = None
@@ -255,17 +277,25 @@ def _run_gpu(args, rank, world, local, dev, stream):
         e2e = {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": int(V.nbytes + T.nbytes + fh.nbytes),
                "d2h_bytes_per_step": int(solh.nbytes)}
 
-    # dominant phase -> roofline object
-    if (near_s + aca_s) >= solve_s:
-        roof = {"kernel": "entry evaluation (near-field + ACA row/column generation)", "bound": "alu",
+    # dominant kernel family of the step -> roofline object
+    traffic = ncu_traffic(args.config) if world == 1 else None
+    if eval_ms >= mv_kern_ms_step:
+        roof = {"kernel": "entry evaluation (k_eval_* near-field + ACA rows/columns)", "bound": "alu",
                 "achieved": round(eval_rate / 1e9, 2), "peak": round(eval_peak / 1e9, 2), "unit": "Geval/s",
-                "frac": round(eval_rate / eval_peak, 4), "traffic": None,
-                "peak_source": "measured: minimal IEEE FP64 evaluation sequence on this pool's B200 (profiles/r01_fp64_peak.jsonl)"}
+                "frac": round(eval_rate / eval_peak, 4),
+                "traffic": traffic.get("eval_bytes_per_eval") if traffic else None,
+                "peak_source": f"unit counts: {FP64_LANES_PER_SM} FP64 instr/clk/SM x {SMS} SMs x sm_max clock / "
+                               f"{DP_INSTR_PER_EVAL} FP64 instr per evaluation (SASS)",
+                "share_of_step": round(eval_ms / ms, 4)}
     else:
-        roof = {"kernel": "H-matvec", "bound": "hbm", "achieved": round(mv_gbs, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(mv_gbs / hbm, 4), "traffic": None, "peak_source": hbm_src}
+        roof = {"kernel": "H-matvec (k_mv_batched + k_mv_large_v/u)", "bound": "hbm", "achieved": round(mv_gbs_live, 1),
+                "peak": hbm, "unit": "GB/s", "frac": round(mv_gbs_live / hbm, 4),
+                "traffic": traffic.get("matvec_bytes_per_launch") if traffic else None, "peak_source": hbm_src,
+                "share_of_step": round(mv_kern_ms_step / ms, 4)}
     matvec_roof = {"bound": "hbm", "achieved": round(mv_gbs, 1), "peak": hbm, "unit": "GB/s",
-                   "frac": round(mv_gbs / hbm, 4), "alg_bytes_per_launch": int(alg_bytes_rank), "peak_source": hbm_src}
+                   "frac": round(mv_gbs / hbm, 4), "alg_bytes_per_launch": int(alg_bytes_rank), "peak_source": hbm_src,
+                   "timing": "median of flushed-L2 products", "achieved_in_solve": round(mv_gbs_live, 1),
+                   "traffic": traffic.get("matvec_bytes_per_launch") if traffic else None}
 
     out = None
     if rank == 0:
@@ -284,7 +314,10 @@ def _run_gpu(args, rank, world, local, dev, stream):
                           "aca_s": round(aca_s, 6), "solve_s": round(solve_s, 6), "solve_iters": iters,
                           "solve_relres": rr, "matvec_s": round(mv_ms / 1e3, 6), "matvec_GBps": round(mv_gbs, 1),
                           "matvec_frac_hbm": round(mv_gbs / hbm, 4), "stored_GB_total": round(stored_tot / 1e9, 3),
-                          "k_mean": st["k_mean"], "evals": evals, "eval_rate_Gps": round(eval_rate / 1e9, 2)},
+                          "k_mean": st["k_mean"], "evals": evals, "eval_rate_Gps": round(eval_rate / 1e9, 2),
+                          "eval_rate_phase_Gps": round(eval_rate_phase / 1e9, 2),
+                          "kernel_ms_per_step": {"eval": round(eval_ms, 3), "aca_other": round(aca_other_ms, 3),
+                                                 "matvec": round(mv_kern_ms_step, 3)}},
             "roofline": roof, "matvec_roofline": matvec_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         }

@@ -35,25 +35,46 @@ struct AcaState {
 struct AcaWork {
   DBuf<AcaBlk> blk;
   DBuf<AcaState> state;
-  DBuf<int32_t> owned, piv;
+  DBuf<int32_t> owned, piv, act, flag, pos, big;
   DBuf<int64_t> rsz, csz, rpre, cpre;
   DBuf<double> Uw, Vw;
   DBuf<uint32_t> bmap;
   DBuf<char> tmp;
   DBuf<unsigned long long> ev, cnt;
+  DBuf<int64_t> tot;
   DBuf<EntryRef> lists;
 };
 
 namespace {
 
-__global__ void k_step_sizes(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S, int64_t nb,
-                             int64_t* __restrict__ rsz, int64_t* __restrict__ csz) {
+// Active-block compaction for one ACA step: flag[c] = block c still running; after the scan
+// pos, act[pos[c]] = c and the row / column lengths of the active blocks are packed in front
+// (the rest of rsz / csz stays 0), so the entry batches, pivot and update kernels only see
+// the active blocks.
+__global__ void k_step_flags(const AcaState* __restrict__ S, int64_t nb, int32_t* __restrict__ flag) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c > nb) return;
-  if (c == nb) { rsz[c] = 0; csz[c] = 0; return; }
-  const bool act = S[c].status == 0;
-  rsz[c] = act ? B[c].n : 0;
-  csz[c] = act ? B[c].m : 0;
+  flag[c] = c < nb && S[c].status == 0;
+}
+
+__global__ void k_step_compact(const AcaBlk* __restrict__ B, const int32_t* __restrict__ flag,
+                               const int32_t* __restrict__ pos, int64_t nb, int32_t* __restrict__ act,
+                               int64_t* __restrict__ rsz, int64_t* __restrict__ csz) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > nb) return;
+  if (c >= pos[nb]) { rsz[c] = 0; csz[c] = 0; }   // slots past the active count (disjoint from the writes below)
+  if (c == nb || !flag[c]) return;
+  const int32_t a = pos[c];
+  act[a] = (int32_t)c;
+  rsz[a] = B[c].n;
+  csz[a] = B[c].m;
+}
+
+__global__ void k_step_totals(const int64_t* __restrict__ rpre, const int64_t* __restrict__ cpre,
+                              const int32_t* __restrict__ pos, int64_t nb, int64_t* __restrict__ tot) {
+  tot[0] = rpre[nb];
+  tot[1] = cpre[nb];
+  tot[2] = pos[nb];
 }
 
 // Residual row (ROW) or column entries of the active blocks of a chunk, as a batch mapping
@@ -65,16 +86,18 @@ struct AcaMap {
   const Panel* P;
   const AcaBlk* B;
   const AcaState* S;
-  const int64_t* pre;   // nb + 1 prefix of this step's row (or column) lengths
+  const int64_t* pre;   // nb + 1 prefix of this step's row (or column) lengths, active blocks first
+  const int32_t* act;   // compact index -> block
   int64_t nb;
   double* Uw;
   double* Vw;
   __device__ bool locate(int64_t e, bool valid, EntryRef& r) const {
-    const int64_t c = warp_find_segment(pre, nb + 1, e, valid);
+    const int64_t a = warp_find_segment(pre, nb + 1, e, valid);
     if (!valid) return false;
+    const int32_t c = act[a];
     if (!ROW && (S[c].skip || S[c].status != 0)) return false;
-    r.seg = (int32_t)c;
-    r.idx = (int32_t)(e - pre[c]);
+    r.seg = c;
+    r.idx = (int32_t)(e - pre[a]);
     return true;
   }
   __device__ void pair(EntryRef r, int& s, int& t) const {
@@ -129,11 +152,12 @@ __device__ int first_unused(const uint32_t* bm, int m, int lane) {
   return best == INT_MAX ? -1 : best;
 }
 
-__global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, int64_t nb,
-                            double* __restrict__ Vw, uint32_t* __restrict__ bmap) {
-  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+__global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, const int32_t* __restrict__ act,
+                            int64_t nact, double* __restrict__ Vw, uint32_t* __restrict__ bmap) {
+  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (c >= nb) return;
+  if (a >= nact) return;
+  const int64_t c = act[a];
   AcaState st = S[c];
   if (st.status != 0) return;
   const AcaBlk b = B[c];
@@ -174,35 +198,97 @@ __global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__
   }
 }
 
-__global__ void k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, int64_t nb,
-                             const double* __restrict__ Uw, const double* __restrict__ Vw,
-                             const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv, int kws, double eps) {
-  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (c >= nb) return;
-  AcaState st = S[c];
-  if (st.status != 0 || st.skip) return;
-  const AcaBlk b = B[c];
+// Sum 16 per-lane values over the warp by recursive halving (16 shuffles instead of 16 x 5):
+// on return a[0] of lane L holds the warp total of value index
+// 8*bit4(L) + 4*bit3(L) + 2*bit2(L) + bit1(L)  (two lanes per index).
+__device__ __forceinline__ void warp_reduce16(double (&a)[16], int lane) {
+#pragma unroll
+  for (int lvl = 0; lvl < 4; ++lvl) {
+    const int o = 16 >> lvl, half = 8 >> lvl;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < half) {
+        const double send = up ? a[i] : a[i + half];
+        const double keep = up ? a[i + half] : a[i];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+  }
+  a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+}
+__device__ __forceinline__ int reduce16_index(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
+// Frobenius update of step k (A11): S2 += 2 sum_l (u^T U_l)(V_l^T v) + |u|^2 |v|^2, the stop
+// test, and the next row pivot.  A group of G warps works on one block (G = 1 for most
+// blocks, G = 8 for blocks with m + n >= kBigMN); the cross products are formed 8 columns per
+// pass with the 8 (u^T U_l) and 8 (V_l^T v) partial sums in registers (u_t / v_j loaded once
+// per pass, 8 independent loads in flight) and reduced together by one recursive-halving
+// butterfly.  Norms feed the stop test only (A15: tree-reduced on the GPU).
+constexpr int kBigMN = 2048;
+
+template <int G>
+__device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, const double* __restrict__ Uw,
+                                                 const double* __restrict__ Vw, const uint32_t* __restrict__ bmap,
+                                                 int32_t* __restrict__ piv, int64_t c, int kws, double eps, int gw,
+                                                 int lane, double* red /* smem [G][17] (G > 1) */) {
   const double* U = Uw + b.uoff;
   const double* V = Vw + b.voff;
   const double* u = U + (int64_t)st.k * b.m;
   const double* v = V + (int64_t)st.k * b.n;
+  const int t0 = gw * 32 + lane, stride = G * 32;
   double uu = 0.0;
-  for (int t = lane; t < b.m; t += 32) uu += u[t] * u[t];
+  for (int t = t0; t < b.m; t += stride) uu = fma(u[t], u[t], uu);
   uu = warp_sum(uu);
   double cross = 0.0;
-  for (int l = 0; l < st.k; ++l) {
-    double du = 0.0, dv = 0.0;
-    for (int t = lane; t < b.m; t += 32) du += u[t] * U[t + (int64_t)l * b.m];
-    for (int j = lane; j < b.n; j += 32) dv += V[j + (int64_t)l * b.n] * v[j];
-    du = warp_sum(du);
-    dv = warp_sum(dv);
-    cross += du * dv;
+  for (int l0 = 0; l0 < st.k; l0 += 8) {
+    const int kc = min(8, st.k - l0);
+    double acc[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) acc[l] = 0.0;
+    for (int t = t0; t < b.m; t += stride) {
+      const double ut = u[t];
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < kc) acc[l] = fma(ut, U[t + (int64_t)(l0 + l) * b.m], acc[l]);
+    }
+    for (int j = t0; j < b.n; j += stride) {
+      const double vj = v[j];
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < kc) acc[8 + l] = fma(V[j + (int64_t)(l0 + l) * b.n], vj, acc[8 + l]);
+    }
+    warp_reduce16(acc, lane);   // lane L: total of index reduce16_index(L); du_l at bit4 = 0, dv_l at L ^ 16
+    if (G > 1) {
+      if ((lane & 1) == 0) red[gw * 17 + reduce16_index(lane)] = acc[0];
+      __syncthreads();
+      double tsum = 0.0;
+      if (lane < 16)
+        for (int g = 0; g < G; ++g) tsum += red[g * 17 + lane];
+      const double other = __shfl_down_sync(0xffffffffu, tsum, 8);
+      const double part = (lane < 8 && lane < kc) ? tsum * other : 0.0;
+      cross += warp_sum(part);
+      __syncthreads();
+    } else {
+      const double other = __shfl_xor_sync(0xffffffffu, acc[0], 16);
+      const int idx = reduce16_index(lane);
+      const double part = ((lane & 17) == 0 && idx < kc) ? acc[0] * other : 0.0;
+      cross += warp_sum(part);
+    }
+  }
+  if (G > 1) {
+    if (lane == 0) red[gw * 17 + 16] = uu;
+    __syncthreads();
+    uu = 0.0;
+    for (int g = 0; g < G; ++g) uu += red[g * 17 + 16];
+    __syncthreads();
   }
   st.S2 = (st.S2 + 2.0 * cross) + uu * st.vv;
-  if (lane == 0) {
-    piv[(int64_t)c * 2 * kws + 2 * st.k] = st.i;
-    piv[(int64_t)c * 2 * kws + 2 * st.k + 1] = st.js;
+  if (gw == 0 && lane == 0) {
+    piv[c * 2 * kws + 2 * st.k] = st.i;
+    piv[c * 2 * kws + 2 * st.k + 1] = st.js;
   }
   st.k += 1;
   if (sqrt(uu) * sqrt(st.vv) <= eps * sqrt(st.S2)) st.status = 1;    // stop test (A11)
@@ -212,16 +298,58 @@ __global__ void k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict_
     const uint32_t* bm = bmap + b.boff;
     double best = -1.0;
     int bt = INT_MAX;
-    for (int t = lane; t < b.m; t += 32) {
+    for (int t = t0; t < b.m; t += stride) {
       if (is_used(bm, t)) continue;
-      double a = fabs(u[t]);
+      const double a = fabs(u[t]);
       if (a > best) { best = a; bt = t; }
     }
     warp_argmax(best, bt);
+    if (G > 1) {
+      int* ri = reinterpret_cast<int*>(red + G * 17);
+      if (lane == 0) { red[gw * 17] = best; ri[gw] = bt; }
+      __syncthreads();
+      best = red[0]; bt = ri[0];
+      for (int g = 1; g < G; ++g) {
+        const double ob = red[g * 17];
+        const int oi = ri[g];
+        if (ob > best || (ob == best && oi < bt)) { best = ob; bt = oi; }
+      }
+    }
     if (bt == INT_MAX) st.status = 1;
     else st.i = bt;
   }
+}
+
+// G = 1: one warp per active block (small blocks; big ones are skipped), act[] = compact list
+__global__ void __launch_bounds__(256) k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
+                                                    const int32_t* __restrict__ act, int64_t nact,
+                                                    const double* __restrict__ Uw, const double* __restrict__ Vw,
+                                                    const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv,
+                                                    int kws, double eps) {
+  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (a >= nact) return;
+  const int64_t c = act[a];
+  AcaState st = S[c];
+  if (st.status != 0 || st.skip) return;
+  const AcaBlk b = B[c];
+  if (b.m + b.n >= kBigMN) return;
+  aca_update_block<1>(b, st, Uw, Vw, bmap, piv, c, kws, eps, 0, lane, nullptr);
   if (lane == 0) S[c] = st;
+}
+
+// G = 8: one CTA per big block of the chunk (list fixed per chunk; finished blocks return)
+__global__ void __launch_bounds__(256) k_aca_update_big(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
+                                                        const int32_t* __restrict__ big, const double* __restrict__ Uw,
+                                                        const double* __restrict__ Vw, const uint32_t* __restrict__ bmap,
+                                                        int32_t* __restrict__ piv, int kws, double eps) {
+  __shared__ double red[8 * 17 + 8];
+  const int64_t c = big[blockIdx.x];
+  AcaState st = S[c];
+  if (st.status != 0 || st.skip) return;
+  const AcaBlk b = B[c];
+  aca_update_block<8>(b, st, Uw, Vw, bmap, piv, c, kws, eps, threadIdx.x >> 5, threadIdx.x & 31, red);
+  if (threadIdx.x == 0) S[c] = st;
 }
 
 __global__ void k_init_state(AcaState* __restrict__ S, int64_t nb) {
@@ -279,6 +407,7 @@ void aca_eval(Context& C, const M& m, int64_t total, AcaWork& W) {
   cudaStream_t st = C.stream;
   W.cnt.alloc(2);
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 2 * sizeof(unsigned long long), st));
+  KScope ks(C, KF_EVAL_ACA);
   k_eval_class3<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(total, 128), 148 * 16);
@@ -295,6 +424,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   cudaStream_t st = C.stream;
   const int64_t nb = (int64_t)ids.size();
   std::vector<AcaBlk> hb(nb);
+  std::vector<int32_t> hbig;
   int64_t uo = 0, vo = 0, bo = 0;
   for (int64_t c = 0; c < nb; ++c) {
     const Quad& q = C.h_adm[C.adm_begin + ids[c]];
@@ -308,8 +438,12 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     uo += (int64_t)b.m * kws;
     vo += (int64_t)b.n * kws;
     bo += (b.m + 31) / 32;
+    if (b.m + b.n >= kBigMN) hbig.push_back((int32_t)c);
   }
+  const int64_t nbig = (int64_t)hbig.size();
   W.blk.alloc(nb); W.state.alloc(nb); W.owned.alloc(nb); W.piv.alloc(nb * 2 * kws);
+  W.act.alloc(nb + 1); W.flag.alloc(nb + 1); W.pos.alloc(nb + 1); W.tot.alloc(3); W.big.alloc(nbig);
+  if (nbig) HM_CUDA(cudaMemcpyAsync(W.big.get(), hbig.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   W.rsz.alloc(nb + 1); W.csz.alloc(nb + 1); W.rpre.alloc(nb + 1); W.cpre.alloc(nb + 1);
   W.Uw.alloc(uo); W.Vw.alloc(vo); W.bmap.alloc(bo);
   HM_CUDA(cudaMemcpyAsync(W.blk.get(), hb.data(), nb * sizeof(AcaBlk), cudaMemcpyHostToDevice, st));
@@ -319,7 +453,14 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   HM_CHECK_LAUNCH();
   const Panel* P = C.panel.get();
   for (int step = 0;; ++step) {
-    k_step_sizes<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.rsz.get(), W.csz.get());
+    std::unique_ptr<KScope> ks(new KScope(C, KF_ACA_OTHER));
+    k_step_flags<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.state.get(), nb, W.flag.get());
+    HM_CHECK_LAUNCH();
+    cub_call(W.tmp, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, W.flag.get(), W.pos.get(), nb + 1, st);
+    });
+    k_step_compact<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.flag.get(), W.pos.get(), nb, W.act.get(),
+                                                          W.rsz.get(), W.csz.get());
     HM_CHECK_LAUNCH();
     cub_call(W.tmp, [&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, W.rsz.get(), W.rpre.get(), nb + 1, st);
@@ -327,21 +468,35 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     cub_call(W.tmp, [&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, W.csz.get(), W.cpre.get(), nb + 1, st);
     });
-    int64_t tot[2];
-    HM_CUDA(cudaMemcpyAsync(&tot[0], W.rpre.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    HM_CUDA(cudaMemcpyAsync(&tot[1], W.cpre.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    k_step_totals<<<1, 1, 0, st>>>(W.rpre.get(), W.cpre.get(), W.pos.get(), nb, W.tot.get());
+    HM_CHECK_LAUNCH();
+    int64_t tot[3];
+    HM_CUDA(cudaMemcpyAsync(tot, W.tot.get(), sizeof(tot), cudaMemcpyDeviceToHost, st));
+    ks.reset();
     HM_CUDA(cudaStreamSynchronize(st));
     if (tot[0] == 0) break;
+    const int64_t nact = tot[2];
     C.aca_steps++;
     C.entries_aca += (double)(tot[0] + tot[1]);
     W.lists.alloc(std::max(tot[0], tot[1]));
-    aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), nb, W.Uw.get(), W.Vw.get()}, tot[0], W);
-    k_aca_pivot<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Vw.get(), W.bmap.get());
+    aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), nb, W.Uw.get(), W.Vw.get()},
+             tot[0], W);
+    ks.reset(new KScope(C, KF_ACA_OTHER));
+    k_aca_pivot<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, W.Vw.get(),
+                                                          W.bmap.get());
     HM_CHECK_LAUNCH();
-    aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), nb, W.Uw.get(), W.Vw.get()}, tot[1], W);
-    k_aca_update<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.Uw.get(), W.Vw.get(),
-                                                         W.bmap.get(), W.piv.get(), kws, C.eps_aca);
+    ks.reset();
+    aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), nb, W.Uw.get(), W.Vw.get()},
+             tot[1], W);
+    ks.reset(new KScope(C, KF_ACA_OTHER));
+    k_aca_update<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, W.Uw.get(),
+                                                           W.Vw.get(), W.bmap.get(), W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();
+    if (nbig) {
+      k_aca_update_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), W.Uw.get(), W.Vw.get(),
+                                                       W.bmap.get(), W.piv.get(), kws, C.eps_aca);
+      HM_CHECK_LAUNCH();
+    }
   }
   // pack finished blocks into the factor pool
   k_final_sizes<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.rsz.get());

@@ -113,6 +113,35 @@ void VmmPool::release() {
   base = 0; reserved = mapped = used = 0;
 }
 
+// ---- kernel-family timers -------------------------------------------------------------------
+cudaEvent_t KTimer::get() {
+  if (pool.empty()) {
+    cudaEvent_t e;
+    HM_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = pool.back();
+  pool.pop_back();
+  return e;
+}
+void KTimer::resolve() {
+  for (auto& p : pend) {
+    float t = 0;
+    if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) { ms[p.fam] += t; n[p.fam] += 1; }
+    else cudaGetLastError();
+    pool.push_back(p.a);
+    pool.push_back(p.b);
+  }
+  pend.clear();
+}
+void KTimer::reset() {
+  for (int f = 0; f < KF_NUM; ++f) { ms[f] = 0; n[f] = 0; }
+}
+KTimer::~KTimer() {
+  for (auto& p : pend) { pool.push_back(p.a); pool.push_back(p.b); }
+  for (auto e : pool) cudaEventDestroy(e);
+}
+
 // ---- NCCL ---------------------------------------------------------------------------------
 void allreduce_sum(Context& C, double* buf, int64_t n) {
   HM_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, C.comm, C.stream));
@@ -267,6 +296,13 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
     else if (k == "aca_kws") { if (v < 1 || v > 64) bad(); C.aca_kws = v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
+    else if (k == "kernel_timing") {
+      if (v != 0 && v != 1) bad();
+      HM_CUDA(cudaStreamSynchronize(C.stream));
+      C.kt.resolve();
+      C.kt.reset();
+      C.kt.on = v == 1;
+    }
     else hm::fail(HM_ERR_ARG, "hm_set_option: unknown key '" + k + "'");
   });
 }
@@ -282,6 +318,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "aca_chunk_mb") *v = C.aca_chunk_mb;
     else if (k == "aca_kws") *v = C.aca_kws;
     else if (k == "record_pivots") *v = C.record_pivots;
+    else if (k == "kernel_timing") *v = C.kt.on ? 1 : 0;
     else hm::fail(HM_ERR_ARG, "hm_get_option: unknown key '" + k + "'");
   });
 }
@@ -323,6 +360,7 @@ hm_status hm_setup(hm_ctx ctx, double eps_aca) {
       C.times.plan_ms = t.ms();
     }
     C.times.setup_ms = all.ms();
+    C.kt.resolve();
     C.have_setup = true;
   });
 }
@@ -360,6 +398,7 @@ hm_status hm_solve(hm_ctx ctx, const double* rhs, double* sol, double tol, int* 
     hm::scatter_perm(C, C.yin.get(), vx.out());
     vx.finish();
     C.times.solve_ms = t.ms();
+    C.kt.resolve();
     C.times.solve_iters = it;
     C.times.solve_relres = rr;
     if (iters_out) *iters_out = it;
@@ -490,6 +529,8 @@ hm_status hm_quadrature_table(int n, double* nodes, double* weights) {
 
 hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
   return guarded(ctx, [&](Context& C) {
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+    C.kt.resolve();
     std::ostringstream o;
     o.precision(17);
     int64_t kmin = 0, kmax = 0;
@@ -519,7 +560,11 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
       << ",\"solve_iters\":" << C.times.solve_iters << ",\"solve_relres\":" << C.times.solve_relres
       << ",\"launches\":" << hm::g_launches << ",\"mv_batches\":" << C.mv_nbatches << ",\"lr_small\":" << C.n_lr_small << ",\"lr_large\":" << C.n_lr_large << ",\"rank_hist\":[";
     for (int k = 0; k <= 64; ++k) o << (k ? "," : "") << hist[k];
-    o << "]}";
+    o << "],\"kt\":{\"on\":" << (C.kt.on ? 1 : 0);
+    const char* fam[hm::KF_NUM] = {"eval_near", "eval_aca", "aca_other", "matvec"};
+    for (int f = 0; f < hm::KF_NUM; ++f)
+      o << ",\"" << fam[f] << "_ms\":" << C.kt.ms[f] << ",\"" << fam[f] << "_n\":" << C.kt.n[f];
+    o << "}}";
     std::string s = o.str();
     if (!buf || len < (int64_t)s.size() + 1)
       hm::fail(HM_ERR_ARG, "hm_get_stats: buffer too small, need " + std::to_string(s.size() + 1));

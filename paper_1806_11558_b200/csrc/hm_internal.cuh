@@ -104,20 +104,26 @@ struct VmmPool {
   ~VmmPool() { release(); }
 };
 
-// matvec plan records (matvec.cu)
+// matvec plan records (matvec.cu).  A batch is one pipeline stage of k_mv_batched:
+//   [header + task records | x_sigma segments | leaf storage], each part 16-B aligned,
+// filled by bulk copies (MvSeg) from four bases: 0 dense store, 1 factor pool, 2 the task
+// stream (C.mv_tasks), 3 the x vector.
 struct MvTask {
-  int32_t rlo, clo, loff;   // loff: offset in doubles from the batch's staged start
+  int32_t rlo;              // first internal row of the leaf (y += ...)
+  int32_t xoff;             // stage offset (doubles) of x[clo]
+  int32_t loff;             // stage offset (doubles) of the leaf's storage
   uint32_t mnk;             // m | n << 11 | k << 22 (k == 0: dense m x n row-major)
-};
-struct MvSeg {              // one bulk copy: [src, src + bytes) of a base -> stage offset dst
+};                          // header record of a batch: {count, 0, 0, 0}
+struct MvSeg {              // one bulk copy: [src, src + bytes) of base -> stage offset dst
   int64_t src;              // byte offset (16-B aligned) from the base pointer
-  int32_t bytes;            // multiple of 16
-  int32_t dst;              // byte offset in the stage (16-B aligned)
+  uint16_t bytes;           // multiple of 16
+  uint16_t dst;             // byte offset in the stage (16-B aligned)
+  uint16_t base;            // 0 dense store, 1 factor pool, 2 task stream, 3 x
+  uint16_t pad;
 };
 struct MvBatch {
   int32_t first_seg, nseg;  // bulk copies filling one stage
-  int32_t first, count;     // tasks
-  int32_t base, bytes;      // base 0 dense store / 1 factor pool; total bytes of the stage
+  int32_t bytes, count;     // total bytes of the stage (expect_tx), tasks
 };
 struct MvLarge {
   int32_t rlo, clo, m, n, k, pad;
@@ -149,6 +155,22 @@ struct PhaseTimes {
   double last_matvec_ms = 0, solve_ms = 0;
   int solve_iters = 0;
   double solve_relres = 0;
+};
+
+// Per-kernel-family device timing (option "kernel_timing"): CUDA events recorded on the
+// library stream around every launch of a family, resolved at the next synchronous point.
+enum KFam { KF_EVAL_NEAR = 0, KF_EVAL_ACA = 1, KF_ACA_OTHER = 2, KF_MATVEC = 3, KF_NUM = 4 };
+struct KTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  struct P { int fam; cudaEvent_t a, b; };
+  std::vector<P> pend;
+  double ms[KF_NUM] = {0, 0, 0, 0};
+  int64_t n[KF_NUM] = {0, 0, 0, 0};
+  cudaEvent_t get();
+  void resolve();   // caller has synchronised the stream
+  void reset();
+  ~KTimer();
 };
 
 // Context ---------------------------------------------------------------------------------
@@ -227,7 +249,24 @@ struct Context {
   int64_t mv_n_large = 0, mv_n_dense_big = 0, mv_n_tiles_v = 0, mv_n_tiles_u = 0;
 
   PhaseTimes times;
+  KTimer kt;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+// scope = one timed launch (or a group of launches) of family f on the library stream
+struct KScope {
+  Context& C;
+  int f;
+  cudaEvent_t a = nullptr;
+  KScope(Context& c, int fam) : C(c), f(fam) {
+    if (C.kt.on) { a = C.kt.get(); cudaEventRecord(a, C.stream); }
+  }
+  ~KScope() {
+    if (!a) return;
+    cudaEvent_t b = C.kt.get();
+    cudaEventRecord(b, C.stream);
+    C.kt.pend.push_back(KTimer::P{f, a, b});
+  }
 };
 
 // tree.cu

@@ -26,7 +26,7 @@
 namespace hm {
 
 constexpr int kMvStages = 4;
-constexpr int kMvStageBytes = 44 * 1024;
+constexpr int kMvStageBytes = 48 * 1024;
 constexpr int kMvThreads = 512;
 constexpr int kMvSmallMax = 16 * 1024;
 
@@ -70,50 +70,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
-// x_sigma for a leaf, preloaded once per warp (one coalesced load per 32 columns) and handed
-// to the lane that needs column c with a shuffle: no L2 round trip inside the column loop.
-template <int NX>
-struct XReg {
-  double v[NX];
-  __device__ __forceinline__ void load(const double* __restrict__ x, int n, int lane) {
-#pragma unroll
-    for (int i = 0; i < NX; ++i) v[i] = (i * 32 + lane < n) ? __ldg(x + i * 32 + lane) : 0.0;
-  }
-  __device__ __forceinline__ double get(int c) const {   // warp-collective, c uniform per lane group
-    double r = 0.0;
-#pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      const double t = __shfl_sync(0xffffffffu, v[i], c & 31);
-      r = (c >> 5) == i ? t : r;
-    }
-    return r;
-  }
-};
-
-// Dense m x n row-major block: S lanes per row (consecutive columns -> conflict-free shared
-// loads for the leaf widths of CBC), 32/S rows per pass, P passes held in registers so the
-// P shuffle reductions are independent (ILP instead of P serial reduction chains).
-template <int S, int P, int NX>
-__device__ __forceinline__ void dense_block(const double* __restrict__ B, int m, int n, const double* __restrict__ x,
+// Dense m x n row-major block out of shared memory, x_sigma staged beside it: S lanes per
+// row (consecutive columns -> conflict-free shared loads for the leaf widths of CBC), 32/S
+// rows per pass, P passes held in registers so the P shuffle reductions are independent.
+template <int S, int P>
+__device__ __forceinline__ void dense_block(const double* __restrict__ B, int m, int n, const double* __restrict__ xs,
                                             double* __restrict__ y, int lane) {
   constexpr int RPP = 32 / S;
   const int sub = lane % S, rr = lane / S;
-  XReg<NX> xr;
-  xr.load(x, n, lane);
-  const int iters = (n + S - 1) / S;
   for (int r0 = 0; r0 < m; r0 += RPP * P) {
     double acc[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) acc[p] = 0.0;
-    for (int it = 0; it < iters; ++it) {
-      const int c = sub + it * S;
-      const double xc = xr.get(c);
-      if (c < n)
+    for (int c = sub; c < n; c += S) {
+      const double xc = xs[c];
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const int r = r0 + rr + p * RPP;
-          if (r < m) acc[p] += B[r * n + c] * xc;
-        }
+      for (int p = 0; p < P; ++p) {
+        const int r = r0 + rr + p * RPP;
+        if (r < m) acc[p] = __fma_rn(B[r * n + c], xc, acc[p]);
+      }
     }
 #pragma unroll
     for (int o = S / 2; o > 0; o >>= 1)
@@ -128,48 +103,28 @@ __device__ __forceinline__ void dense_block(const double* __restrict__ B, int m,
   }
 }
 
-__device__ __forceinline__ void dense_any(const double* B, int m, int n, const double* x, double* y, int lane) {
-  if (n <= 16) dense_block<2, 4, 1>(B, m, n, x, y, lane);
-  else if (n <= 32) dense_block<4, 4, 1>(B, m, n, x, y, lane);
-  else if (n <= 64) dense_block<4, 4, 2>(B, m, n, x, y, lane);
-  else if (n <= 128) dense_block<8, 4, 4>(B, m, n, x, y, lane);
-  else {   // generic (large leaf_size only): direct loads
-    for (int r = 0; r < m; ++r) {
-      double acc = 0.0;
-      for (int c = lane; c < n; c += 32) acc += B[r * n + c] * __ldg(x + c);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) atomicAdd(y + r, acc);
-    }
-  }
+__device__ __forceinline__ void dense_any(const double* B, int m, int n, const double* xs, double* y, int lane) {
+  if (n <= 16) dense_block<2, 4>(B, m, n, xs, y, lane);
+  else if (n <= 64) dense_block<4, 4>(B, m, n, xs, y, lane);
+  else dense_block<8, 4>(B, m, n, xs, y, lane);
 }
 
-// Low-rank block U (m x k) | V (n x k), column-major, columns [l0, l0 + kc) (kc <= KB): t = V^T x
-// with all kc column sums in registers (x_j loaded up front, 4 rows of x per lane in flight),
-// one butterfly reduction over the kc sums at once, then y += U t (kc independent loads per row).
+// Low-rank block U (m x k) | V (n x k), column-major, columns [l0, l0 + kc) (kc <= KB), out of
+// shared memory: t = V^T x with all kc column sums in registers, one butterfly over the kc
+// sums at once, then y += U t (one FP64 atomic per row).
 template <int KB>
 __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int m, int n, int k, int l0, int kc,
-                                              const double* __restrict__ x, double* __restrict__ y, int lane) {
-  const double* V = U0 + (int64_t)m * k + (int64_t)l0 * n;
-  const double* U = U0 + (int64_t)l0 * m;
+                                              const double* __restrict__ xs, double* __restrict__ y, int lane) {
+  const double* V = U0 + m * k + l0 * n;
+  const double* U = U0 + l0 * m;
   double acc[KB];
 #pragma unroll
   for (int l = 0; l < KB; ++l) acc[l] = 0.0;
-  for (int j0 = 0; j0 < n; j0 += 128) {
-    double xj[4];
+  for (int j = lane; j < n; j += 32) {
+    const double xj = xs[j];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = j0 + q * 32 + lane;
-      xj[q] = j < n ? __ldg(x + j) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = j0 + q * 32 + lane;
-      if (j < n)
-#pragma unroll
-        for (int l = 0; l < KB; ++l)
-          if (l < kc) acc[l] += V[j + (int64_t)l * n] * xj[q];
-    }
+    for (int l = 0; l < KB; ++l)
+      if (l < kc) acc[l] = __fma_rn(V[j + l * n], xj, acc[l]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
@@ -179,26 +134,28 @@ __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int
     double s = 0.0;
 #pragma unroll
     for (int l = 0; l < KB; ++l)
-      if (l < kc) s += U[t + (int64_t)l * m] * acc[l];
+      if (l < kc) s = __fma_rn(U[t + l * m], acc[l], s);
     atomicAdd(y + t, s);
   }
 }
 
-__device__ __forceinline__ void lowrank_any(const double* U, int m, int n, int k, const double* x, double* y,
+__device__ __forceinline__ void lowrank_any(const double* U, int m, int n, int k, const double* xs, double* y,
                                             int lane) {
-  if (k <= 8) lowrank_block<8>(U, m, n, k, 0, k, x, y, lane);
-  else if (k <= 16) lowrank_block<16>(U, m, n, k, 0, k, x, y, lane);
+  if (k <= 8) lowrank_block<8>(U, m, n, k, 0, k, xs, y, lane);
+  else if (k <= 16) lowrank_block<16>(U, m, n, k, 0, k, xs, y, lane);
   else
-    for (int l0 = 0; l0 < k; l0 += 16) lowrank_block<16>(U, m, n, k, l0, min(16, k - l0), x, y, lane);
+    for (int l0 = 0; l0 < k; l0 += 16) lowrank_block<16>(U, m, n, k, l0, min(16, k - l0), xs, y, lane);
 }
 
-// Warp-specialised pipeline: warp 0 is the producer (one lane issues the bulk copies, waits
-// on the per-stage "empty" barrier before reusing a stage); warps 1..NW-1 consume every stage
-// (tasks round-robin), then arrive on its "empty" barrier.  A slow task delays only the refill
-// of its own stage, not the other consumers.
+// Warp-specialised pipeline.  Warp 0 is the producer: per batch, lane 0 posts the stage's
+// byte count on its "full" mbarrier, then the 32 lanes issue the batch's bulk copies
+// (task records, x_sigma segments, leaf storage) after the stage's "empty" barrier has
+// flipped.  Warps 1..NW-1 consume every stage entirely out of shared memory (tasks
+// round-robin) — no global load on the consumer side, only fire-and-forget atomics into
+// the L2-resident y — then arrive on the stage's "empty" barrier.
 __global__ void __launch_bounds__(kMvThreads, 1)
     k_mv_batched(const MvBatch* __restrict__ batches, const MvSeg* __restrict__ segs, const int32_t* __restrict__ cta_first,
-                 const MvTask* __restrict__ tasks, const char* __restrict__ base0, const char* __restrict__ base1,
+                 const char* __restrict__ base0, const char* __restrict__ base1, const char* __restrict__ base2,
                  const double* __restrict__ x, double* __restrict__ y) {
   constexpr int NW = kMvThreads / 32, NC = NW - 1;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -216,17 +173,18 @@ __global__ void __launch_bounds__(kMvThreads, 1)
   }
   __syncthreads();
   if (warp == 0) {
-    if (lane == 0) {
-      for (int it = 0; it < nb; ++it) {
-        const int stage = it % kMvStages;
-        if (it >= kMvStages) mbar_wait(&empty[stage], (unsigned)(((it / kMvStages) - 1) & 1));
-        const MvBatch B = batches[b0 + it];
-        mbar_expect_tx(&full[stage], (unsigned)B.bytes);
-        const char* base = B.base ? base1 : base0;
-        for (int s = 0; s < B.nseg; ++s) {
-          const MvSeg S = segs[B.first_seg + s];
-          bulk_g2s(buf + stage * kMvStageBytes + S.dst, base + S.src, (unsigned)S.bytes, &full[stage]);
-        }
+    for (int it = 0; it < nb; ++it) {
+      const int stage = it % kMvStages;
+      if (it >= kMvStages) mbar_wait(&empty[stage], (unsigned)(((it / kMvStages) - 1) & 1));
+      const MvBatch B = batches[b0 + it];
+      if (lane == 0) mbar_expect_tx(&full[stage], (unsigned)B.bytes);
+      __syncwarp();
+      unsigned char* sb = buf + stage * kMvStageBytes;
+      for (int s = lane; s < B.nseg; s += 32) {
+        const MvSeg S = segs[B.first_seg + s];
+        const char* base = S.base == 0 ? base0 : S.base == 1 ? base1 : S.base == 2 ? base2
+                                                                     : reinterpret_cast<const char*>(x);
+        bulk_g2s(sb + S.dst, base + S.src, (unsigned)S.bytes, &full[stage]);
       }
     }
     return;
@@ -234,23 +192,16 @@ __global__ void __launch_bounds__(kMvThreads, 1)
   for (int it = 0; it < nb; ++it) {
     const int stage = it % kMvStages;
     mbar_wait(&full[stage], (unsigned)((it / kMvStages) & 1));
-    const MvBatch B = batches[b0 + it];
-    const double* data = reinterpret_cast<const double*>(buf + stage * kMvStageBytes);
-    // this warp's task descriptors for the stage, one per lane, loaded at once
-    MvTask mine = {0, 0, 0, 0};
-    {
-      const int t = warp - 1 + NC * lane;
-      if (t < B.count) mine = tasks[B.first + t];
-    }
-    for (int i = 0, t = warp - 1; t < B.count; ++i, t += NC) {
-      MvTask T;
-      T.rlo = __shfl_sync(0xffffffffu, mine.rlo, i);
-      T.clo = __shfl_sync(0xffffffffu, mine.clo, i);
-      T.loff = __shfl_sync(0xffffffffu, mine.loff, i);
-      T.mnk = __shfl_sync(0xffffffffu, mine.mnk, i);
-      const int m = T.mnk & 2047, n = (T.mnk >> 11) & 2047, k = T.mnk >> 22;
-      if (k == 0) dense_any(data + T.loff, m, n, x + T.clo, y + T.rlo, lane);
-      else lowrank_any(data + T.loff, m, n, k, x + T.clo, y + T.rlo, lane);
+    const unsigned char* sb = buf + stage * kMvStageBytes;
+    const double* sd = reinterpret_cast<const double*>(sb);
+    const int4* rec = reinterpret_cast<const int4*>(sb);
+    const int count = rec[0].x;
+    for (int t = warp - 1; t < count; t += NC) {
+      const int4 T = rec[1 + t];
+      const uint32_t mnk = (uint32_t)T.w;
+      const int m = mnk & 2047, n = (mnk >> 11) & 2047, k = mnk >> 22;
+      if (k == 0) dense_any(sd + T.z, m, n, sd + T.y, y + T.x, lane);
+      else lowrank_any(sd + T.z, m, n, k, sd + T.y, y + T.x, lane);
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[stage])) : "memory");
@@ -285,7 +236,7 @@ __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ 
         vb[l] = (l < kc && two) ? __ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
       }
 #pragma unroll
-      for (int l = 0; l < 8; ++l) acc[l] += va[l] * xa + vb[l] * xb;
+      for (int l = 0; l < 8; ++l) acc[l] = __fma_rn(vb[l], xb, __fma_rn(va[l], xa, acc[l]));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -321,12 +272,12 @@ __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ 
         const double u0 = __ldg(U + t + (int64_t)l * B.m), u1 = __ldg(U + t + (int64_t)(l + 1) * B.m);
         const double w0 = two ? __ldg(U + t + 32 + (int64_t)l * B.m) : 0.0;
         const double w1 = two ? __ldg(U + t + 32 + (int64_t)(l + 1) * B.m) : 0.0;
-        s0 += u0 * ta; s1 += u1 * tb; r0 += w0 * ta; r1 += w1 * tb;
+        s0 = __fma_rn(u0, ta, s0); s1 = __fma_rn(u1, tb, s1); r0 = __fma_rn(w0, ta, r0); r1 = __fma_rn(w1, tb, r1);
       }
       if (l < B.k) {
         const double ta = __ldg(tl + l);
-        s0 += __ldg(U + t + (int64_t)l * B.m) * ta;
-        if (two) r0 += __ldg(U + t + 32 + (int64_t)l * B.m) * ta;
+        s0 = __fma_rn(__ldg(U + t + (int64_t)l * B.m), ta, s0);
+        if (two) r0 = __fma_rn(__ldg(U + t + 32 + (int64_t)l * B.m), ta, r0);
       }
       atomicAdd(y + B.rlo + t, s0 + s1);
       if (two) atomicAdd(y + B.rlo + t + 32, r0 + r1);
@@ -358,7 +309,7 @@ void plan_matvec(Context& C) {
     HM_CUDA(cudaMemcpyAsync(C.h_dense.data(), C.dense.get(), C.ndense * sizeof(Quad), cudaMemcpyDeviceToHost, st));
   }
   HM_CUDA(cudaStreamSynchronize(st));
-  struct Item { int64_t byte0, bytes; int base; MvTask t; };
+  struct Item { int64_t byte0, bytes; int base; int32_t rlo, clo, n; uint32_t mnk; };
   std::vector<Item> items;
   items.reserve(nd + na);
   std::vector<MvLarge> dense_big, large;
@@ -366,11 +317,11 @@ void plan_matvec(Context& C) {
     const Quad& q = C.h_dense[C.dense_begin + b];
     const int m = q.rhi - q.rlo, n = q.chi - q.clo;
     const int64_t bytes = 8 * (int64_t)m * n;
-    if (bytes + 32 > kMvStageBytes || m > 2047 || n > 2047) {
+    if (bytes + 8 * n + 64 > kMvStageBytes || m > 2047 || n > 2047) {
       dense_big.push_back(MvLarge{q.rlo, q.clo, m, n, 0, 0, hoff[b], 0});
       continue;
     }
-    items.push_back(Item{8 * hoff[b], bytes, 0, MvTask{q.rlo, q.clo, 0, (uint32_t)m | ((uint32_t)n << 11)}});
+    items.push_back(Item{8 * hoff[b], bytes, 0, q.rlo, q.clo, n, (uint32_t)m | ((uint32_t)n << 11)});
   }
   std::vector<int64_t> lr_order;
   for (int64_t b = 0; b < na; ++b)
@@ -382,52 +333,82 @@ void plan_matvec(Context& C) {
     const Quad& q = C.h_adm[C.adm_begin + b];
     const int m = q.rhi - q.rlo, n = q.chi - q.clo, k = C.h_rank[b];
     const int64_t bytes = 8 * (int64_t)k * (m + n);
-    if (bytes <= kMvSmallMax && m <= 2047 && n <= 2047) {
-      items.push_back(Item{8 * C.h_foff[b], bytes, 1,
-                           MvTask{q.rlo, q.clo, 0, (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)}});
+    if (bytes <= kMvSmallMax && m <= 2047 && n <= 2047 && k <= 1023) {
+      items.push_back(Item{8 * C.h_foff[b], bytes, 1, q.rlo, q.clo, n,
+                           (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)});
     } else {
       large.push_back(MvLarge{q.rlo, q.clo, m, n, k, 0, C.h_foff[b], tl});
       tl += k;
     }
   }
-  // batches: consecutive items (same base) filling one stage; each contiguous run of items
-  // becomes one bulk-copy segment (16-B aligned superset of the run)
+  // Batches: consecutive items filling one stage = [header + task records | x_sigma ranges |
+  // storage runs].  x ranges are 16-B aligned supersets [clo & ~1, (clo + n + 1) & ~1) in
+  // doubles, shared by the leaves of a batch with the same sigma; storage runs are maximal
+  // runs of contiguous items (16-B aligned supersets), one bulk copy each.
   std::vector<MvBatch> batches;
   std::vector<MvSeg> segs;
-  std::vector<MvTask> tasks;
-  tasks.reserve(items.size());
+  std::vector<MvTask> stream;     // per batch: header {count,0,0,0} + count task records
+  stream.reserve(items.size() + items.size() / 4 + 16);
+  struct XR { int64_t a0, a1; };
+  struct Run { int base; int64_t a0, a1, end; };
+  std::vector<XR> xr;
+  std::vector<Run> runs;
+  std::vector<int> item_x, item_run;
   for (size_t i = 0; i < items.size();) {
-    MvBatch B{};
-    B.first_seg = (int32_t)segs.size();
-    B.first = (int32_t)tasks.size();
-    B.base = items[i].base;
-    int32_t used = 0;
+    xr.clear(); runs.clear(); item_x.clear(); item_run.clear();
+    int64_t xb = 0, db = 0;
     size_t j = i;
-    while (j < items.size() && items[j].base == B.base) {
-      // the run of contiguous items starting at j
-      size_t r = j + 1;
-      int64_t end = items[j].byte0 + items[j].bytes;
-      const int64_t a0 = items[j].byte0 & ~int64_t(15);
-      while (r < items.size() && items[r].base == B.base && items[r].byte0 == end &&
-             ((items[r].byte0 + items[r].bytes + 15) & ~int64_t(15)) - a0 + used <= kMvStageBytes) {
-        end = items[r].byte0 + items[r].bytes;
-        ++r;
-      }
-      const int64_t a1 = (end + 15) & ~int64_t(15);
-      if (used + (a1 - a0) > kMvStageBytes) break;          // next run does not fit: close the batch
-      segs.push_back(MvSeg{a0, (int32_t)(a1 - a0), used});
-      for (size_t k = j; k < r; ++k) {
-        MvTask t = items[k].t;
-        t.loff = (int32_t)((used + (items[k].byte0 - a0)) / 8);
-        tasks.push_back(t);
-      }
-      used += (int32_t)(a1 - a0);
-      j = r;
+    for (; j < items.size(); ++j) {
+      const Item& it = items[j];
+      const int64_t xa0 = it.clo & ~int64_t(1), xa1 = (it.clo + it.n + 1) & ~int64_t(1);
+      int xi = -1;
+      for (int r = (int)xr.size() - 1; r >= 0 && r >= (int)xr.size() - 8; --r)
+        if (xr[r].a0 <= xa0 && xa1 <= xr[r].a1) { xi = r; break; }
+      const int64_t xcost = xi >= 0 ? 0 : 8 * (xa1 - xa0);
+      const bool ext = !runs.empty() && runs.back().base == it.base && runs.back().end == it.byte0;
+      const int64_t ra0 = ext ? runs.back().a0 : (it.byte0 & ~int64_t(15));
+      const int64_t ra1 = (it.byte0 + it.bytes + 15) & ~int64_t(15);
+      const int64_t dcost = ext ? ra1 - runs.back().a1 : ra1 - ra0;
+      const int64_t hb = 16 * (int64_t)(item_x.size() + 2);
+      if (hb + xb + xcost + db + dcost > kMvStageBytes) break;
+      if (xi < 0) { xr.push_back(XR{xa0, xa1}); xi = (int)xr.size() - 1; }
+      xb += xcost;
+      if (ext) { runs.back().a1 = ra1; runs.back().end = it.byte0 + it.bytes; }
+      else runs.push_back(Run{it.base, ra0, ra1, it.byte0 + it.bytes});
+      db += dcost;
+      item_x.push_back(xi);
+      item_run.push_back((int)runs.size() - 1);
     }
     if (j == i) fail(HM_ERR_CUDA, "matvec plan: leaf larger than a pipeline stage");
+    const int count = (int)(j - i);
+    MvBatch B{};
+    B.first_seg = (int32_t)segs.size();
+    B.count = count;
+    // layout
+    const int64_t hbytes = 16 * (int64_t)(count + 1);
+    std::vector<int64_t> xoff(xr.size()), roff(runs.size());
+    int64_t off = hbytes;
+    for (size_t r = 0; r < xr.size(); ++r) { xoff[r] = off; off += 8 * (xr[r].a1 - xr[r].a0); }
+    for (size_t r = 0; r < runs.size(); ++r) { roff[r] = off; off += runs[r].a1 - runs[r].a0; }
+    B.bytes = (int32_t)off;
+    segs.push_back(MvSeg{16 * (int64_t)stream.size(), (uint16_t)hbytes, 0, 2, 0});
+    for (size_t r = 0; r < xr.size(); ++r)
+      segs.push_back(MvSeg{8 * xr[r].a0, (uint16_t)(8 * (xr[r].a1 - xr[r].a0)), (uint16_t)xoff[r], 3, 0});
+    for (size_t r = 0; r < runs.size(); ++r)
+      segs.push_back(MvSeg{runs[r].a0, (uint16_t)(runs[r].a1 - runs[r].a0), (uint16_t)roff[r], (uint16_t)runs[r].base, 0});
     B.nseg = (int32_t)segs.size() - B.first_seg;
-    B.count = (int32_t)(j - i);
-    B.bytes = used;
+    stream.push_back(MvTask{count, 0, 0, 0});
+    for (int c = 0; c < count; ++c) {
+      const Item& it = items[i + c];
+      const XR& X = xr[item_x[c]];
+      const Run& R = runs[item_run[c]];
+      MvTask t;
+      t.rlo = it.rlo;
+      t.xoff = (int32_t)((xoff[item_x[c]] + 8 * (it.clo - X.a0)) / 8);
+      t.loff = (int32_t)((roff[item_run[c]] + (it.byte0 - R.a0)) / 8);
+      t.mnk = it.mnk;
+      stream.push_back(t);
+    }
     batches.push_back(B);
     i = j;
   }
@@ -465,7 +446,7 @@ void plan_matvec(Context& C) {
   };
   up(C.mv_batches, batches);
   up(C.mv_segs, segs);
-  up(C.mv_tasks, tasks);
+  up(C.mv_tasks, stream);
   up(C.mv_cta, cta_first);
   up(C.mv_large, large);
   up(C.mv_dense_big, dense_big);
@@ -503,13 +484,22 @@ void scatter_perm(Context& C, const double* y_int, double* y_app) {
 // y_int = (local leaves of H) x_int, then summed over ranks
 void matvec_internal(Context& C, const double* x_int, double* y_int) {
   cudaStream_t st = C.stream;
+  // the staged x_sigma copies need a 16-B aligned x with one readable double past N (every
+  // internal caller passes such a vector; anything else goes through an aligned copy)
+  if (reinterpret_cast<uintptr_t>(x_int) & 15) {
+    C.work.alloc(C.N + 2);
+    HM_CUDA(cudaMemcpyAsync(C.work.get(), x_int, C.N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    x_int = C.work.get();
+  }
+  std::unique_ptr<KScope> ks(new KScope(C, KF_MATVEC));
   HM_CUDA(cudaMemsetAsync(y_int, 0, C.N * sizeof(double), st));
   if (C.mv_tlen) HM_CUDA(cudaMemsetAsync(C.mv_tbuf.get(), 0, C.mv_tlen * sizeof(double), st));
   const double* pool = (const double*)C.fpool.base;
   if (C.mv_nbatches) {
     const int smem = 128 + kMvStages * kMvStageBytes;
-    k_mv_batched<<<C.mv_grid, kMvThreads, smem, st>>>(C.mv_batches.get(), C.mv_segs.get(), C.mv_cta.get(), C.mv_tasks.get(),
-                                                       (const char*)C.dstore.get(), (const char*)pool, x_int, y_int);
+    k_mv_batched<<<C.mv_grid, kMvThreads, smem, st>>>(C.mv_batches.get(), C.mv_segs.get(), C.mv_cta.get(),
+                                                       (const char*)C.dstore.get(), (const char*)pool,
+                                                       (const char*)C.mv_tasks.get(), x_int, y_int);
     HM_CHECK_LAUNCH();
   }
   if (C.mv_n_dense_big) {
@@ -525,6 +515,7 @@ void matvec_internal(Context& C, const double* x_int, double* y_int) {
                                           C.mv_tbuf.get(), y_int);
     HM_CHECK_LAUNCH();
   }
+  ks.reset();
   if (C.world > 1) allreduce_sum(C, y_int, C.N);
 }
 

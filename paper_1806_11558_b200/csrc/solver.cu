@@ -142,8 +142,9 @@ double true_relres(Context& C, Red& R, const double* b, const double* x, double 
 void cg(Context& C, const double* b, double* x, double tol, int* iters, double* relres) {
   const int64_t N = C.N;
   cudaStream_t st = C.stream;
-  C.krylov.alloc(3 * N);
-  double *r = C.krylov.get(), *p = r + N, *Ap = p + N;
+  const int64_t ld = (N + 32) & ~int64_t(31);   // 256-B aligned vectors with slack (matvec x staging)
+  C.krylov.alloc(3 * ld);
+  double *r = C.krylov.get(), *p = r + ld, *Ap = p + ld;
   Red R(C);
   HM_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st));
   HM_CUDA(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -174,9 +175,10 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
   const int64_t N = C.N;
   const int m = std::max(1, C.restart);
   cudaStream_t st = C.stream;
-  C.krylov.alloc((size_t)(m + 2) * N);
+  const int64_t ld = (N + 32) & ~int64_t(31);   // 256-B aligned basis vectors with slack (matvec x staging)
+  C.krylov.alloc((size_t)(m + 2) * ld);
   double* Vb = C.krylov.get();
-  double* w = Vb + (int64_t)(m + 1) * N;
+  double* w = Vb + (int64_t)(m + 1) * ld;
   Red R(C);
   DBuf<double> hdev, hsum;
   hdev.alloc(m + 8);
@@ -199,15 +201,15 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
     int jend = 0;
     bool conv = false;
     for (int j = 0; j < m; ++j) {
-      apply(C, Vb + (int64_t)j * N, w);
+      apply(C, Vb + (int64_t)j * ld, w);
       ++total;
       // CGS2
-      double* d1 = R.mdot(Vb, N, j + 1, w);
-      k_msub<<<vgrid(N), 256, 0, st>>>(Vb, N, j + 1, d1, w, N);
+      double* d1 = R.mdot(Vb, ld, j + 1, w);
+      k_msub<<<vgrid(N), 256, 0, st>>>(Vb, ld, j + 1, d1, w, N);
       HM_CHECK_LAUNCH();
       HM_CUDA(cudaMemcpyAsync(h.data(), d1, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
-      double* d2 = R.mdot(Vb, N, j + 1, w);
-      k_msub<<<vgrid(N), 256, 0, st>>>(Vb, N, j + 1, d2, w, N);
+      double* d2 = R.mdot(Vb, ld, j + 1, w);
+      k_msub<<<vgrid(N), 256, 0, st>>>(Vb, ld, j + 1, d2, w, N);
       HM_CHECK_LAUNCH();
       HM_CUDA(cudaMemcpyAsync(h2.data(), d2, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
       HM_CUDA(cudaStreamSynchronize(st));
@@ -228,7 +230,7 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
       jend = j + 1;
       if (std::fabs(g[j + 1]) <= tol * bn || total >= C.max_iter || hn == 0.0) { conv = true; break; }
       HM_CUDA(cudaMemcpyAsync(hdev.get(), &hn, sizeof(double), cudaMemcpyHostToDevice, st));
-      k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb + (int64_t)(j + 1) * N, N);
+      k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb + (int64_t)(j + 1) * ld, N);
       HM_CHECK_LAUNCH();
     }
     for (int i = jend - 1; i >= 0; --i) {
@@ -237,7 +239,7 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
       y[i] = s / H[i + (size_t)i * (m + 1)];
     }
     HM_CUDA(cudaMemcpyAsync(hdev.get(), y.data(), jend * sizeof(double), cudaMemcpyHostToDevice, st));
-    k_madd<<<vgrid(N), 256, 0, st>>>(Vb, N, jend, hdev.get(), x, N);
+    k_madd<<<vgrid(N), 256, 0, st>>>(Vb, ld, jend, hdev.get(), x, N);
     HM_CHECK_LAUNCH();
     HM_CUDA(cudaStreamSynchronize(st));
     if (conv && (std::fabs(g[jend]) <= tol * bn || total >= C.max_iter)) break;
