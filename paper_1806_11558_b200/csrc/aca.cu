@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 
 #include "entry_batch.cuh"
 
@@ -35,13 +36,16 @@ struct AcaState {
 struct AcaWork {
   DBuf<AcaBlk> blk;
   DBuf<AcaState> state;
-  DBuf<int32_t> owned, piv, act, flag, pos, big;
+  DBuf<int32_t> owned, piv, act, flag, pos, big, rtab, ctab;
   DBuf<int64_t> rsz, csz, rpre, cpre;
   DBuf<double> Uw, Vw;
   DBuf<uint32_t> bmap;
   DBuf<char> tmp;
   DBuf<unsigned long long> ev, cnt;
   DBuf<int64_t> tot;
+  std::vector<AcaBlk> h_blk;
+  std::vector<AcaState> h_state;
+  std::vector<int32_t> h_ids, h_big;
   DBuf<EntryRef> lists;
 };
 
@@ -70,6 +74,15 @@ __global__ void k_step_compact(const AcaBlk* __restrict__ B, const int32_t* __re
   csz[a] = B[c].m;
 }
 
+// segment-start table of a flattened batch: every 32-entry slot w gets the segment holding
+// entry 32 w (thread per active segment; the segments tile [0, total))
+__global__ void k_seg_table(const int64_t* __restrict__ pre, int64_t nact, int32_t* __restrict__ tab) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= nact) return;
+  const int64_t lo = pre[a], hi = pre[a + 1];
+  for (int64_t w = (lo + 31) >> 5; (w << 5) < hi; ++w) tab[w] = (int32_t)a;
+}
+
 __global__ void k_step_totals(const int64_t* __restrict__ rpre, const int64_t* __restrict__ cpre,
                               const int32_t* __restrict__ pos, int64_t nb, int64_t* __restrict__ tot) {
   tot[0] = rpre[nb];
@@ -88,12 +101,14 @@ struct AcaMap {
   const AcaState* S;
   const int64_t* pre;   // nb + 1 prefix of this step's row (or column) lengths, active blocks first
   const int32_t* act;   // compact index -> block
+  const int32_t* tab;   // tab[e / 32] = compact segment of entry 32 * (e / 32)
   int64_t nb;
   double* Uw;
   double* Vw;
   __device__ bool locate(int64_t e, bool valid, EntryRef& r) const {
-    const int64_t a = warp_find_segment(pre, nb + 1, e, valid);
     if (!valid) return false;
+    int64_t a = tab[e >> 5];
+    while (pre[a + 1] <= e) ++a;
     const int32_t c = act[a];
     if (!ROW && (S[c].skip || S[c].status != 0)) return false;
     r.seg = c;
@@ -422,9 +437,14 @@ void aca_eval(Context& C, const M& m, int64_t total, AcaWork& W) {
 void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws, std::vector<int32_t>& overflow,
                std::vector<std::vector<int32_t>>* pivots_out) {
   cudaStream_t st = C.stream;
+  using clk = std::chrono::steady_clock;
+  auto ms_since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
+  const auto t0 = clk::now();
   const int64_t nb = (int64_t)ids.size();
-  std::vector<AcaBlk> hb(nb);
-  std::vector<int32_t> hbig;
+  std::vector<AcaBlk>& hb = W.h_blk;
+  hb.resize(nb);
+  std::vector<int32_t>& hbig = W.h_big;
+  hbig.clear();
   int64_t uo = 0, vo = 0, bo = 0;
   for (int64_t c = 0; c < nb; ++c) {
     const Quad& q = C.h_adm[C.adm_begin + ids[c]];
@@ -452,6 +472,8 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   k_init_state<<<grid_for(nb, 256), 256, 0, st>>>(W.state.get(), nb);
   HM_CHECK_LAUNCH();
   const Panel* P = C.panel.get();
+  C.times.aca_phase_ms[0] += ms_since(t0);
+  const auto t1 = clk::now();
   for (int step = 0;; ++step) {
     std::unique_ptr<KScope> ks(new KScope(C, KF_ACA_OTHER));
     k_step_flags<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.state.get(), nb, W.flag.get());
@@ -473,20 +495,28 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     int64_t tot[3];
     HM_CUDA(cudaMemcpyAsync(tot, W.tot.get(), sizeof(tot), cudaMemcpyDeviceToHost, st));
     ks.reset();
+    const auto ts = clk::now();
     HM_CUDA(cudaStreamSynchronize(st));
+    C.times.aca_phase_ms[2] += ms_since(ts);
     if (tot[0] == 0) break;
     const int64_t nact = tot[2];
     C.aca_steps++;
     C.entries_aca += (double)(tot[0] + tot[1]);
     W.lists.alloc(std::max(tot[0], tot[1]));
-    aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), nb, W.Uw.get(), W.Vw.get()},
+    W.rtab.alloc(tot[0] / 32 + 2);
+    W.ctab.alloc(tot[1] / 32 + 2);
+    k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.rpre.get(), nact, W.rtab.get());
+    HM_CHECK_LAUNCH();
+    k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.cpre.get(), nact, W.ctab.get());
+    HM_CHECK_LAUNCH();
+    aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(), nb, W.Uw.get(), W.Vw.get()},
              tot[0], W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
     k_aca_pivot<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, W.Vw.get(),
                                                           W.bmap.get());
     HM_CHECK_LAUNCH();
     ks.reset();
-    aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), nb, W.Uw.get(), W.Vw.get()},
+    aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(), nb, W.Uw.get(), W.Vw.get()},
              tot[1], W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
     k_aca_update<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, W.Uw.get(),
@@ -498,6 +528,8 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
       HM_CHECK_LAUNCH();
     }
   }
+  C.times.aca_phase_ms[1] += ms_since(t1);
+  const auto t2 = clk::now();
   // pack finished blocks into the factor pool
   k_final_sizes<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.rsz.get());
   HM_CHECK_LAUNCH();
@@ -506,7 +538,8 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   });
   int64_t add = 0;
   HM_CUDA(cudaMemcpyAsync(&add, W.rpre.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  std::vector<AcaState> hs(nb);
+  std::vector<AcaState>& hs = W.h_state;
+  hs.resize(nb);
   HM_CUDA(cudaMemcpyAsync(hs.data(), W.state.get(), nb * sizeof(AcaState), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
   const int64_t base = (int64_t)(C.fpool.used / sizeof(double));
@@ -522,6 +555,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     HM_CUDA(cudaMemcpyAsync(hp.data(), W.piv.get(), hp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   }
   HM_CUDA(cudaStreamSynchronize(st));
+  C.times.aca_phase_ms[3] += ms_since(t2);
   for (int64_t c = 0; c < nb; ++c) {
     if (hs[c].status == 2) { overflow.push_back(ids[c]); continue; }
     if (pivots_out)
@@ -535,12 +569,16 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
 
 void setup_aca(Context& C) {
   cudaStream_t st = C.stream;
+  using clk = std::chrono::steady_clock;
+  auto ms_since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
+  const auto t0 = clk::now();
   const int64_t nb = C.adm_end - C.adm_begin;
   C.foff.alloc(nb + 1);
   C.frank.alloc(nb + 1);
   HM_CUDA(cudaMemsetAsync(C.frank.get(), 0, (nb + 1) * sizeof(int32_t), st));
   C.fpool.used = 0;
   C.aca_steps = 0; C.aca_chunks = 0; C.aca_overflow = 0;
+  for (double& t : C.times.aca_phase_ms) t = 0;
   C.entries_aca = 0;
   if (nb == 0) { C.factor_doubles = 0; C.evals_aca = 0; return; }
   if (C.h_adm.size() != (size_t)C.nadm) {
@@ -548,6 +586,7 @@ void setup_aca(Context& C) {
     HM_CUDA(cudaMemcpyAsync(C.h_adm.data(), C.adm.get(), C.nadm * sizeof(Quad), cudaMemcpyDeviceToHost, st));
     HM_CUDA(cudaStreamSynchronize(st));
   }
+  C.times.aca_phase_ms[8] = ms_since(t0);
   // reserve VA for the worst case (k_max terms per block), map on demand
   size_t worst = 0;
   for (int64_t b = C.adm_begin; b < C.adm_end; ++b) {
@@ -578,8 +617,14 @@ void setup_aca(Context& C) {
     if (ws > b) { W.Uw.release(); W.Vw.release(); }
     return std::max(b, 64.0 * 1048576.0);
   };
+  C.times.aca_phase_ms[6] = ms_since(t0);
+  const auto tb = clk::now();
   double budget = chunk_budget();
-  std::vector<int32_t> ids, overflow;
+  C.times.aca_phase_ms[7] = ms_since(tb);
+  std::vector<int32_t>& ids = W.h_ids;
+  std::vector<int32_t> overflow;
+  ids.clear();
+  C.times.aca_phase_ms[4] = ms_since(t0);
   double used = 0;
   for (int64_t b = 0; b <= nb; ++b) {
     double need = 0;
@@ -617,6 +662,7 @@ void setup_aca(Context& C) {
     }
     if (!none.empty()) fail(HM_ERR_CUDA, "ACA overflow re-run did not converge within k_max");
   }
+  const auto t5 = clk::now();
   C.h_rank.resize(nb);
   C.h_foff.resize(nb);
   HM_CUDA(cudaMemcpyAsync(C.h_rank.data(), C.frank.get(), nb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -627,6 +673,7 @@ void setup_aca(Context& C) {
   HM_CUDA(cudaStreamSynchronize(st));
   C.evals_aca = (double)hev;
   C.factor_doubles = (int64_t)(C.fpool.used / sizeof(double));
+  C.times.aca_phase_ms[5] = ms_since(t5);
 }
 
 }  // namespace hm

@@ -296,6 +296,13 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
     else if (k == "aca_kws") { if (v < 1 || v > 64) bad(); C.aca_kws = v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
+    else if (k == "mv_kernel") { if (v != 0 && v != 1 && v != 2 && v != 3) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
+    else if (k == "mv_profile") {
+      if (v != 0 && v != 1) bad();
+      if (v == 1) { C.mv_prof.alloc(4); HM_CUDA(cudaMemsetAsync(C.mv_prof.get(), 0, 32, C.stream)); }
+      else C.mv_prof.release();
+    }
+    else if (k == "mv_scramble") { if (v != 0 && v != 1) bad(); C.mv_scramble = (int)v; }
     else if (k == "kernel_timing") {
       if (v != 0 && v != 1) bad();
       HM_CUDA(cudaStreamSynchronize(C.stream));
@@ -319,6 +326,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "aca_kws") *v = C.aca_kws;
     else if (k == "record_pivots") *v = C.record_pivots;
     else if (k == "kernel_timing") *v = C.kt.on ? 1 : 0;
+    else if (k == "mv_kernel") *v = C.mv_kind;
     else hm::fail(HM_ERR_ARG, "hm_get_option: unknown key '" + k + "'");
   });
 }
@@ -555,12 +563,24 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
       << ",\"aca_overflow\":" << C.aca_overflow << ",\"tree_ms\":" << C.times.tree_ms << ",\"tree_phase_ms\":[" << C.times.tree_phase_ms[0] << ","
       << C.times.tree_phase_ms[1] << "," << C.times.tree_phase_ms[2] << "," << C.times.tree_phase_ms[3] << ","
       << C.times.tree_phase_ms[4] << "," << C.times.tree_phase_ms[5] << "]"
+      << ",\"plan_phase_ms\":[" << C.times.plan_phase_ms[0] << "," << C.times.plan_phase_ms[1] << ","
+      << C.times.plan_phase_ms[2] << "]"
+      << ",\"aca_phase_ms\":[" << C.times.aca_phase_ms[0] << "," << C.times.aca_phase_ms[1] << ","
+      << C.times.aca_phase_ms[2] << "," << C.times.aca_phase_ms[3] << "," << C.times.aca_phase_ms[4] << ","
+      << C.times.aca_phase_ms[5] << "," << C.times.aca_phase_ms[6] << "," << C.times.aca_phase_ms[7] << ","
+      << C.times.aca_phase_ms[8] << "]"
       << ",\"near_ms\":" << C.times.near_ms << ",\"aca_ms\":" << C.times.aca_ms << ",\"plan_ms\":" << C.times.plan_ms
       << ",\"setup_ms\":" << C.times.setup_ms << ",\"solve_ms\":" << C.times.solve_ms
       << ",\"solve_iters\":" << C.times.solve_iters << ",\"solve_relres\":" << C.times.solve_relres
-      << ",\"launches\":" << hm::g_launches << ",\"mv_batches\":" << C.mv_nbatches << ",\"lr_small\":" << C.n_lr_small << ",\"lr_large\":" << C.n_lr_large << ",\"rank_hist\":[";
+      << ",\"launches\":" << hm::g_launches << ",\"mv_batches\":" << C.mv_nbatches << ",\"mv_segs\":" << C.mv_nsegs << ",\"lr_small\":" << C.n_lr_small << ",\"lr_large\":" << C.n_lr_large << ",\"rank_hist\":[";
     for (int k = 0; k <= 64; ++k) o << (k ? "," : "") << hist[k];
-    o << "],\"kt\":{\"on\":" << (C.kt.on ? 1 : 0);
+    o << "]";
+    if (C.mv_prof.n) {
+      unsigned long long pr[4] = {0, 0, 0, 0};
+      HM_CUDA(cudaMemcpy(pr, C.mv_prof.get(), sizeof(pr), cudaMemcpyDeviceToHost));
+      o << ",\"mv_prof_cycles\":[" << pr[0] << "," << pr[1] << "," << pr[2] << "]";
+    }
+    o << ",\"kt\":{\"on\":" << (C.kt.on ? 1 : 0);
     const char* fam[hm::KF_NUM] = {"eval_near", "eval_aca", "aca_other", "matvec"};
     for (int f = 0; f < hm::KF_NUM; ++f)
       o << ",\"" << fam[f] << "_ms\":" << C.kt.ms[f] << ",\"" << fam[f] << "_n\":" << C.kt.n[f];

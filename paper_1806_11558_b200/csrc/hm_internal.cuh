@@ -146,12 +146,16 @@ struct TreeWs {
   DBuf<char> tmp;
 };
 struct EntryBatchWork;   // entry_batch.cuh
+struct PlanWs;           // matvec.cu
 struct AcaWork;          // aca.cu
 
 // Timers ----------------------------------------------------------------------------------
 struct PhaseTimes {
   double tree_ms = 0, near_ms = 0, aca_ms = 0, plan_ms = 0, setup_ms = 0;
   double tree_phase_ms[6] = {0, 0, 0, 0, 0, 0};   // geometry, morton+sort, cluster, block, leafsort, partition
+  double plan_phase_ms[3] = {0, 0, 0};              // items, batches, upload (host)
+  double aca_phase_ms[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // chunk prep, step loop, of which in sync, store, pre, post,
+                                                        // pre up to the budget, budget, pre up to the VA reserve (host)
   double last_matvec_ms = 0, solve_ms = 0;
   int solve_iters = 0;
   double solve_relres = 0;
@@ -231,7 +235,10 @@ struct Context {
   DBuf<MvTileU> mv_tiles_u;
   DBuf<double> mv_tbuf;
   int mv_grid = 0;
-  int64_t mv_nbatches = 0, mv_tlen = 0;
+  DBuf<unsigned long long> mv_prof;   // option "mv_profile": [producer empty-wait, consumer full-wait, consumer work] cycles
+  int mv_scramble = 0;         // diagnostic option "mv_scramble" (wrong results): see k_mv_batched
+  int mv_kind = 1;             // option "mv_kernel": 1 CTA ring 4 x 48 KiB (default), 2 / 3 CTA ring 8 x 24 / 6 x 32 KiB, 0 warp rings
+  int64_t mv_nbatches = 0, mv_tlen = 0, mv_nsegs = 0;
   int64_t n_lr_small = 0, n_lr_large = 0;
 
   // work vectors (internal order)
@@ -246,6 +253,7 @@ struct Context {
   DBuf<char> near_tmp;
   std::shared_ptr<EntryBatchWork> near_ws;
   std::shared_ptr<AcaWork> aca_ws;
+  std::shared_ptr<PlanWs> plan_ws;
   int64_t mv_n_large = 0, mv_n_dense_big = 0, mv_n_tiles_v = 0, mv_n_tiles_u = 0;
 
   PhaseTimes times;

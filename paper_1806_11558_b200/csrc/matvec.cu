@@ -20,15 +20,24 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <thread>
 
 #include "entry.cuh"
 
 namespace hm {
 
-constexpr int kMvStages = 4;
+constexpr int kMvStages = 4;              // k_mv_batched (CTA ring): 4 x 48 KiB stages
 constexpr int kMvStageBytes = 48 * 1024;
 constexpr int kMvThreads = 512;
+constexpr int kWrWarps = 8;               // k_mv_warps (warp rings): 8 warps x 2 x 13 KiB stages
+constexpr int kWrStages = 2;
+constexpr int kWrStageBytes = 13 * 1024;
 constexpr int kMvSmallMax = 16 * 1024;
+constexpr int kMaxX = 12;         // x_sigma ranges (bulk copies) per batch
+constexpr int64_t kXGap = 64;     // doubles: merge x ranges closer than this
 
 namespace {
 
@@ -109,9 +118,42 @@ __device__ __forceinline__ void dense_any(const double* B, int m, int n, const d
   else dense_block<8, 4>(B, m, n, xs, y, lane);
 }
 
+// Warp sum of KB per-lane values (KB = 8 or 16) by recursive halving (KB - 1 shuffles + the
+// last levels), then every lane gets all KB totals back (KB shuffles): 2 KB + 1 shuffles
+// instead of 5 KB for KB independent butterflies.
+template <int KB>
+__device__ __forceinline__ void warp_allreduce_vec(double (&a)[KB], int lane) {
+  constexpr int LV = KB == 16 ? 4 : 3;           // halving levels: offsets 16, 8, (4, (2))
+  double v[KB];
+#pragma unroll
+  for (int i = 0; i < KB; ++i) v[i] = a[i];
+#pragma unroll
+  for (int lvl = 0; lvl < LV; ++lvl) {
+    const int o = 16 >> lvl, half = (KB >> 1) >> lvl;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < KB / 2; ++i)
+      if (i < half) {
+        const double send = up ? v[i] : v[i + half];
+        const double keep = up ? v[i + half] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+  }
+#pragma unroll
+  for (int o = 16 >> LV; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  // lane L now holds the total of index sum_j bit(L, 4 - j) << (LV - 1 - j)
+#pragma unroll
+  for (int l = 0; l < KB; ++l) {
+    int src = 0;
+#pragma unroll
+    for (int j = 0; j < LV; ++j) src |= ((l >> (LV - 1 - j)) & 1) << (4 - j);
+    a[l] = __shfl_sync(0xffffffffu, v[0], src);
+  }
+}
+
 // Low-rank block U (m x k) | V (n x k), column-major, columns [l0, l0 + kc) (kc <= KB), out of
-// shared memory: t = V^T x with all kc column sums in registers, one butterfly over the kc
-// sums at once, then y += U t (one FP64 atomic per row).
+// shared memory: t = V^T x with all kc column sums in registers, one vector all-reduce over
+// the warp, then y += U t (one FP64 atomic per row).
 template <int KB>
 __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int m, int n, int k, int l0, int kc,
                                               const double* __restrict__ xs, double* __restrict__ y, int lane) {
@@ -126,10 +168,7 @@ __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int
     for (int l = 0; l < KB; ++l)
       if (l < kc) acc[l] = __fma_rn(V[j + l * n], xj, acc[l]);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int l = 0; l < KB; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], o);
+  warp_allreduce_vec<KB>(acc, lane);
   for (int t = lane; t < m; t += 32) {
     double s = 0.0;
 #pragma unroll
@@ -153,46 +192,98 @@ __device__ __forceinline__ void lowrank_any(const double* U, int m, int n, int k
 // flipped.  Warps 1..NW-1 consume every stage entirely out of shared memory (tasks
 // round-robin) — no global load on the consumer side, only fire-and-forget atomics into
 // the L2-resident y — then arrive on the stage's "empty" barrier.
+// A sequence of 16-byte records read through two 32-record register windows (one record per
+// lane): record i is available for w0 <= i < w0 + 64; advancing past a window issues the load
+// of the window after next, 32 records ahead of use.  Warp-collective.
+struct RecWindow {
+  const int4* src;
+  int64_t w0, end;
+  int4 cur, nxt;
+  __device__ __forceinline__ int4 load(int64_t i) const { return i < end ? __ldg(src + i) : make_int4(0, 0, 0, 0); }
+  __device__ __forceinline__ void init(const int4* p, int64_t begin, int64_t e, int lane) {
+    src = p; w0 = begin; end = e;
+    cur = load(w0 + lane);
+    nxt = load(w0 + 32 + lane);
+  }
+  __device__ __forceinline__ void advance_to(int64_t i, int lane) {
+    while (i >= w0 + 32) { cur = nxt; w0 += 32; nxt = load(w0 + 32 + lane); }
+  }
+  __device__ __forceinline__ int4 get(int64_t i, int lane) const {
+    const int64_t d = i - w0;
+    const int sl = (int)(d & 31);
+    int4 a, b;
+    a.x = __shfl_sync(0xffffffffu, cur.x, sl); a.y = __shfl_sync(0xffffffffu, cur.y, sl);
+    a.z = __shfl_sync(0xffffffffu, cur.z, sl); a.w = __shfl_sync(0xffffffffu, cur.w, sl);
+    b.x = __shfl_sync(0xffffffffu, nxt.x, sl); b.y = __shfl_sync(0xffffffffu, nxt.y, sl);
+    b.z = __shfl_sync(0xffffffffu, nxt.z, sl); b.w = __shfl_sync(0xffffffffu, nxt.w, sl);
+    return d < 32 ? a : b;
+  }
+};
+
+template <int STAGES, int SBYTES>
 __global__ void __launch_bounds__(kMvThreads, 1)
-    k_mv_batched(const MvBatch* __restrict__ batches, const MvSeg* __restrict__ segs, const int32_t* __restrict__ cta_first,
+    k_mv_batched(const MvBatch* __restrict__ batches, const MvSeg* __restrict__ segs, int64_t nsegs_total,
+                 const int32_t* __restrict__ cta_first,
                  const char* __restrict__ base0, const char* __restrict__ base1, const char* __restrict__ base2,
-                 const double* __restrict__ x, double* __restrict__ y) {
+                 const double* __restrict__ x, double* __restrict__ y, int64_t scramble_n,
+                 unsigned long long* __restrict__ prof) {
   constexpr int NW = kMvThreads / 32, NC = NW - 1;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + kMvStages;
-  unsigned char* buf = smem + 128;
+  uint64_t* empty = full + STAGES;
+  unsigned char* buf = smem + 256;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = cta_first[blockIdx.x], nb = cta_first[blockIdx.x + 1] - b0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kMvStages; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  long long pw_empty = 0;
   if (warp == 0) {
+    // batch and segment descriptors stream through register windows 32-64 records ahead, so
+    // no descriptor read sits on the producer's critical path
+    RecWindow wb, ws;
+    wb.init(reinterpret_cast<const int4*>(batches), b0, b0 + nb, lane);
+    bool ws_ready = false;
     for (int it = 0; it < nb; ++it) {
-      const int stage = it % kMvStages;
-      if (it >= kMvStages) mbar_wait(&empty[stage], (unsigned)(((it / kMvStages) - 1) & 1));
-      const MvBatch B = batches[b0 + it];
-      if (lane == 0) mbar_expect_tx(&full[stage], (unsigned)B.bytes);
+      const int stage = it % STAGES;
+      wb.advance_to(b0 + it, lane);
+      const int4 Bv = wb.get(b0 + it, lane);
+      const int first_seg = Bv.x, nseg = Bv.y, bytes = Bv.z;
+      if (!ws_ready) { ws.init(reinterpret_cast<const int4*>(segs), first_seg, nsegs_total, lane); ws_ready = true; }
+      const long long tw0 = prof ? clock64() : 0;
+      if (it >= STAGES) mbar_wait(&empty[stage], (unsigned)(((it / STAGES) - 1) & 1));
+      if (prof && lane == 0) pw_empty += clock64() - tw0;
+      if (lane == 0) mbar_expect_tx(&full[stage], (unsigned)bytes);
       __syncwarp();
-      unsigned char* sb = buf + stage * kMvStageBytes;
-      for (int s = lane; s < B.nseg; s += 32) {
-        const MvSeg S = segs[B.first_seg + s];
-        const char* base = S.base == 0 ? base0 : S.base == 1 ? base1 : S.base == 2 ? base2
-                                                                     : reinterpret_cast<const char*>(x);
-        bulk_g2s(sb + S.dst, base + S.src, (unsigned)S.bytes, &full[stage]);
+      unsigned char* sb = buf + stage * SBYTES;
+      for (int s0 = 0; s0 < nseg; s0 += 32) {
+        ws.advance_to(first_seg + s0, lane);
+        const int4 Sv = ws.get(first_seg + s0 + lane, lane);
+        if (s0 + lane < nseg) {
+          const int64_t src = (int64_t)(((uint64_t)(uint32_t)Sv.y << 32) | (uint32_t)Sv.x);
+          const unsigned sbytes = (uint32_t)Sv.z & 0xffffu, dst = (uint32_t)Sv.z >> 16, sbase = (uint32_t)Sv.w & 0xffffu;
+          const char* base = sbase == 0 ? base0 : sbase == 1 ? base1 : sbase == 2 ? base2
+                                                                 : reinterpret_cast<const char*>(x);
+          bulk_g2s(sb + dst, base + src, sbytes, &full[stage]);
+        }
       }
     }
+    if (prof && lane == 0) atomicAdd(&prof[0], (unsigned long long)pw_empty);
     return;
   }
+  long long cw_full = 0, cw_work = 0;
   for (int it = 0; it < nb; ++it) {
-    const int stage = it % kMvStages;
-    mbar_wait(&full[stage], (unsigned)((it / kMvStages) & 1));
-    const unsigned char* sb = buf + stage * kMvStageBytes;
+    const int stage = it % STAGES;
+    const long long t0 = prof ? clock64() : 0;
+    mbar_wait(&full[stage], (unsigned)((it / STAGES) & 1));
+    const long long t1 = prof ? clock64() : 0;
+    cw_full += t1 - t0;
+    const unsigned char* sb = buf + stage * SBYTES;
     const double* sd = reinterpret_cast<const double*>(sb);
     const int4* rec = reinterpret_cast<const int4*>(sb);
     const int count = rec[0].x;
@@ -200,11 +291,81 @@ __global__ void __launch_bounds__(kMvThreads, 1)
       const int4 T = rec[1 + t];
       const uint32_t mnk = (uint32_t)T.w;
       const int m = mnk & 2047, n = (mnk >> 11) & 2047, k = mnk >> 22;
+      // scramble_n > 0: diagnostic only (wrong result) — task row bases spread over y, to
+      // measure same-address atomic contention
+      const int64_t r0 = scramble_n > 0 ? ((int64_t)T.x * 2654435761ll) % scramble_n : T.x;
+      if (k == 0) dense_any(sd + T.z, m, n, sd + T.y, y + r0, lane);
+      else lowrank_any(sd + T.z, m, n, k, sd + T.y, y + r0, lane);
+    }
+    __syncwarp();
+    if (prof) cw_work += clock64() - t1;
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[stage])) : "memory");
+  }
+  if (prof && lane == 0) {
+    atomicAdd(&prof[1], (unsigned long long)cw_full);
+    atomicAdd(&prof[2], (unsigned long long)cw_work);
+  }
+}
+
+// Warp rings: every warp streams its own contiguous, byte-balanced range of batches through
+// its own kWrStages shared-memory stages — it issues the bulk copies of batch it + kWrStages
+// itself right after it has consumed batch it (32 lanes in parallel), so a slow task delays
+// only its own warp's stream and no stage waits for the slowest of many consumers.
+__global__ void __launch_bounds__(kWrWarps * 32, 1)
+    k_mv_warps(const MvBatch* __restrict__ batches, const MvSeg* __restrict__ segs, const int32_t* __restrict__ warp_first,
+               const char* __restrict__ base0, const char* __restrict__ base1, const char* __restrict__ base2,
+               const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem) + warp * kWrStages;
+  unsigned char* buf = smem + 256 + (size_t)warp * kWrStages * kWrStageBytes;
+  const int gw = blockIdx.x * kWrWarps + warp;
+  const int b0 = warp_first[gw], nb = warp_first[gw + 1] - b0;
+  if (lane == 0) {
+    for (int s = 0; s < kWrStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // descriptors of the next batch to issue (and the lane's first segment of it) are loaded one
+  // batch ahead, off the critical path
+  MvBatch next = nb > 0 ? batches[b0] : MvBatch{0, 0, 0, 0};
+  MvSeg nseg0 = (nb > 0 && lane < next.nseg) ? segs[next.first_seg + lane] : MvSeg{0, 0, 0, 0, 0};
+  auto issue = [&](int it) {
+    const MvBatch B = next;
+    const MvSeg S0 = nseg0;
+    if (it + 1 < nb) {
+      next = batches[b0 + it + 1];
+      nseg0 = lane < next.nseg ? segs[next.first_seg + lane] : MvSeg{0, 0, 0, 0, 0};
+    }
+    const int st = it % kWrStages;
+    if (lane == 0) mbar_expect_tx(&full[st], (unsigned)B.bytes);
+    __syncwarp();
+    unsigned char* sb = buf + st * kWrStageBytes;
+    for (int s = lane; s < B.nseg; s += 32) {
+      const MvSeg S = s == lane ? S0 : segs[B.first_seg + s];
+      const char* base = S.base == 0 ? base0 : S.base == 1 ? base1 : S.base == 2 ? base2
+                                                             : reinterpret_cast<const char*>(x);
+      bulk_g2s(sb + S.dst, base + S.src, (unsigned)S.bytes, &full[st]);
+    }
+  };
+  for (int it = 0; it < kWrStages && it < nb; ++it) issue(it);
+  for (int it = 0; it < nb; ++it) {
+    const int st = it % kWrStages;
+    mbar_wait(&full[st], (unsigned)((it / kWrStages) & 1));
+    const unsigned char* sb = buf + st * kWrStageBytes;
+    const double* sd = reinterpret_cast<const double*>(sb);
+    const int4* rec = reinterpret_cast<const int4*>(sb);
+    const int count = rec[0].x;
+    for (int t = 0; t < count; ++t) {
+      const int4 T = rec[1 + t];
+      const uint32_t mnk = (uint32_t)T.w;
+      const int m = mnk & 2047, n = (mnk >> 11) & 2047, k = mnk >> 22;
       if (k == 0) dense_any(sd + T.z, m, n, sd + T.y, y + T.x, lane);
       else lowrank_any(sd + T.z, m, n, k, sd + T.y, y + T.x, lane);
     }
     __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[stage])) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads before the async refill
+    if (it + kWrStages < nb) issue(it + kWrStages);
   }
 }
 
@@ -299,174 +460,304 @@ __global__ void k_mv_dense_direct(const MvLarge* __restrict__ L, int64_t nl, con
 
 }  // namespace
 
-void plan_matvec(Context& C) {
-  cudaStream_t st = C.stream;
-  const int64_t nd = C.dense_end - C.dense_begin, na = C.adm_end - C.adm_begin;
-  std::vector<int64_t> hoff(nd + 1);
-  HM_CUDA(cudaMemcpyAsync(hoff.data(), C.doff.get(), (nd + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  if (C.h_dense.size() != (size_t)C.ndense) {
-    C.h_dense.resize(C.ndense);
-    HM_CUDA(cudaMemcpyAsync(C.h_dense.data(), C.dense.get(), C.ndense * sizeof(Quad), cudaMemcpyDeviceToHost, st));
-  }
-  HM_CUDA(cudaStreamSynchronize(st));
-  struct Item { int64_t byte0, bytes; int base; int32_t rlo, clo, n; uint32_t mnk; };
-  std::vector<Item> items;
-  items.reserve(nd + na);
-  std::vector<MvLarge> dense_big, large;
-  for (int64_t b = 0; b < nd; ++b) {
-    const Quad& q = C.h_dense[C.dense_begin + b];
-    const int m = q.rhi - q.rlo, n = q.chi - q.clo;
-    const int64_t bytes = 8 * (int64_t)m * n;
-    if (bytes + 8 * n + 64 > kMvStageBytes || m > 2047 || n > 2047) {
-      dense_big.push_back(MvLarge{q.rlo, q.clo, m, n, 0, 0, hoff[b], 0});
-      continue;
+// ---- plan (host) ----------------------------------------------------------------------------
+// Grow-only pinned host buffer: page-faulted and registered once, reused by every hm_setup,
+// and a true DMA source for the plan upload.
+template <class T>
+struct PinnedVec {
+  T* p = nullptr;
+  size_t n = 0, cap = 0;
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  PinnedVec& operator=(const PinnedVec&) = delete;
+  ~PinnedVec() { if (p) cudaFreeHost(p); }
+  void resize(size_t m) {
+    if (m > cap) {
+      const size_t c = std::max(m, cap + cap / 2);
+      T* q = nullptr;
+      HM_CUDA(cudaHostAlloc(&q, c * sizeof(T) + 16, cudaHostAllocDefault));
+      if (p) { std::memcpy(q, p, n * sizeof(T)); cudaFreeHost(p); }
+      p = q;
+      cap = c;
     }
-    items.push_back(Item{8 * hoff[b], bytes, 0, q.rlo, q.clo, n, (uint32_t)m | ((uint32_t)n << 11)});
+    n = m;
   }
-  std::vector<int64_t> lr_order;
-  for (int64_t b = 0; b < na; ++b)
-    if (C.h_rank[b] > 0) lr_order.push_back(b);
-  if (!std::is_sorted(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; }))
-    std::sort(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; });
-  int64_t tl = 0;
-  for (int64_t b : lr_order) {
-    const Quad& q = C.h_adm[C.adm_begin + b];
-    const int m = q.rhi - q.rlo, n = q.chi - q.clo, k = C.h_rank[b];
-    const int64_t bytes = 8 * (int64_t)k * (m + n);
-    if (bytes <= kMvSmallMax && m <= 2047 && n <= 2047 && k <= 1023) {
-      items.push_back(Item{8 * C.h_foff[b], bytes, 1, q.rlo, q.clo, n,
-                           (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)});
-    } else {
-      large.push_back(MvLarge{q.rlo, q.clo, m, n, k, 0, C.h_foff[b], tl});
-      tl += k;
-    }
-  }
-  // Batches: consecutive items filling one stage = [header + task records | x_sigma ranges |
-  // storage runs].  x ranges are 16-B aligned supersets [clo & ~1, (clo + n + 1) & ~1) in
-  // doubles, shared by the leaves of a batch with the same sigma; storage runs are maximal
-  // runs of contiguous items (16-B aligned supersets), one bulk copy each.
+  T* data() { return p; }
+  size_t size() const { return n; }
+  T& operator[](size_t i) { return p[i]; }
+};
+
+namespace {
+struct Item { int64_t byte0, bytes; int base; int32_t rlo, clo, n; uint32_t mnk; };
+// one planner thread's output over a contiguous slice of the item sequence
+struct PlanPart {
   std::vector<MvBatch> batches;
   std::vector<MvSeg> segs;
-  std::vector<MvTask> stream;     // per batch: header {count,0,0,0} + count task records
-  stream.reserve(items.size() + items.size() / 4 + 16);
+  std::vector<MvTask> stream;
+  std::vector<MvLarge> dense_big, large;
+  std::vector<Item> items;
   struct XR { int64_t a0, a1; };
   struct Run { int base; int64_t a0, a1, end; };
   std::vector<XR> xr;
   std::vector<Run> runs;
   std::vector<int> item_x, item_run;
-  for (size_t i = 0; i < items.size();) {
-    xr.clear(); runs.clear(); item_x.clear(); item_run.clear();
-    int64_t xb = 0, db = 0;
-    size_t j = i;
-    for (; j < items.size(); ++j) {
-      const Item& it = items[j];
-      const int64_t xa0 = it.clo & ~int64_t(1), xa1 = (it.clo + it.n + 1) & ~int64_t(1);
-      int xi = -1;
-      for (int r = (int)xr.size() - 1; r >= 0 && r >= (int)xr.size() - 8; --r)
-        if (xr[r].a0 <= xa0 && xa1 <= xr[r].a1) { xi = r; break; }
-      const int64_t xcost = xi >= 0 ? 0 : 8 * (xa1 - xa0);
-      const bool ext = !runs.empty() && runs.back().base == it.base && runs.back().end == it.byte0;
-      const int64_t ra0 = ext ? runs.back().a0 : (it.byte0 & ~int64_t(15));
-      const int64_t ra1 = (it.byte0 + it.bytes + 15) & ~int64_t(15);
-      const int64_t dcost = ext ? ra1 - runs.back().a1 : ra1 - ra0;
-      const int64_t hb = 16 * (int64_t)(item_x.size() + 2);
-      if (hb + xb + xcost + db + dcost > kMvStageBytes) break;
-      if (xi < 0) { xr.push_back(XR{xa0, xa1}); xi = (int)xr.size() - 1; }
-      xb += xcost;
-      if (ext) { runs.back().a1 = ra1; runs.back().end = it.byte0 + it.bytes; }
-      else runs.push_back(Run{it.base, ra0, ra1, it.byte0 + it.bytes});
-      db += dcost;
-      item_x.push_back(xi);
-      item_run.push_back((int)runs.size() - 1);
-    }
-    if (j == i) fail(HM_ERR_CUDA, "matvec plan: leaf larger than a pipeline stage");
-    const int count = (int)(j - i);
-    MvBatch B{};
-    B.first_seg = (int32_t)segs.size();
-    B.count = count;
-    // layout
-    const int64_t hbytes = 16 * (int64_t)(count + 1);
-    std::vector<int64_t> xoff(xr.size()), roff(runs.size());
-    int64_t off = hbytes;
-    for (size_t r = 0; r < xr.size(); ++r) { xoff[r] = off; off += 8 * (xr[r].a1 - xr[r].a0); }
-    for (size_t r = 0; r < runs.size(); ++r) { roff[r] = off; off += runs[r].a1 - runs[r].a0; }
-    B.bytes = (int32_t)off;
-    segs.push_back(MvSeg{16 * (int64_t)stream.size(), (uint16_t)hbytes, 0, 2, 0});
-    for (size_t r = 0; r < xr.size(); ++r)
-      segs.push_back(MvSeg{8 * xr[r].a0, (uint16_t)(8 * (xr[r].a1 - xr[r].a0)), (uint16_t)xoff[r], 3, 0});
-    for (size_t r = 0; r < runs.size(); ++r)
-      segs.push_back(MvSeg{runs[r].a0, (uint16_t)(runs[r].a1 - runs[r].a0), (uint16_t)roff[r], (uint16_t)runs[r].base, 0});
-    B.nseg = (int32_t)segs.size() - B.first_seg;
-    stream.push_back(MvTask{count, 0, 0, 0});
-    for (int c = 0; c < count; ++c) {
-      const Item& it = items[i + c];
-      const XR& X = xr[item_x[c]];
-      const Run& R = runs[item_run[c]];
-      MvTask t;
-      t.rlo = it.rlo;
-      t.xoff = (int32_t)((xoff[item_x[c]] + 8 * (it.clo - X.a0)) / 8);
-      t.loff = (int32_t)((roff[item_run[c]] + (it.byte0 - R.a0)) / 8);
-      t.mnk = it.mnk;
-      stream.push_back(t);
-    }
-    batches.push_back(B);
-    i = j;
+  std::vector<int64_t> xoff, roff;
+  void clear() {
+    batches.clear(); segs.clear(); stream.clear(); dense_big.clear(); large.clear(); items.clear();
   }
-  // byte-balanced contiguous batch ranges, one persistent CTA per SM
+  // Batches over items[0, n): consecutive items filling one stage = [header + task records |
+  // x_sigma ranges | storage runs].  x ranges are 16-B aligned supersets [clo & ~1,
+  // (clo + n + 1) & ~1) in doubles, shared by the leaves of a batch with the same sigma;
+  // storage runs are maximal runs of contiguous items (16-B aligned supersets), one bulk copy
+  // each.  Stream offsets (base 2) are local to the part and shifted when parts are joined.
+  void batch(int64_t cap) {
+    for (size_t i = 0; i < items.size();) {
+      xr.clear(); runs.clear(); item_x.clear(); item_run.clear();
+      int64_t xb = 0, db = 0;
+      size_t j = i;
+      for (; j < items.size(); ++j) {
+        const Item& it = items[j];
+        const int64_t xa0 = it.clo & ~int64_t(1), xa1 = (it.clo + it.n + 1) & ~int64_t(1);
+        // x_sigma: reuse / widen a staged range within kXGap doubles, else a new range (a
+        // batch holds at most kMaxX ranges: more small bulk copies per stage cost bandwidth,
+        // tools/tma_stream_bench.cu)
+        int xi = -1;
+        int64_t xcost = 8 * (xa1 - xa0);
+        for (int r = (int)xr.size() - 1; r >= 0; --r)
+          if (xa0 <= xr[r].a1 + kXGap && xr[r].a0 <= xa1 + kXGap) {
+            const int64_t c = 8 * ((std::max(xr[r].a1, xa1) - std::min(xr[r].a0, xa0)) - (xr[r].a1 - xr[r].a0));
+            if (xi < 0 || c < xcost) { xi = r; xcost = c; }
+          }
+        if (xi < 0 && (int)xr.size() >= kMaxX) break;
+        const bool ext = !runs.empty() && runs.back().base == it.base && runs.back().end == it.byte0;
+        const int64_t ra0 = ext ? runs.back().a0 : (it.byte0 & ~int64_t(15));
+        const int64_t ra1 = (it.byte0 + it.bytes + 15) & ~int64_t(15);
+        const int64_t dcost = ext ? ra1 - runs.back().a1 : ra1 - ra0;
+        const int64_t hb = 16 * (int64_t)(item_x.size() + 2);
+        if (hb + xb + xcost + db + dcost > cap) break;
+        if (xi < 0) { xr.push_back(XR{xa0, xa1}); xi = (int)xr.size() - 1; }
+        else { xr[xi].a0 = std::min(xr[xi].a0, xa0); xr[xi].a1 = std::max(xr[xi].a1, xa1); }
+        xb += xcost;
+        if (ext) { runs.back().a1 = ra1; runs.back().end = it.byte0 + it.bytes; }
+        else runs.push_back(Run{it.base, ra0, ra1, it.byte0 + it.bytes});
+        db += dcost;
+        item_x.push_back(xi);
+        item_run.push_back((int)runs.size() - 1);
+      }
+      if (j == i) fail(HM_ERR_CUDA, "matvec plan: leaf larger than a pipeline stage");
+      const int count = (int)(j - i);
+      MvBatch B{};
+      B.first_seg = (int32_t)segs.size();
+      B.count = count;
+      const int64_t hbytes = 16 * (int64_t)(count + 1);
+      xoff.resize(xr.size());
+      roff.resize(runs.size());
+      int64_t off = hbytes;
+      for (size_t r = 0; r < xr.size(); ++r) { xoff[r] = off; off += 8 * (xr[r].a1 - xr[r].a0); }
+      for (size_t r = 0; r < runs.size(); ++r) { roff[r] = off; off += runs[r].a1 - runs[r].a0; }
+      B.bytes = (int32_t)off;
+      segs.push_back(MvSeg{16 * (int64_t)stream.size(), (uint16_t)hbytes, 0, 2, 0});
+      for (size_t r = 0; r < xr.size(); ++r)
+        segs.push_back(MvSeg{8 * xr[r].a0, (uint16_t)(8 * (xr[r].a1 - xr[r].a0)), (uint16_t)xoff[r], 3, 0});
+      for (size_t r = 0; r < runs.size(); ++r)
+        segs.push_back(MvSeg{runs[r].a0, (uint16_t)(runs[r].a1 - runs[r].a0), (uint16_t)roff[r], (uint16_t)runs[r].base, 0});
+      B.nseg = (int32_t)segs.size() - B.first_seg;
+      stream.push_back(MvTask{count, 0, 0, 0});
+      for (int c = 0; c < count; ++c) {
+        const Item& it = items[i + c];
+        const XR& X = xr[item_x[c]];
+        const Run& R = runs[item_run[c]];
+        MvTask t;
+        t.rlo = it.rlo;
+        t.xoff = (int32_t)((xoff[item_x[c]] + 8 * (it.clo - X.a0)) / 8);
+        t.loff = (int32_t)((roff[item_run[c]] + (it.byte0 - R.a0)) / 8);
+        t.mnk = it.mnk;
+        stream.push_back(t);
+      }
+      batches.push_back(B);
+      i = j;
+    }
+  }
+};
+}  // namespace
+
+struct PlanWs {
+  std::vector<int64_t> hoff, lr_order;
+  std::vector<PlanPart> parts;
+  PinnedVec<MvBatch> batches;
+  PinnedVec<MvSeg> segs;
+  PinnedVec<MvTask> stream;
+  PinnedVec<MvLarge> large, dense_big;
+  PinnedVec<MvTileV> tv;
+  PinnedVec<MvTileU> tu;
+  PinnedVec<int32_t> cta;
+};
+
+// The matvec plan, built on the host by T threads over contiguous slices of the item sequence
+// (owned dense leaves in list order, then owned low-rank leaves in factor-pool order); batches
+// never straddle two slices.
+void plan_matvec(Context& C) {
+  cudaStream_t st = C.stream;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  if (!C.plan_ws) C.plan_ws = std::make_shared<PlanWs>();
+  PlanWs& W = *C.plan_ws;
+  const int64_t nd = C.dense_end - C.dense_begin, na = C.adm_end - C.adm_begin;
+  W.hoff.resize(nd + 1);
+  HM_CUDA(cudaMemcpyAsync(W.hoff.data(), C.doff.get(), (nd + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (C.h_dense.size() != (size_t)C.ndense) {
+    C.h_dense.resize(C.ndense);
+    HM_CUDA(cudaMemcpyAsync(C.h_dense.data(), C.dense.get(), C.ndense * sizeof(Quad), cudaMemcpyDeviceToHost, st));
+  }
+  HM_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t>& lr_order = W.lr_order;
+  lr_order.clear();
+  for (int64_t b = 0; b < na; ++b)
+    if (C.h_rank[b] > 0) lr_order.push_back(b);
+  if (!std::is_sorted(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; }))
+    std::sort(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; });
+  const int64_t nlr = (int64_t)lr_order.size(), total = nd + nlr;
+  const int T = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()),
+                                                              16, total / 20000 + 1}));
+  W.parts.resize(T);
+  const int64_t* hoff = W.hoff.data();
+  const bool wr = C.mv_kind == 0;
+  const int64_t cap = wr ? kWrStageBytes : C.mv_kind == 1 ? 48 * 1024 : C.mv_kind == 2 ? 24 * 1024 : 32 * 1024;
+  auto work = [&](int t) {
+    PlanPart& P = W.parts[t];
+    P.clear();
+    const int64_t i0 = total * t / T, i1 = total * (t + 1) / T;
+    P.items.reserve(i1 - i0);
+    for (int64_t i = i0; i < i1; ++i) {
+      if (i < nd) {
+        const int64_t b = i;
+        const Quad& q = C.h_dense[C.dense_begin + b];
+        const int m = q.rhi - q.rlo, n = q.chi - q.clo;
+        const int64_t bytes = 8 * (int64_t)m * n;
+        if (bytes + 8 * n + 64 > cap || m > 2047 || n > 2047)
+          P.dense_big.push_back(MvLarge{q.rlo, q.clo, m, n, 0, 0, hoff[b], 0});
+        else
+          P.items.push_back(Item{8 * hoff[b], bytes, 0, q.rlo, q.clo, n, (uint32_t)m | ((uint32_t)n << 11)});
+      } else {
+        const int64_t b = lr_order[i - nd];
+        const Quad& q = C.h_adm[C.adm_begin + b];
+        const int m = q.rhi - q.rlo, n = q.chi - q.clo, k = C.h_rank[b];
+        const int64_t bytes = 8 * (int64_t)k * (m + n);
+        if (bytes <= std::min<int64_t>(kMvSmallMax, cap - 8 * n - 64) && m <= 2047 && n <= 2047 && k <= 1023)
+          P.items.push_back(Item{8 * C.h_foff[b], bytes, 1, q.rlo, q.clo, n,
+                                 (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)});
+        else
+          P.large.push_back(MvLarge{q.rlo, q.clo, m, n, k, 0, C.h_foff[b], 0});
+      }
+    }
+    P.batch(cap);
+  };
+  {
+    std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(T);
+    for (int t = 1; t < T; ++t)
+      th.emplace_back([&, t]() { try { work(t); } catch (...) { err[t] = std::current_exception(); } });
+    try { work(0); } catch (...) { err[0] = std::current_exception(); }
+    for (auto& x : th) x.join();
+    for (auto& e : err) if (e) std::rethrow_exception(e);
+  }
+  const auto t1 = clk::now();
+  // join the parts: shift segment indices and task-stream offsets
+  size_t nbat = 0, nseg = 0, nstr = 0, nlarge = 0, nbig = 0;
+  for (auto& P : W.parts) {
+    nbat += P.batches.size(); nseg += P.segs.size(); nstr += P.stream.size();
+    nlarge += P.large.size(); nbig += P.dense_big.size();
+  }
+  W.batches.resize(nbat); W.segs.resize(nseg); W.stream.resize(nstr); W.large.resize(nlarge); W.dense_big.resize(nbig);
+  {
+    size_t ob = 0, os = 0, ot = 0, ol = 0, od = 0;
+    int64_t tl = 0;
+    for (auto& P : W.parts) {
+      for (const MvBatch& B : P.batches) { MvBatch b = B; b.first_seg += (int32_t)os; W.batches[ob++] = b; }
+      for (const MvSeg& S : P.segs) { MvSeg g = S; if (g.base == 2) g.src += 16 * (int64_t)ot; W.segs[os++] = g; }
+      std::memcpy(W.stream.data() + ot, P.stream.data(), P.stream.size() * sizeof(MvTask));
+      ot += P.stream.size();
+      for (MvLarge L : P.large) { L.toff = tl; tl += L.k; W.large[ol++] = L; }
+      for (const MvLarge& L : P.dense_big) W.dense_big[od++] = L;
+    }
+    C.mv_tlen = tl;
+  }
+  const auto t2 = clk::now();
+  // byte-balanced contiguous batch ranges: one per persistent CTA (CTA ring) or per warp of
+  // one persistent CTA per SM (warp rings)
   int sms = 148;
   HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, C.device));
-  const int G = std::max(1, std::min<int>(sms, (int)batches.size()));
-  std::vector<int32_t> cta_first(G + 1, (int32_t)batches.size());
+  const int G = wr ? sms * kWrWarps : std::max(1, std::min<int>(sms, (int)nbat));
+  W.cta.resize(G + 1);
   {
-    double total = 0;
-    for (auto& B : batches) total += B.bytes;
+    double tot = 0;
+    for (size_t b = 0; b < nbat; ++b) tot += W.batches[b].bytes;
+    for (int g = 0; g <= G; ++g) W.cta[g] = (int32_t)nbat;
     double acc = 0;
     int g = 0;
-    cta_first[0] = 0;
-    for (size_t b = 0; b < batches.size() && g + 1 < G; ++b) {
-      while (g + 1 < G && acc >= total * (g + 1) / G) cta_first[++g] = (int32_t)b;
-      acc += batches[b].bytes;
+    W.cta[0] = 0;
+    for (size_t b = 0; b < nbat && g + 1 < G; ++b) {
+      while (g + 1 < G && acc >= tot * (g + 1) / G) W.cta[++g] = (int32_t)b;
+      acc += W.batches[b].bytes;
     }
-    while (g + 1 < G) cta_first[++g] = (int32_t)batches.size();
+    while (g + 1 < G) W.cta[++g] = (int32_t)nbat;
   }
   // tiles of the large low-rank blocks
-  std::vector<MvTileV> tv;
-  std::vector<MvTileU> tu;
-  for (size_t i = 0; i < large.size(); ++i) {
-    const MvLarge& B = large[i];
-    for (int l0 = 0; l0 < B.k; l0 += 8)
-      for (int j0 = 0; j0 < B.n; j0 += 2048) tv.push_back(MvTileV{(int32_t)i, l0, j0, std::min(B.n, j0 + 2048)});
-    const int rows = 256;
-    for (int t0 = 0; t0 < B.m; t0 += rows) tu.push_back(MvTileU{(int32_t)i, t0, std::min(B.m, t0 + rows), 0});
+  size_t ntv = 0, ntu = 0;
+  for (size_t i = 0; i < nlarge; ++i) {
+    const MvLarge& B = W.large[i];
+    ntv += (size_t)((B.k + 7) / 8) * ((B.n + 2047) / 2048);
+    ntu += (size_t)((B.m + 255) / 256);
   }
-  auto up = [&](auto& dbuf, const auto& v) {
+  W.tv.resize(ntv);
+  W.tu.resize(ntu);
+  {
+    size_t a = 0, c = 0;
+    for (size_t i = 0; i < nlarge; ++i) {
+      const MvLarge& B = W.large[i];
+      for (int l0 = 0; l0 < B.k; l0 += 8)
+        for (int j0 = 0; j0 < B.n; j0 += 2048) W.tv[a++] = MvTileV{(int32_t)i, l0, j0, std::min(B.n, j0 + 2048)};
+      for (int t0 = 0; t0 < B.m; t0 += 256) W.tu[c++] = MvTileU{(int32_t)i, t0, std::min(B.m, t0 + 256), 0};
+    }
+  }
+  auto up = [&](auto& dbuf, auto& v) {
     dbuf.alloc(v.size());
-    if (!v.empty())
+    if (v.size())
       HM_CUDA(cudaMemcpyAsync(dbuf.get(), v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, st));
   };
-  up(C.mv_batches, batches);
-  up(C.mv_segs, segs);
-  up(C.mv_tasks, stream);
-  up(C.mv_cta, cta_first);
-  up(C.mv_large, large);
-  up(C.mv_dense_big, dense_big);
-  up(C.mv_tiles_v, tv);
-  up(C.mv_tiles_u, tu);
-  C.mv_grid = G;
-  C.mv_nbatches = (int64_t)batches.size();
-  C.mv_tbuf.alloc(tl + 1);
-  C.mv_n_large = (int64_t)large.size();
-  C.mv_n_dense_big = (int64_t)dense_big.size();
-  C.mv_n_tiles_v = (int64_t)tv.size();
-  C.mv_n_tiles_u = (int64_t)tu.size();
-  C.mv_tlen = tl;
-  C.n_lr_small = (int64_t)(lr_order.size() - large.size());
-  C.n_lr_large = (int64_t)large.size();
+  up(C.mv_batches, W.batches);
+  up(C.mv_segs, W.segs);
+  up(C.mv_tasks, W.stream);
+  up(C.mv_cta, W.cta);
+  up(C.mv_large, W.large);
+  up(C.mv_dense_big, W.dense_big);
+  up(C.mv_tiles_v, W.tv);
+  up(C.mv_tiles_u, W.tu);
+  C.mv_grid = wr ? sms : G;
+  C.mv_nbatches = (int64_t)nbat;
+  C.mv_nsegs = (int64_t)nseg;
+  C.mv_tbuf.alloc(C.mv_tlen + 1);
+  C.mv_n_large = (int64_t)nlarge;
+  C.mv_n_dense_big = (int64_t)nbig;
+  C.mv_n_tiles_v = (int64_t)ntv;
+  C.mv_n_tiles_u = (int64_t)ntu;
+  C.n_lr_small = nlr - (int64_t)nlarge;
+  C.n_lr_large = (int64_t)nlarge;
   HM_CUDA(cudaStreamSynchronize(st));
+  const auto t3 = clk::now();
+  C.times.plan_phase_ms[0] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  C.times.plan_phase_ms[1] = std::chrono::duration<double, std::milli>(t2 - t1).count();
+  C.times.plan_phase_ms[2] = std::chrono::duration<double, std::milli>(t3 - t2).count();
   static bool attr = false;
   if (!attr) {
-    const int smem = 128 + kMvStages * kMvStageBytes;
-    HM_CUDA(cudaFuncSetAttribute(k_mv_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<4, 48 * 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 4 * 48 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<8, 24 * 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 8 * 24 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<6, 32 * 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 6 * 32 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_warps, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + kWrWarps * kWrStages * kWrStageBytes));
     attr = true;
   }
 }
@@ -496,10 +787,23 @@ void matvec_internal(Context& C, const double* x_int, double* y_int) {
   if (C.mv_tlen) HM_CUDA(cudaMemsetAsync(C.mv_tbuf.get(), 0, C.mv_tlen * sizeof(double), st));
   const double* pool = (const double*)C.fpool.base;
   if (C.mv_nbatches) {
-    const int smem = 128 + kMvStages * kMvStageBytes;
-    k_mv_batched<<<C.mv_grid, kMvThreads, smem, st>>>(C.mv_batches.get(), C.mv_segs.get(), C.mv_cta.get(),
-                                                       (const char*)C.dstore.get(), (const char*)pool,
-                                                       (const char*)C.mv_tasks.get(), x_int, y_int);
+    if (C.mv_kind == 0) {
+      k_mv_warps<<<C.mv_grid, kWrWarps * 32, 256 + kWrWarps * kWrStages * kWrStageBytes, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int);
+    } else if (C.mv_kind == 1) {
+      k_mv_batched<4, 48 * 1024><<<C.mv_grid, kMvThreads, 256 + 4 * 48 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
+    } else if (C.mv_kind == 2) {
+      k_mv_batched<8, 24 * 1024><<<C.mv_grid, kMvThreads, 256 + 8 * 24 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
+    } else {
+      k_mv_batched<6, 32 * 1024><<<C.mv_grid, kMvThreads, 256 + 6 * 32 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
+    }
     HM_CHECK_LAUNCH();
   }
   if (C.mv_n_dense_big) {

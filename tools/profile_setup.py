@@ -10,7 +10,10 @@ nmv = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 V, T = config_mesh(cfg)
 H = HMatrix(device=0)
 H.build_tree(V, T, 32, 1.0)
-H.setup(1e-6)
+if os.environ.get("HM_KT"):
+    H.set_option("kernel_timing", 1)
+for _ in range(int(os.environ.get("HM_SETUPS", "1"))):
+    H.setup(1e-6)
 x = torch.randn(T.shape[0], dtype=torch.float64, device="cuda")
 for _ in range(nmv):
     y = H.matvec(x)
