@@ -217,6 +217,14 @@ def _run_gpu(args, rank, world, local, dev, stream):
     aca_other_ms = max_over_ranks(kt["aca_other_ms"] / K, world)
     mv_kern_ms = max_over_ranks(kt["matvec_ms"] / max(1, kt["matvec_n"]), world)
     mv_kern_ms_step = max_over_ranks(kt["matvec_ms"] / K, world)
+    per_rank = None
+    if world > 1:                      # per-rank phase times (load balance of the leaf partition)
+        import torch.distributed as dist
+        mine = torch.tensor([st["near_ms"], st["aca_ms"], st["setup_ms"], st["solve_ms"], st["stored_bytes"] / 1e9],
+                            dtype=torch.float64, device=dev)
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = [[round(float(v), 3) for v in t.cpu().tolist()] for t in allr]
     tree_s = max_over_ranks(st["tree_ms"], world) / 1e3
     setup_s = max_over_ranks(st["setup_ms"], world) / 1e3
     near_s = max_over_ranks(st["near_ms"], world) / 1e3
@@ -317,7 +325,8 @@ def _run_gpu(args, rank, world, local, dev, stream):
                           "k_mean": st["k_mean"], "evals": evals, "eval_rate_Gps": round(eval_rate / 1e9, 2),
                           "eval_rate_phase_Gps": round(eval_rate_phase / 1e9, 2),
                           "kernel_ms_per_step": {"eval": round(eval_ms, 3), "aca_other": round(aca_other_ms, 3),
-                                                 "matvec": round(mv_kern_ms_step, 3)}},
+                                                 "matvec": round(mv_kern_ms_step, 3)},
+                          "per_rank_near_aca_setup_solve_ms_storedGB": per_rank},
             "roofline": roof, "matvec_roofline": matvec_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         }

@@ -43,7 +43,11 @@ struct AcaWork {
   DBuf<char> tmp;
   DBuf<unsigned long long> ev, cnt;
   DBuf<int64_t> tot;
-  std::vector<AcaBlk> h_blk;
+  DBuf<int32_t> ovf;
+  DBuf<unsigned long long> novf;
+  PinnedVec<int64_t> h_tot;
+  PinnedVec<AcaBlk> h_blk;
+  PinnedVec<int32_t> h_idsp;
   std::vector<AcaState> h_state;
   std::vector<int32_t> h_ids, h_big;
   DBuf<EntryRef> lists;
@@ -81,6 +85,12 @@ __global__ void k_seg_table(const int64_t* __restrict__ pre, int64_t nact, int32
   if (a >= nact) return;
   const int64_t lo = pre[a], hi = pre[a + 1];
   for (int64_t w = (lo + 31) >> 5; (w << 5) < hi; ++w) tab[w] = (int32_t)a;
+}
+
+__global__ void k_store_totals(const int64_t* __restrict__ add, const unsigned long long* __restrict__ novf,
+                               int64_t* __restrict__ tot) {
+  tot[0] = *add;
+  tot[1] = (int64_t)*novf;
 }
 
 __global__ void k_step_totals(const int64_t* __restrict__ rpre, const int64_t* __restrict__ cpre,
@@ -375,31 +385,36 @@ __global__ void k_init_state(AcaState* __restrict__ S, int64_t nb) {
   S[c] = s;
 }
 
+// factor-pool size of every finished block; blocks that filled the workspace (status 2) are
+// appended to the overflow list (re-run with k_max columns)
 __global__ void k_final_sizes(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S, int64_t nb,
-                              int64_t* __restrict__ fsz) {
+                              int64_t* __restrict__ fsz, const int32_t* __restrict__ owned,
+                              int32_t* __restrict__ ovf, unsigned long long* __restrict__ novf) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c > nb) return;
   if (c == nb) { fsz[c] = 0; return; }
-  fsz[c] = S[c].status == 1 ? (int64_t)S[c].k * (B[c].m + B[c].n) : 0;
+  const AcaState st = S[c];
+  fsz[c] = st.status == 1 ? (int64_t)st.k * (B[c].m + B[c].n) : 0;
+  if (st.status == 2) ovf[atomicAdd(novf, 1ull)] = owned[c];
 }
-
 // pack finished blocks: [U (m x k) | V (n x k)] column-major, straight copies of the
-// first k workspace columns
-__global__ void k_aca_store(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S, int64_t nb,
-                            const int32_t* __restrict__ owned, const int64_t* __restrict__ fpre, int64_t base,
-                            const double* __restrict__ Uw, const double* __restrict__ Vw, double* __restrict__ pool,
-                            int64_t* __restrict__ foff, int32_t* __restrict__ frank) {
-  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+// first k workspace columns; one CTA per block
+__global__ void __launch_bounds__(256) k_aca_store(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S,
+                                                   int64_t nb, const int32_t* __restrict__ owned,
+                                                   const int64_t* __restrict__ fpre, int64_t base,
+                                                   const double* __restrict__ Uw, const double* __restrict__ Vw,
+                                                   double* __restrict__ pool, int64_t* __restrict__ foff,
+                                                   int32_t* __restrict__ frank) {
+  const int64_t c = blockIdx.x;
   if (c >= nb) return;
   const AcaState st = S[c];
   if (st.status != 1) return;
   const AcaBlk b = B[c];
   const int64_t o = base + fpre[c];
   const int64_t mu = (int64_t)st.k * b.m, nv = (int64_t)st.k * b.n;
-  for (int64_t x = lane; x < mu; x += 32) pool[o + x] = Uw[b.uoff + x];
-  for (int64_t x = lane; x < nv; x += 32) pool[o + mu + x] = Vw[b.voff + x];
-  if (lane == 0) {
+  for (int64_t x = threadIdx.x; x < mu; x += blockDim.x) pool[o + x] = Uw[b.uoff + x];
+  for (int64_t x = threadIdx.x; x < nv; x += blockDim.x) pool[o + mu + x] = Vw[b.voff + x];
+  if (threadIdx.x == 0) {
     foff[owned[c]] = o;
     frank[owned[c]] = st.k;
   }
@@ -441,7 +456,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   auto ms_since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
   const auto t0 = clk::now();
   const int64_t nb = (int64_t)ids.size();
-  std::vector<AcaBlk>& hb = W.h_blk;
+  PinnedVec<AcaBlk>& hb = W.h_blk;
   hb.resize(nb);
   std::vector<int32_t>& hbig = W.h_big;
   hbig.clear();
@@ -463,11 +478,14 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   const int64_t nbig = (int64_t)hbig.size();
   W.blk.alloc(nb); W.state.alloc(nb); W.owned.alloc(nb); W.piv.alloc(nb * 2 * kws);
   W.act.alloc(nb + 1); W.flag.alloc(nb + 1); W.pos.alloc(nb + 1); W.tot.alloc(3); W.big.alloc(nbig);
+  W.ovf.alloc(nb); W.novf.alloc(1); W.h_tot.resize(4);
   if (nbig) HM_CUDA(cudaMemcpyAsync(W.big.get(), hbig.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   W.rsz.alloc(nb + 1); W.csz.alloc(nb + 1); W.rpre.alloc(nb + 1); W.cpre.alloc(nb + 1);
   W.Uw.alloc(uo); W.Vw.alloc(vo); W.bmap.alloc(bo);
   HM_CUDA(cudaMemcpyAsync(W.blk.get(), hb.data(), nb * sizeof(AcaBlk), cudaMemcpyHostToDevice, st));
-  HM_CUDA(cudaMemcpyAsync(W.owned.get(), ids.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  W.h_idsp.resize(nb);
+  std::memcpy(W.h_idsp.data(), ids.data(), nb * sizeof(int32_t));
+  HM_CUDA(cudaMemcpyAsync(W.owned.get(), W.h_idsp.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   HM_CUDA(cudaMemsetAsync(W.bmap.get(), 0, bo * sizeof(uint32_t), st));
   k_init_state<<<grid_for(nb, 256), 256, 0, st>>>(W.state.get(), nb);
   HM_CHECK_LAUNCH();
@@ -531,36 +549,44 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   C.times.aca_phase_ms[1] += ms_since(t1);
   const auto t2 = clk::now();
   // pack finished blocks into the factor pool
-  k_final_sizes<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.rsz.get());
+  HM_CUDA(cudaMemsetAsync(W.novf.get(), 0, sizeof(unsigned long long), st));
+  k_final_sizes<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.rsz.get(), W.owned.get(),
+                                                       W.ovf.get(), W.novf.get());
   HM_CHECK_LAUNCH();
   cub_call(W.tmp, [&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, W.rsz.get(), W.rpre.get(), nb + 1, st);
   });
-  int64_t add = 0;
-  HM_CUDA(cudaMemcpyAsync(&add, W.rpre.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  std::vector<AcaState>& hs = W.h_state;
-  hs.resize(nb);
-  HM_CUDA(cudaMemcpyAsync(hs.data(), W.state.get(), nb * sizeof(AcaState), cudaMemcpyDeviceToHost, st));
+  k_store_totals<<<1, 1, 0, st>>>(W.rpre.get() + nb, W.novf.get(), W.tot.get());
+  HM_CHECK_LAUNCH();
+  int64_t* ht = W.h_tot.data();
+  HM_CUDA(cudaMemcpyAsync(ht, W.tot.get(), 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
+  const int64_t add = ht[0], nov = ht[1];
   const int64_t base = (int64_t)(C.fpool.used / sizeof(double));
   C.fpool.ensure((base + add) * sizeof(double) + 64);
   C.fpool.used = (base + add) * sizeof(double);
-  k_aca_store<<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(),
-                                                      base, W.Uw.get(), W.Vw.get(), (double*)C.fpool.base,
-                                                      C.foff.get(), C.frank.get());
+  k_aca_store<<<(unsigned)nb, 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(), base,
+                                           W.Uw.get(), W.Vw.get(), (double*)C.fpool.base, C.foff.get(), C.frank.get());
   HM_CHECK_LAUNCH();
-  std::vector<int32_t> hp;
+  if (nov) {
+    const size_t o0 = overflow.size();
+    overflow.resize(o0 + nov);
+    HM_CUDA(cudaMemcpyAsync(overflow.data() + o0, W.ovf.get(), nov * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
   if (pivots_out) {
-    hp.resize(nb * 2 * kws);
+    std::vector<AcaState>& hs = W.h_state;
+    hs.resize(nb);
+    HM_CUDA(cudaMemcpyAsync(hs.data(), W.state.get(), nb * sizeof(AcaState), cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> hp(nb * 2 * kws);
     HM_CUDA(cudaMemcpyAsync(hp.data(), W.piv.get(), hp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaStreamSynchronize(st));
+    for (int64_t c = 0; c < nb; ++c)
+      if (hs[c].status == 1)
+        (*pivots_out)[ids[c]].assign(hp.begin() + c * 2 * kws, hp.begin() + c * 2 * kws + 2 * hs[c].k);
   }
   HM_CUDA(cudaStreamSynchronize(st));
+  if (nov) std::sort(overflow.end() - nov, overflow.end());
   C.times.aca_phase_ms[3] += ms_since(t2);
-  for (int64_t c = 0; c < nb; ++c) {
-    if (hs[c].status == 2) { overflow.push_back(ids[c]); continue; }
-    if (pivots_out)
-      (*pivots_out)[ids[c]].assign(hp.begin() + c * 2 * kws, hp.begin() + c * 2 * kws + 2 * hs[c].k);
-  }
 }
 
 }  // namespace

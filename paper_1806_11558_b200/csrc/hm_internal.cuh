@@ -7,7 +7,9 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
@@ -88,6 +90,32 @@ struct DBuf {
     alloc(count);
   }
   T* get() const { return p; }
+};
+
+// Grow-only pinned host buffer: page-faulted and registered once, reused by every hm_setup,
+// and a true DMA source for the plan upload.
+template <class T>
+struct PinnedVec {
+  T* p = nullptr;
+  size_t n = 0, cap = 0;
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  PinnedVec& operator=(const PinnedVec&) = delete;
+  ~PinnedVec() { if (p) cudaFreeHost(p); }
+  void resize(size_t m) {
+    if (m > cap) {
+      const size_t c = std::max(m, cap + cap / 2);
+      T* q = nullptr;
+      HM_CUDA(cudaHostAlloc(&q, c * sizeof(T) + 16, cudaHostAllocDefault));
+      if (p) { std::memcpy(q, p, n * sizeof(T)); cudaFreeHost(p); }
+      p = q;
+      cap = c;
+    }
+    n = m;
+  }
+  T* data() { return p; }
+  size_t size() const { return n; }
+  T& operator[](size_t i) { return p[i]; }
 };
 
 // Growable device pool backed by CUDA virtual memory management: one reserved VA range,

@@ -220,14 +220,14 @@ struct RecWindow {
   }
 };
 
-template <int STAGES, int SBYTES>
-__global__ void __launch_bounds__(kMvThreads, 1)
+template <int STAGES, int SBYTES, int THREADS = kMvThreads, int MINB = 1>
+__global__ void __launch_bounds__(THREADS, MINB)
     k_mv_batched(const MvBatch* __restrict__ batches, const MvSeg* __restrict__ segs, int64_t nsegs_total,
                  const int32_t* __restrict__ cta_first,
                  const char* __restrict__ base0, const char* __restrict__ base1, const char* __restrict__ base2,
                  const double* __restrict__ x, double* __restrict__ y, int64_t scramble_n,
                  unsigned long long* __restrict__ prof) {
-  constexpr int NW = kMvThreads / 32, NC = NW - 1;
+  constexpr int NW = THREADS / 32, NC = NW - 1;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + STAGES;
@@ -461,32 +461,6 @@ __global__ void k_mv_dense_direct(const MvLarge* __restrict__ L, int64_t nl, con
 }  // namespace
 
 // ---- plan (host) ----------------------------------------------------------------------------
-// Grow-only pinned host buffer: page-faulted and registered once, reused by every hm_setup,
-// and a true DMA source for the plan upload.
-template <class T>
-struct PinnedVec {
-  T* p = nullptr;
-  size_t n = 0, cap = 0;
-  PinnedVec() = default;
-  PinnedVec(const PinnedVec&) = delete;
-  PinnedVec& operator=(const PinnedVec&) = delete;
-  ~PinnedVec() { if (p) cudaFreeHost(p); }
-  void resize(size_t m) {
-    if (m > cap) {
-      const size_t c = std::max(m, cap + cap / 2);
-      T* q = nullptr;
-      HM_CUDA(cudaHostAlloc(&q, c * sizeof(T) + 16, cudaHostAllocDefault));
-      if (p) { std::memcpy(q, p, n * sizeof(T)); cudaFreeHost(p); }
-      p = q;
-      cap = c;
-    }
-    n = m;
-  }
-  T* data() { return p; }
-  size_t size() const { return n; }
-  T& operator[](size_t i) { return p[i]; }
-};
-
 namespace {
 struct Item { int64_t byte0, bytes; int base; int32_t rlo, clo, n; uint32_t mnk; };
 // one planner thread's output over a contiguous slice of the item sequence
@@ -622,7 +596,7 @@ void plan_matvec(Context& C) {
   W.parts.resize(T);
   const int64_t* hoff = W.hoff.data();
   const bool wr = C.mv_kind == 0;
-  const int64_t cap = wr ? kWrStageBytes : C.mv_kind == 1 ? 48 * 1024 : C.mv_kind == 2 ? 24 * 1024 : 32 * 1024;
+  const int64_t cap = wr ? kWrStageBytes : (C.mv_kind == 1 || C.mv_kind == 4) ? 48 * 1024 : C.mv_kind == 2 ? 24 * 1024 : 32 * 1024;
   auto work = [&](int t) {
     PlanPart& P = W.parts[t];
     P.clear();
@@ -687,7 +661,7 @@ void plan_matvec(Context& C) {
   // one persistent CTA per SM (warp rings)
   int sms = 148;
   HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, C.device));
-  const int G = wr ? sms * kWrWarps : std::max(1, std::min<int>(sms, (int)nbat));
+  const int G = wr ? sms * kWrWarps : std::max(1, std::min<int>(C.mv_kind == 4 ? 2 * sms : sms, (int)nbat));
   W.cta.resize(G + 1);
   {
     double tot = 0;
@@ -756,6 +730,8 @@ void plan_matvec(Context& C) {
                                  256 + 8 * 24 * 1024));
     HM_CUDA(cudaFuncSetAttribute(k_mv_batched<6, 32 * 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  256 + 6 * 32 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<2, 48 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 2 * 48 * 1024));
     HM_CUDA(cudaFuncSetAttribute(k_mv_warps, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  256 + kWrWarps * kWrStages * kWrStageBytes));
     attr = true;
@@ -797,6 +773,10 @@ void matvec_internal(Context& C, const double* x_int, double* y_int) {
           (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
     } else if (C.mv_kind == 2) {
       k_mv_batched<8, 24 * 1024><<<C.mv_grid, kMvThreads, 256 + 8 * 24 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
+    } else if (C.mv_kind == 4) {
+      k_mv_batched<2, 48 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 2 * 48 * 1024, st>>>(
           C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
           (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
     } else {
