@@ -90,11 +90,21 @@ const char* hm_last_error(hm_ctx ctx);
  *   "solver"       0 = GMRES(restart) (BASELINE.json), 1 = CG; default 0
  *   "restart"      GMRES restart length m, default 100
  *   "max_iter"     Krylov iteration cap (total matvecs), default 10000
- *   "aca_chunk_mb" ACA workspace budget per chunk in MiB, default 16384, capped at 1/4 of the
- *                  free device memory at hm_setup
- *   "aca_kws"      ACA workspace columns per block before the overflow re-run, default 16
+ *   "aca_chunk_mb" ACA workspace budget per chunk in MiB, default 32768, capped before every
+ *                  chunk at 0.45 x (free device memory + current workspace)
+ *   "aca_kws"      ACA workspace columns per block before the overflow re-run, default 12
  *   "record_pivots" keep each block's ACA pivot sequence for hm_get_lowrank: 1 on, 0 off,
  *                  -1 (default) on iff N <= 25000
+ *   "kernel_timing" 1: record CUDA events on the context stream around every launch of
+ *                  each kernel family (near-field evaluation, ACA evaluation, other ACA,
+ *                  matvec, Krylov BLAS-1); totals in hm_get_stats "kt"; setting it resets them
+ *   "mv_kernel"    small-leaf matvec pipeline: 4 (default) two CTA rings per SM, 2 x 48 KiB
+ *                  stages each; 1 one ring of 4 x 48 KiB; 2 / 3 one ring of 8 x 24 / 6 x 32
+ *                  KiB; 0 per-warp rings of 2 x 13 KiB.  Re-plans the matvec if set up.
+ *   "mv_profile"   1: accumulate producer/consumer wait and work cycles of the CTA-ring
+ *                  matvec (hm_get_stats "mv_prof_cycles"); diagnostic
+ *   "mv_scramble"  1: DIAGNOSTIC ONLY, wrong products: spread the row bases of the CTA-ring
+ *                  matvec's y atomics over y (measures same-address atomic contention)
  * Errors: HM_ERR_ARG for an unknown key or an out-of-range value. */
 hm_status hm_set_option(hm_ctx ctx, const char* key, double value);
 hm_status hm_get_option(hm_ctx ctx, const char* key, double* value);

@@ -78,15 +78,6 @@ __global__ void k_step_compact(const AcaBlk* __restrict__ B, const int32_t* __re
   csz[a] = B[c].m;
 }
 
-// segment-start table of a flattened batch: every 32-entry slot w gets the segment holding
-// entry 32 w (thread per active segment; the segments tile [0, total))
-__global__ void k_seg_table(const int64_t* __restrict__ pre, int64_t nact, int32_t* __restrict__ tab) {
-  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (a >= nact) return;
-  const int64_t lo = pre[a], hi = pre[a + 1];
-  for (int64_t w = (lo + 31) >> 5; (w << 5) < hi; ++w) tab[w] = (int32_t)a;
-}
-
 __global__ void k_store_totals(const int64_t* __restrict__ add, const unsigned long long* __restrict__ novf,
                                int64_t* __restrict__ tot) {
   tot[0] = *add;
@@ -130,6 +121,15 @@ struct AcaMap {
     const AcaState& st = S[r.seg];
     s = ROW ? b.q.rlo + st.i : b.q.rlo + r.idx;
     t = ROW ? b.q.clo + r.idx : b.q.clo + st.js;
+  }
+  // pull the k residual-correction operands of entry r into L1 before the quadrature, so put()
+  // does not expose their HBM latency at the end of the thread's work
+  __device__ void prefetch(EntryRef r) const {
+    const AcaBlk& b = B[r.seg];
+    const AcaState st = S[r.seg];
+    const double* p = ROW ? Vw + b.voff + r.idx : Uw + b.uoff + r.idx;
+    const int64_t stride = ROW ? b.n : b.m;
+    for (int l = 0; l < st.k; ++l) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + l * stride));
   }
   __device__ void put(EntryRef r, double a) const {
     const AcaBlk& b = B[r.seg];
@@ -177,6 +177,9 @@ __device__ int first_unused(const uint32_t* bm, int m, int lane) {
   return best == INT_MAX ? -1 : best;
 }
 
+// blocks with m + n >= kBigMN get a CTA (not a warp) in the pivot and update kernels
+constexpr int kBigMN = 2048;
+
 __global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, const int32_t* __restrict__ act,
                             int64_t nact, double* __restrict__ Vw, uint32_t* __restrict__ bmap) {
   const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -186,6 +189,7 @@ __global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__
   AcaState st = S[c];
   if (st.status != 0) return;
   const AcaBlk b = B[c];
+  if (b.m + b.n >= kBigMN) return;                      // k_aca_pivot_big
   double* r = Vw + b.voff + (int64_t)st.k * b.n;
   uint32_t* bm = bmap + b.boff;
   double best = -1.0;
@@ -223,6 +227,65 @@ __global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__
   }
 }
 
+// k_aca_pivot for the big blocks of the chunk (m + n >= kBigMN): one CTA per block
+__global__ void __launch_bounds__(256) k_aca_pivot_big(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
+                                                       const int32_t* __restrict__ big, double* __restrict__ Vw,
+                                                       uint32_t* __restrict__ bmap) {
+  __shared__ double sbest[8];
+  __shared__ int sidx[8];
+  const int64_t c = big[blockIdx.x];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  AcaState st = S[c];
+  if (st.status != 0) return;
+  const AcaBlk b = B[c];
+  double* r = Vw + b.voff + (int64_t)st.k * b.n;
+  uint32_t* bm = bmap + b.boff;
+  double best = -1.0;
+  int bj = INT_MAX;
+  for (int j = threadIdx.x; j < b.n; j += 256) {
+    const double a = fabs(r[j]);
+    if (a > best) { best = a; bj = j; }
+  }
+  warp_argmax(best, bj);
+  if (lane == 0) { sbest[w] = best; sidx[w] = bj; }
+  __syncthreads();
+  best = sbest[0]; bj = sidx[0];
+  for (int g = 1; g < 8; ++g)
+    if (sbest[g] > best || (sbest[g] == best && sidx[g] < bj)) { best = sbest[g]; bj = sidx[g]; }
+  if (threadIdx.x == 0) bm[st.i >> 5] |= 1u << (st.i & 31);   // row i is used (A12)
+  __syncthreads();
+  const double piv = r[bj];
+  if (piv == 0.0) {                                            // zero residual row: next unused row
+    if (w == 0) {
+      const int nx = first_unused(bm, b.m, lane);
+      if (lane == 0) {
+        if (nx < 0) st.status = 1;
+        else { st.i = nx; st.skip = 1; }
+        S[c] = st;
+      }
+    }
+    return;
+  }
+  double vv = 0.0;
+  for (int j = threadIdx.x; j < b.n; j += 256) {
+    const double v = ddiv(r[j], piv);
+    r[j] = v;
+    vv += v * v;
+  }
+  vv = warp_sum(vv);
+  __syncthreads();
+  if (lane == 0) sbest[w] = vv;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    vv = 0.0;
+    for (int g = 0; g < 8; ++g) vv += sbest[g];
+    st.js = bj;
+    st.vv = vv;
+    st.skip = 0;
+    S[c] = st;
+  }
+}
+
 // Sum 16 per-lane values over the warp by recursive halving (16 shuffles instead of 16 x 5):
 // on return a[0] of lane L holds the warp total of value index
 // 8*bit4(L) + 4*bit3(L) + 2*bit2(L) + bit1(L)  (two lanes per index).
@@ -252,7 +315,6 @@ __device__ __forceinline__ int reduce16_index(int lane) {
 // pass with the 8 (u^T U_l) and 8 (V_l^T v) partial sums in registers (u_t / v_j loaded once
 // per pass, 8 independent loads in flight) and reduced together by one recursive-halving
 // butterfly.  Norms feed the stop test only (A15: tree-reduced on the GPU).
-constexpr int kBigMN = 2048;
 
 template <int G>
 __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, const double* __restrict__ Uw,
@@ -523,9 +585,9 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     W.lists.alloc(std::max(tot[0], tot[1]));
     W.rtab.alloc(tot[0] / 32 + 2);
     W.ctab.alloc(tot[1] / 32 + 2);
-    k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.rpre.get(), nact, W.rtab.get());
+    k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.rpre.get(), nact, 0, W.rtab.get());
     HM_CHECK_LAUNCH();
-    k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.cpre.get(), nact, W.ctab.get());
+    k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.cpre.get(), nact, 0, W.ctab.get());
     HM_CHECK_LAUNCH();
     aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(), nb, W.Uw.get(), W.Vw.get()},
              tot[0], W);
@@ -533,6 +595,10 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     k_aca_pivot<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, W.Vw.get(),
                                                           W.bmap.get());
     HM_CHECK_LAUNCH();
+    if (nbig) {
+      k_aca_pivot_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), W.Vw.get(), W.bmap.get());
+      HM_CHECK_LAUNCH();
+    }
     ks.reset();
     aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(), nb, W.Uw.get(), W.Vw.get()},
              tot[1], W);
@@ -640,7 +706,10 @@ void setup_aca(Context& C) {
     HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double ws = 8.0 * (double)(W.Uw.n + W.Vw.n);
     const double b = std::min(C.aca_chunk_mb * 1048576.0, 0.45 * ((double)free_b + ws));
-    if (ws > b) { W.Uw.release(); W.Vw.release(); }
+    // hysteresis: keep the allocated workspace while it is at most twice the budget (a chunk
+    // then uses at most the budget of it); re-allocating multi-GB buffers costs tens of ms
+    // and while the free memory still holds a full chunk's factor output (<= the budget)
+    if (ws > 2.0 * b || (double)free_b < b) { W.Uw.release(); W.Vw.release(); }
     return std::max(b, 64.0 * 1048576.0);
   };
   C.times.aca_phase_ms[6] = ms_since(t0);

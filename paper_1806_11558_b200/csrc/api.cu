@@ -113,6 +113,13 @@ void VmmPool::release() {
   base = 0; reserved = mapped = used = 0;
 }
 
+__global__ void k_seg_table(const int64_t* __restrict__ pre, int64_t nseg, int64_t e0, int32_t* __restrict__ tab) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= nseg) return;
+  const int64_t lo = pre[a] - e0, hi = pre[a + 1] - e0;
+  for (int64_t w = (lo + 31) >> 5; (w << 5) < hi; ++w) tab[w] = (int32_t)a;
+}
+
 // ---- kernel-family timers -------------------------------------------------------------------
 cudaEvent_t KTimer::get() {
   if (pool.empty()) {
@@ -581,7 +588,7 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
       o << ",\"mv_prof_cycles\":[" << pr[0] << "," << pr[1] << "," << pr[2] << "]";
     }
     o << ",\"kt\":{\"on\":" << (C.kt.on ? 1 : 0);
-    const char* fam[hm::KF_NUM] = {"eval_near", "eval_aca", "aca_other", "matvec"};
+    const char* fam[hm::KF_NUM] = {"eval_near", "eval_aca", "aca_other", "matvec", "krylov"};
     for (int f = 0; f < hm::KF_NUM; ++f)
       o << ",\"" << fam[f] << "_ms\":" << C.kt.ms[f] << ",\"" << fam[f] << "_n\":" << C.kt.n[f];
     o << "}}";

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256) k_eval_fused(M m, int64_t total, unsigned
 //   k_eval_list<4>  persistent grid-stride over the order-4 list (count read on the device);
 //   k_eval_rest     persistent, in-CTA class sort of the remaining few.
 template <class M>
-__global__ void __launch_bounds__(128) k_eval_class3(M m, int64_t total, EntryRef* __restrict__ lists,
+__global__ void __launch_bounds__(128, 4) k_eval_class3(M m, int64_t total, EntryRef* __restrict__ lists,
                                                      unsigned long long* __restrict__ cnt /* [n4, nrest] */,
                                                      unsigned long long* __restrict__ evals) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(128) k_eval_class3(M m, int64_t total, EntryRe
   else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
   unsigned long long ev = 0;
   if (cls == 3) {
+    m.prefetch(r);
     double X[9], Y[9];
     load_panel_vertices(m.P, xs, X);
     load_panel_vertices(m.P, ys, Y);
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(128) k_eval_list(M m, const EntryRef* __restri
     const EntryRef r = list[k];
     int s, t, xs, ys;
     m.pair(r, s, t);
+    m.prefetch(r);
     canonical_class(m.P, s, t, xs, ys);
     double X[9], Y[9];
     load_panel_vertices(m.P, xs, X);

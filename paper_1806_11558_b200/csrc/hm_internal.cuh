@@ -191,14 +191,14 @@ struct PhaseTimes {
 
 // Per-kernel-family device timing (option "kernel_timing"): CUDA events recorded on the
 // library stream around every launch of a family, resolved at the next synchronous point.
-enum KFam { KF_EVAL_NEAR = 0, KF_EVAL_ACA = 1, KF_ACA_OTHER = 2, KF_MATVEC = 3, KF_NUM = 4 };
+enum KFam { KF_EVAL_NEAR = 0, KF_EVAL_ACA = 1, KF_ACA_OTHER = 2, KF_MATVEC = 3, KF_KRYLOV = 4, KF_NUM = 5 };
 struct KTimer {
   bool on = false;
   std::vector<cudaEvent_t> pool;
   struct P { int fam; cudaEvent_t a, b; };
   std::vector<P> pend;
-  double ms[KF_NUM] = {0, 0, 0, 0};
-  int64_t n[KF_NUM] = {0, 0, 0, 0};
+  double ms[KF_NUM] = {0, 0, 0, 0, 0};
+  int64_t n[KF_NUM] = {0, 0, 0, 0, 0};
   cudaEvent_t get();
   void resolve();   // caller has synchronised the stream
   void reset();
@@ -216,7 +216,7 @@ struct Context {
   // options
   int k_max = 64, solver = 0, restart = 100, max_iter = 10000;
   int record_pivots = -1;      // -1 auto (N <= 25000), 0 off, 1 on
-  double aca_chunk_mb = 16384, aca_kws = 16;
+  double aca_chunk_mb = 32768, aca_kws = 12;
 
   // tree state
   bool have_tree = false, have_setup = false;
@@ -265,7 +265,7 @@ struct Context {
   int mv_grid = 0;
   DBuf<unsigned long long> mv_prof;   // option "mv_profile": [producer empty-wait, consumer full-wait, consumer work] cycles
   int mv_scramble = 0;         // diagnostic option "mv_scramble" (wrong results): see k_mv_batched
-  int mv_kind = 1;             // option "mv_kernel": 1 CTA ring 4 x 48 KiB (default), 2 / 3 CTA ring 8 x 24 / 6 x 32 KiB, 0 warp rings
+  int mv_kind = 4;             // option "mv_kernel": 4 two CTA rings per SM, 2 x 48 KiB each (default); 1 one CTA ring 4 x 48 KiB; 2 / 3 one ring 8 x 24 / 6 x 32 KiB; 0 warp rings
   int64_t mv_nbatches = 0, mv_tlen = 0, mv_nsegs = 0;
   int64_t n_lr_small = 0, n_lr_large = 0;
 
@@ -278,6 +278,7 @@ struct Context {
   // persistent scratch (grow-only)
   TreeWs tws;
   DBuf<int64_t> near_sz;
+  DBuf<int32_t> near_tab;
   DBuf<char> near_tmp;
   std::shared_ptr<EntryBatchWork> near_ws;
   std::shared_ptr<AcaWork> aca_ws;
@@ -352,6 +353,11 @@ __device__ __forceinline__ int64_t warp_find_segment(const I* __restrict__ pre, 
     while (lo + 1 < nseg && (int64_t)__ldg(pre + lo + 1) <= e) ++lo;
   return lo;
 }
+
+// Segment-start table of a flattened batch of nseg non-empty segments (prefix pre, entries
+// counted from e0): tab[w] = segment holding entry 32 w.  One thread per segment; with it an
+// entry finds its segment by one load and a short forward walk instead of a binary search.
+__global__ void k_seg_table(const int64_t* __restrict__ pre, int64_t nseg, int64_t e0, int32_t* __restrict__ tab);
 
 inline unsigned grid_for(int64_t n, int block) {
   int64_t g = (n + block - 1) / block;

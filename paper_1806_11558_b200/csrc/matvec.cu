@@ -588,8 +588,8 @@ void plan_matvec(Context& C) {
   lr_order.clear();
   for (int64_t b = 0; b < na; ++b)
     if (C.h_rank[b] > 0) lr_order.push_back(b);
-  if (!std::is_sorted(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; }))
-    std::sort(lr_order.begin(), lr_order.end(), [&](int64_t a, int64_t b) { return C.h_foff[a] < C.h_foff[b]; });
+  // block order = factor-pool order except for the few blocks re-run after a workspace
+  // overflow (stored at the end): they just become separate bulk-copy runs, no sort needed
   const int64_t nlr = (int64_t)lr_order.size(), total = nd + nlr;
   const int T = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()),
                                                               16, total / 20000 + 1}));

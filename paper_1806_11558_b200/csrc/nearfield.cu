@@ -26,9 +26,11 @@ struct NearMap {
   int64_t b0, nseg;      // first leaf of the chunk, leaves in the chunk
   int64_t e0;            // off[b0]
   double* store;
+  const int32_t* tab;    // segment-start table of the chunk (k_seg_table)
   __device__ bool locate(int64_t e, bool valid, EntryRef& r) const {
-    const int64_t b = b0 + warp_find_segment(off + b0, nseg, e + e0, valid);
     if (!valid) return false;
+    int64_t b = b0 + tab[e >> 5];
+    while (off[b + 1] - e0 <= e) ++b;
     r.seg = (int32_t)b;
     r.idx = (int32_t)(e + e0 - off[b]);
     return true;
@@ -39,6 +41,7 @@ struct NearMap {
     s = Q.rlo + r.idx / ncol;
     t = Q.clo + r.idx % ncol;
   }
+  __device__ void prefetch(EntryRef) const {}
   __device__ void put(EntryRef r, double a) const { store[off[r.seg] + r.idx] = a; }
 };
 
@@ -81,7 +84,10 @@ void setup_nearfield(Context& C) {
     // leaves [b0, b1) with at most `chunk` entries (at least one leaf)
     int64_t b1 = std::upper_bound(hoff.begin() + b0 + 1, hoff.begin() + nb + 1, hoff[b0] + chunk) - hoff.begin() - 1;
     b1 = std::max(b1, b0 + 1);
-    NearMap m{C.panel.get(), q, C.doff.get(), b0, b1 - b0, hoff[b0], C.dstore.get()};
+    C.near_tab.alloc((hoff[b1] - hoff[b0]) / 32 + 2);
+    k_seg_table<<<grid_for(b1 - b0, 256), 256, 0, st>>>(C.doff.get() + b0, b1 - b0, hoff[b0], C.near_tab.get());
+    HM_CHECK_LAUNCH();
+    NearMap m{C.panel.get(), q, C.doff.get(), b0, b1 - b0, hoff[b0], C.dstore.get(), C.near_tab.get()};
     C.evals_near += eval_batched(C, m, hoff[b1] - hoff[b0], W);
     b0 = b1;
   }

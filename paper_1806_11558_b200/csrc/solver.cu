@@ -113,8 +113,12 @@ struct Red {
   double* mdot(const double* Vb, int64_t ld, int nv, const double* w) {
     part.alloc((size_t)kRedBlocks * nv);
     out.alloc(nv + 8);
+    { KScope ks_(C, KF_KRYLOV);
     k_mdot<<<kRedBlocks, kRedThreads, 0, C.stream>>>(Vb, ld, nv, w, C.N, part.get());
+    }
+    { KScope ks_(C, KF_KRYLOV);
     k_mdot_final<<<(nv + 127) / 128, 128, 0, C.stream>>>(part.get(), kRedBlocks, nv, out.get());
+    }
     HM_CHECK_LAUNCH();
     return out.get();
   }
@@ -133,7 +137,9 @@ void apply(Context& C, const double* x, double* y) { matvec_internal(C, x, y); }
 
 double true_relres(Context& C, Red& R, const double* b, const double* x, double bn, double* tmp) {
   apply(C, x, tmp);
+  { KScope ks_(C, KF_KRYLOV);
   k_sub<<<vgrid(C.N), 256, 0, C.stream>>>(b, tmp, tmp, C.N);
+  }
   HM_CHECK_LAUNCH();
   double rr = R.dot(tmp, tmp);
   return bn > 0 ? std::sqrt(rr) / bn : 0.0;
@@ -158,12 +164,16 @@ void cg(Context& C, const double* b, double* x, double tol, int* iters, double* 
     const double pAp = R.dot(p, Ap);
     if (!(pAp > 0.0)) fail(HM_ERR_BREAKDOWN, "CG breakdown: p^T H p <= 0 at iteration " + std::to_string(it));
     const double alpha = rr / pAp;
+    { KScope ks_(C, KF_KRYLOV);
     k_cg_xr<<<vgrid(N), 256, 0, st>>>(x, r, p, Ap, alpha, N);
+    }
     HM_CHECK_LAUNCH();
     const double rr1 = R.dot(r, r);
     const double beta = rr1 / rr;
     rr = rr1;
+    { KScope ks_(C, KF_KRYLOV);
     k_cg_p<<<vgrid(N), 256, 0, st>>>(p, r, beta, N);
+    }
     HM_CHECK_LAUNCH();
     ++it;
   }
@@ -189,12 +199,16 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
   if (bn == 0.0) { *iters = 0; *relres = 0.0; return; }
   for (;;) {
     apply(C, x, w);
+    { KScope ks_(C, KF_KRYLOV);
     k_sub<<<vgrid(N), 256, 0, st>>>(b, w, w, N);
+    }
     HM_CHECK_LAUNCH();
     const double beta = std::sqrt(R.dot(w, w));
     if (beta <= tol * bn || total >= C.max_iter) break;
     HM_CUDA(cudaMemcpyAsync(hdev.get(), &beta, sizeof(double), cudaMemcpyHostToDevice, st));
+    { KScope ks_(C, KF_KRYLOV);
     k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb, N);
+    }
     HM_CHECK_LAUNCH();
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
@@ -205,11 +219,15 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
       ++total;
       // CGS2
       double* d1 = R.mdot(Vb, ld, j + 1, w);
+      { KScope ks_(C, KF_KRYLOV);
       k_msub<<<vgrid(N), 256, 0, st>>>(Vb, ld, j + 1, d1, w, N);
+      }
       HM_CHECK_LAUNCH();
       HM_CUDA(cudaMemcpyAsync(h.data(), d1, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
       double* d2 = R.mdot(Vb, ld, j + 1, w);
+      { KScope ks_(C, KF_KRYLOV);
       k_msub<<<vgrid(N), 256, 0, st>>>(Vb, ld, j + 1, d2, w, N);
+      }
       HM_CHECK_LAUNCH();
       HM_CUDA(cudaMemcpyAsync(h2.data(), d2, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
       HM_CUDA(cudaStreamSynchronize(st));
@@ -230,7 +248,9 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
       jend = j + 1;
       if (std::fabs(g[j + 1]) <= tol * bn || total >= C.max_iter || hn == 0.0) { conv = true; break; }
       HM_CUDA(cudaMemcpyAsync(hdev.get(), &hn, sizeof(double), cudaMemcpyHostToDevice, st));
+      { KScope ks_(C, KF_KRYLOV);
       k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb + (int64_t)(j + 1) * ld, N);
+      }
       HM_CHECK_LAUNCH();
     }
     for (int i = jend - 1; i >= 0; --i) {
@@ -239,7 +259,9 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
       y[i] = s / H[i + (size_t)i * (m + 1)];
     }
     HM_CUDA(cudaMemcpyAsync(hdev.get(), y.data(), jend * sizeof(double), cudaMemcpyHostToDevice, st));
+    { KScope ks_(C, KF_KRYLOV);
     k_madd<<<vgrid(N), 256, 0, st>>>(Vb, ld, jend, hdev.get(), x, N);
+    }
     HM_CHECK_LAUNCH();
     HM_CUDA(cudaStreamSynchronize(st));
     if (conv && (std::fabs(g[jend]) <= tol * bn || total >= C.max_iter)) break;
