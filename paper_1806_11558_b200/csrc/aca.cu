@@ -122,15 +122,6 @@ struct AcaMap {
     s = ROW ? b.q.rlo + st.i : b.q.rlo + r.idx;
     t = ROW ? b.q.clo + r.idx : b.q.clo + st.js;
   }
-  // pull the k residual-correction operands of entry r into L1 before the quadrature, so put()
-  // does not expose their HBM latency at the end of the thread's work
-  __device__ void prefetch(EntryRef r) const {
-    const AcaBlk& b = B[r.seg];
-    const AcaState st = S[r.seg];
-    const double* p = ROW ? Vw + b.voff + r.idx : Uw + b.uoff + r.idx;
-    const int64_t stride = ROW ? b.n : b.m;
-    for (int l = 0; l < st.k; ++l) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + l * stride));
-  }
   __device__ void put(EntryRef r, double a) const {
     const AcaBlk& b = B[r.seg];
     const AcaState st = S[r.seg];

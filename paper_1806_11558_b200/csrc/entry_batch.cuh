@@ -202,7 +202,6 @@ __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, int64_t total, Entr
   else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
   unsigned long long ev = 0;
   if (cls == 3) {
-    m.prefetch(r);
     double X[9], Y[9];
     load_panel_vertices(m.P, xs, X);
     load_panel_vertices(m.P, ys, Y);
@@ -224,7 +223,6 @@ __global__ void __launch_bounds__(128) k_eval_list(M m, const EntryRef* __restri
     const EntryRef r = list[k];
     int s, t, xs, ys;
     m.pair(r, s, t);
-    m.prefetch(r);
     canonical_class(m.P, s, t, xs, ys);
     double X[9], Y[9];
     load_panel_vertices(m.P, xs, X);

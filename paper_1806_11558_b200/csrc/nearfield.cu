@@ -41,7 +41,6 @@ struct NearMap {
     s = Q.rlo + r.idx / ncol;
     t = Q.clo + r.idx % ncol;
   }
-  __device__ void prefetch(EntryRef) const {}
   __device__ void put(EntryRef r, double a) const { store[off[r.seg] + r.idx] = a; }
 };
 
