@@ -86,7 +86,8 @@ hm_status hm_destroy(hm_ctx ctx);
 const char* hm_last_error(hm_ctx ctx);
 
 /* Options (hm_set_option / hm_get_option), numeric values:
- *   "k_max"        ACA rank cap per block (A11), default 64, >= 1
+ *   "k_max"        ACA rank cap per block (A11), default 64, 1..256; the fixed rank when
+ *                  eps_aca = 0
  *   "solver"       0 = GMRES(restart) (BASELINE.json), 1 = CG; default 0
  *   "restart"      GMRES restart length m, default 100
  *   "max_iter"     Krylov iteration cap (total matvecs), default 10000
@@ -122,8 +123,10 @@ hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double e
 /* Assemble this rank's part of the H-matrix: every owned non-admissible leaf is evaluated
  * densely, every owned admissible leaf is compressed by ACA with partial
  * pivoting and the relative Frobenius stop ||u_k|| ||v_k|| <= eps_aca ||S_k||_F (A11-A12).
+ * eps_aca = 0 selects the paper's fixed-rank mode ("k" of P:447): no stop test,
+ * every block runs to k = min(m, n, option k_max) unless its residual is exactly zero.
  * No communication.  Synchronous.
- * Errors: HM_ERR_STATE (no tree), HM_ERR_ARG (eps_aca <= 0 or not finite), HM_ERR_OOM,
+ * Errors: HM_ERR_STATE (no tree), HM_ERR_ARG (eps_aca < 0 or not finite), HM_ERR_OOM,
  * HM_ERR_NUMERIC (a non-finite entry; message names the block), HM_ERR_CUDA. */
 hm_status hm_setup(hm_ctx ctx, double eps_aca);
 

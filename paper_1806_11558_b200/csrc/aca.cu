@@ -688,7 +688,9 @@ void setup_aca(Context& C) {
   auto& pivots = C.h_piv;
   pivots.clear();
   if (rec) pivots.resize(nb);
-  const int kws = std::max(1, std::min(C.k_max, (int)C.aca_kws));
+  // eps_aca = 0: the paper's fixed-rank mode — no Frobenius stop, every block runs to
+  // k = min(m, n, k_max) (or an exactly zero residual), so the workspace holds k_max columns
+  const int kws = C.eps_aca == 0.0 ? C.k_max : std::max(1, std::min(C.k_max, (int)C.aca_kws));
   // workspace per chunk: the option, capped by the device memory left at the start of the chunk
   // (the factor pool grows by ~k_mean/KWS of the workspace per chunk, so 0.45 of what is free
   // plus the current workspace leaves room for it)

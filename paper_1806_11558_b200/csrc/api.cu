@@ -296,12 +296,12 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     std::string k = key ? key : "";
     auto bad = [&]() { hm::fail(HM_ERR_ARG, "hm_set_option: bad value for " + k); };
     if (!std::isfinite(v)) bad();
-    if (k == "k_max") { if (v < 1 || v > 64) bad(); C.k_max = (int)v; }
+    if (k == "k_max") { if (v < 1 || v > 256) bad(); C.k_max = (int)v; }
     else if (k == "solver") { if (v != 0 && v != 1) bad(); C.solver = (int)v; }
     else if (k == "restart") { if (v < 1 || v > 1000) bad(); C.restart = (int)v; }
     else if (k == "max_iter") { if (v < 1) bad(); C.max_iter = (int)v; }
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
-    else if (k == "aca_kws") { if (v < 1 || v > 64) bad(); C.aca_kws = v; }
+    else if (k == "aca_kws") { if (v < 1 || v > 256) bad(); C.aca_kws = v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
     else if (k == "mv_kernel") { if (v != 0 && v != 1 && v != 2 && v != 3 && v != 4) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_profile") {
@@ -355,7 +355,7 @@ hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double e
 hm_status hm_setup(hm_ctx ctx, double eps_aca) {
   return guarded(ctx, [&](Context& C) {
     need_tree(C);
-    if (!(eps_aca > 0) || !std::isfinite(eps_aca)) hm::fail(HM_ERR_ARG, "hm_setup: eps_aca must be > 0");
+    if (!(eps_aca >= 0) || !std::isfinite(eps_aca)) hm::fail(HM_ERR_ARG, "hm_setup: eps_aca must be finite and >= 0");
     C.have_setup = false;
     C.eps_aca = eps_aca;
     Timer all(C);

@@ -78,7 +78,9 @@ def test_error_codes_and_state_machine():
         H.matvec(torch.zeros(320, dtype=torch.float64, device="cuda"))
     assert e.value.status == 2
     with pytest.raises(HMError):
-        H.setup(0.0)
+        H.setup(-1e-6)                                         # eps_aca = 0 is the fixed-rank mode
+    with pytest.raises(HMError):
+        H.setup(float("nan"))
     with pytest.raises(HMError):
         H.set_option("nope", 1)
     with pytest.raises(HMError):

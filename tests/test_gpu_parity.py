@@ -144,6 +144,30 @@ def test_c1_blocks_pivots_and_matvec(c1):
     assert np.linalg.norm(yh - R.matvec(xs[2])) <= 1e-12 * np.linalg.norm(yh)
 
 
+def test_fixed_rank_mode_c1(O, torch_cuda):
+    """eps_aca = 0 (the paper's fixed rank k) with k_max = 8: every admissible block has
+    exactly min(8, m, n) terms, pivots identical to the oracle's fixed-rank ACA, H-matvec equal
+    to the oracle's H-matvec to 1e-12."""
+    V, T = icosphere(3)
+    H = _gpu(V, T)
+    H.set_option("k_max", 8)
+    H.set_option("record_pivots", 1)
+    H.setup(0.0)
+    R = O.Problem(V, T)
+    R.assemble(0.0, 8)
+    adm, _ = H.leaves(0)
+    for b, q in enumerate(adm):
+        m, n = q[1] - q[0], q[3] - q[2]
+        U, W, pv = H.lowrank(b, m, n, pivots=True)
+        assert U.shape[1] == min(8, m, n) == R.rank(b)
+        assert np.array_equal(pv, R.pivots(b)), f"block {b}"
+    x = seeded_vector(T.shape[0], 4)
+    yg = H.matvec(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+    yo = R.matvec(x)
+    assert np.linalg.norm(yg - yo) <= 1e-12 * np.linalg.norm(yo)
+    H.close()
+
+
 @pytest.mark.parametrize("solver", [0, 1])
 def test_c1_solve_vs_oracle(c1, solver):
     V, T, H, R, A = c1

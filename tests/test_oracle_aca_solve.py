@@ -48,6 +48,30 @@ def test_aca_interpolation_and_full_rank(O):
     assert U.shape[1] == 12 and np.linalg.norm(B - U @ V.T) <= 1e-12 * np.linalg.norm(B)
 
 
+def test_fixed_rank_aca(O):
+    """eps_aca = 0 is the paper's fixed-rank mode: exactly K = min(m, n, kcap) terms on a
+    matrix of full numerical rank; the residual is interpolated at the K pivot rows/columns
+     and shrinks with K like the smooth kernel's singular values."""
+    rng = np.random.default_rng(11)
+    X = rng.uniform(size=(60, 3)); Y = rng.uniform(size=(45, 3)) + np.array([2.5, 0, 0])
+    A = 1.0 / np.linalg.norm(X[:, None] - Y[None], axis=2)
+    s = np.linalg.svd(A, compute_uv=False)
+    errs = []
+    for K in (2, 4, 8, 12):
+        U, V, piv = O.aca_matrix(A, 0.0, K)
+        assert U.shape[1] == K
+        R = A - U @ V.T
+        rows, cols = piv[:, 0], piv[:, 1]
+        assert np.abs(R[rows, :]).max() <= 1e-12 * np.abs(A).max()
+        assert np.abs(R[:, cols]).max() <= 1e-12 * np.abs(A).max()
+        errs.append(np.linalg.norm(R, 2))
+        assert errs[-1] <= 1e3 * s[K]                  # quasi-optimal within a modest factor
+    assert all(b < a for a, b in zip(errs, errs[1:]))
+    U, V, _ = O.aca_matrix(A, 0.0, 64)                 # K >= min(m, n): exact
+    assert U.shape[1] == 45
+    assert np.abs(A - U @ V.T).max() <= 1e-12 * np.abs(A).max()
+
+
 def test_aca_on_admissible_blocks(O):
     V, T = icosphere(3)
     P = O.Problem(V, T)
