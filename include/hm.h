@@ -155,6 +155,16 @@ hm_status hm_solve(hm_ctx ctx, const double* rhs, double* sol, double tol,
  * Errors: HM_ERR_STATE (no tree), HM_ERR_ARG. */
 hm_status hm_assemble_rhs(hm_ctx ctx, int kind, double* f);
 
+/* Single-layer potential of the density sol at m evaluation points (the paper's
+ * accuracy metric evaluates it inside the domain):
+ *   out[p] = (1/4pi) sum_j sol_j int_{T_j} 1/|x_p - y| dy,
+ * each panel integral by the collapsed Gauss rule of the regular entries on T_j with its
+ * order from rho = |x_p - c_j| / h_j in the bands of A14 (reading A23); points must lie off
+ * the surface.  Direct sum over all N panels on every rank (collective-free).
+ * sol: length N, application order; points: m*3 xyz row-major; out: length m; each host or
+ * device.  Synchronous.  Errors: HM_ERR_STATE (no tree), HM_ERR_ARG. */
+hm_status hm_potential(hm_ctx ctx, const double* sol, int64_t m, const double* points, double* out);
+
 /* ---- introspection (host buffers) ---- */
 /* perm[s] = application index of internal position s (length N). */
 hm_status hm_get_perm(hm_ctx ctx, int32_t* perm);

@@ -991,3 +991,55 @@ void or_partition(const int64_t* cost, int64_t n, int p, int64_t* out) {
   while (r < p) out[r++] = n;
   out[p] = n;
 }
+
+/* ---- single-layer potential at evaluation points (reading A23) ------
+ * u(x) = (1/4pi) sum_j alpha_j int_{T_j} 1/|x - y| dy, alpha in application order.  Panel
+ * integral: collapsed Gauss n x n on T_j (the regular rule's panel factor), n by the ratio
+ * rho^2 = |x - c_j|^2 / h_j^2 in the bands of A14 (< 4: 6, < 16: 5, < 64: 4, else 3):
+ *   I_j(x) = (2 |T_j|) * sum_q w_q / sqrt(d2_q),  d2 = fma(dz,dz, fma(dy,dy, dx*dx)).
+ * Points must lie off the surface (the rule is not singular-aware). */
+double or_panel_potential(const double* x, const double* tri, int n) {
+  tri_t T = make_tri(tri, tri + 3, tri + 6);
+  reftab_t R = make_reftab(n);
+  double c[3], area, h;
+  panel_geometry(tri, tri + 3, tri + 6, c, &area, &h);
+  double inner = 0.0;
+  for (int q = 0; q < n * n; ++q) {
+    double y[3];
+    tri_point(&T, R.s[q], R.t[q], y);
+    double dx = x[0] - y[0], dy = x[1] - y[1], dz = x[2] - y[2];
+    double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    inner = inner + R.w[q] / sqrt(d2);
+  }
+  return inner * (2.0 * area);
+}
+
+void or_potential(const or_problem* P, const double* alpha, int64_t M, const double* X, double* out) {
+  reftab_t R[4];
+  for (int n = 3; n <= 6; ++n) R[n - 3] = make_reftab(n);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t p = 0; p < M; ++p) {
+    const double* x = X + 3 * p;
+    double u = 0.0;
+    for (int64_t j = 0; j < P->N; ++j) {
+      const double* c = P->cen + 3 * j;
+      double dx = x[0] - c[0], dy = x[1] - c[1], dz = x[2] - c[2];
+      double dc2 = (dx * dx + dy * dy) + dz * dz;
+      double h2 = P->h[j] * P->h[j];
+      int n = dc2 < 4.0 * h2 ? 6 : dc2 < 16.0 * h2 ? 5 : dc2 < 64.0 * h2 ? 4 : 3;
+      const int32_t* t = P->T + 3 * j;
+      tri_t T = make_tri(P->V + 3 * t[0], P->V + 3 * t[1], P->V + 3 * t[2]);
+      const reftab_t* Rn = &R[n - 3];
+      double inner = 0.0;
+      for (int q = 0; q < n * n; ++q) {
+        double y[3];
+        tri_point(&T, Rn->s[q], Rn->t[q], y);
+        double ex = x[0] - y[0], ey = x[1] - y[1], ez = x[2] - y[2];
+        double d2 = fma(ez, ez, fma(ey, ey, ex * ex));
+        inner = inner + Rn->w[q] / sqrt(d2);
+      }
+      u = u + alpha[j] * (inner * (2.0 * P->area[j]));
+    }
+    out[p] = u * 0.07957747154594767;
+  }
+}

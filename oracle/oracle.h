@@ -104,6 +104,11 @@ int or_gmres(const or_problem* P, const double* b, double* x, double tol, int re
 /* Leaf partition (A18): rank r of p owns leaves [out[r], out[r+1]). */
 void or_partition(const int64_t* cost, int64_t n, int p, int64_t* out);
 
+/* Single-layer potential (1/4pi) sum_j alpha_j int_{T_j} 1/|x-y| at M points X (M*3), alpha
+ * in application order (A23); and one panel's integral with order n. */
+void or_potential(const or_problem* P, const double* alpha, int64_t M, const double* X, double* out);
+double or_panel_potential(const double* x, const double* tri, int n);
+
 /* Work counters of the last or_assemble (kernel evaluations, entries). */
 void or_counters(const or_problem* P, double* out /* [evals_near, evals_aca, entries_near, entries_aca] */);
 

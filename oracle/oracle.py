@@ -50,6 +50,8 @@ def lib():
         L.or_entry_class.restype = i32; L.or_entry_class.argtypes = [P, i64, i64]
         L.or_selfterm_closed.restype = d; L.or_selfterm_closed.argtypes = [ptr, ptr, ptr]
         L.or_sauter_schwab.restype = d; L.or_sauter_schwab.argtypes = [i32, ptr, ptr, i32]
+        L.or_potential.argtypes = [P, ptr, i64, ptr, ptr]
+        L.or_panel_potential.restype = d; L.or_panel_potential.argtypes = [ptr, ptr, i32]
         L.or_ss_reference_monomial.restype = d
         L.or_ss_reference_monomial.argtypes = [i32, i32, i32, i32, i32, i32]
         L.or_regular_rule.restype = d; L.or_regular_rule.argtypes = [ptr, ptr, i32]
@@ -112,6 +114,13 @@ def regular_rule(tx, ty, n):
     a = np.ascontiguousarray(tx, dtype=np.float64).reshape(9)
     b = np.ascontiguousarray(ty, dtype=np.float64).reshape(9)
     return lib().or_regular_rule(_p(a), _p(b), n)
+
+
+def panel_potential(x, tri, n):
+    """int_T 1/|x - y| dy by the collapsed Gauss n x n rule of A23."""
+    a = np.ascontiguousarray(x, dtype=np.float64).reshape(3)
+    t = np.ascontiguousarray(tri, dtype=np.float64).reshape(9)
+    return lib().or_panel_potential(_p(a), _p(t), n)
 
 
 def aca_matrix(A, eps, kcap):
@@ -240,6 +249,14 @@ class Problem:
         y = np.zeros(self.N)
         lib().or_matvec(self._h, _p(x), _p(y))
         return y
+
+    def potential(self, alpha, X):
+        """(1/4pi) sum_j alpha_j int_{T_j} 1/|x - y| at the rows of X (M x 3), A23."""
+        a = np.ascontiguousarray(alpha, dtype=np.float64)
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, 3)
+        out = np.zeros(X.shape[0])
+        lib().or_potential(self._h, _p(a), X.shape[0], _p(X), _p(out))
+        return out
 
     def rhs(self, kind):
         f = np.zeros(self.N); lib().or_rhs(self._h, kind, _p(f)); return f

@@ -421,6 +421,27 @@ hm_status hm_solve(hm_ctx ctx, const double* rhs, double* sol, double tol, int* 
   });
 }
 
+hm_status hm_potential(hm_ctx ctx, const double* sol, int64_t m, const double* points, double* out) {
+  return guarded(ctx, [&](Context& C) {
+    need_tree(C);
+    if (!sol || m < 0 || (m > 0 && (!points || !out))) hm::fail(HM_ERR_ARG, "hm_potential: bad arguments");
+    if (m == 0) return;
+    Vec va(C, C.xapp, sol, nullptr);
+    const bool hp = !is_device_ptr(points), ho = !is_device_ptr(out);
+    const double* X = points;
+    if (hp) {
+      C.pot_x.alloc(3 * m);
+      HM_CUDA(cudaMemcpyAsync(C.pot_x.get(), points, 3 * m * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+      X = C.pot_x.get();
+    }
+    double* o = out;
+    if (ho) { C.pot_out.alloc(m); o = C.pot_out.get(); }
+    hm::potential(C, va.in(), m, X, o);
+    if (ho) HM_CUDA(cudaMemcpyAsync(out, o, m * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    HM_CUDA(cudaStreamSynchronize(C.stream));
+  });
+}
+
 hm_status hm_assemble_rhs(hm_ctx ctx, int kind, double* f) {
   return guarded(ctx, [&](Context& C) {
     need_tree(C);

@@ -270,7 +270,7 @@ struct Context {
   int64_t n_lr_small = 0, n_lr_large = 0;
 
   // work vectors (internal order)
-  DBuf<double> xin, yin, xapp, yapp, work;
+  DBuf<double> xin, yin, xapp, yapp, work, pot_x, pot_out;
   DBuf<double> krylov;         // GMRES basis / CG vectors
   DBuf<double> red;            // reduction scratch
   double* h_red = nullptr;     // pinned host scratch for scalar read-back
@@ -325,6 +325,8 @@ void allreduce_sum(Context& C, double* buf, int64_t n);
 // entries (entry.cu)
 void eval_entries(Context& C, int64_t n, const int64_t* d_pairs, double* d_out);
 void assemble_rhs(Context& C, int kind, double* f_app);
+// potential.cu
+void potential(Context& C, const double* alpha_app, int64_t M, const double* X_dev, double* out_dev);
 void upload_quadrature_tables();
 void quadrature_table_host(int n, double* nodes, double* weights);
 

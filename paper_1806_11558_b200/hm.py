@@ -56,6 +56,7 @@ def lib():
             "hm_matvec": [vp, vp, vp],
             "hm_solve": [vp, vp, vp, d, C.POINTER(i32), C.POINTER(d)],
             "hm_assemble_rhs": [vp, i32, vp],
+            "hm_potential": [vp, vp, i64, vp, vp],
             "hm_get_perm": [vp, vp],
             "hm_get_codes": [vp, vp],
             "hm_get_leaves": [vp, i32, C.POINTER(i64), vp, C.POINTER(i64), C.POINTER(i64)],
@@ -157,6 +158,10 @@ def hm_assemble_rhs(ctx, kind, f):
     _check(ctx, lib().hm_assemble_rhs(ctx, int(kind), _ptr(f)))
 
 
+def hm_potential(ctx, sol, points, out):
+    _check(ctx, lib().hm_potential(ctx, _ptr(sol), int(points.shape[0]), _ptr(points), _ptr(out)))
+
+
 def hm_get_stats(ctx) -> dict:
     buf = C.create_string_buffer(1 << 16)
     _check(ctx, lib().hm_get_stats(ctx, buf, len(buf)))
@@ -219,6 +224,13 @@ class HMatrix:
         if out is None:
             out = np.empty(self.N)
         hm_assemble_rhs(self.ctx, kind, out)
+        return out
+
+    def potential(self, sol, points, out=None):
+        """Single-layer potential of sol (application order) at points (m x 3)."""
+        if out is None:
+            out = points.new_empty(points.shape[0]) if hasattr(points, "new_empty") else np.empty(points.shape[0])
+        hm_potential(self.ctx, sol, points, out)
         return out
 
     # ---- introspection (host arrays) ----

@@ -244,3 +244,28 @@ def test_c3_full_size_sampled_rows(O, torch_cuda):
     st = H.stats()
     assert st["aca_overflow"] == 0 or st["k_max_seen"] <= 64
     H.close()
+
+
+def test_potential_parity_and_sphere_closed_form(O, torch_cuda, c2):
+    """hm_potential (A23): equal to the oracle's potential to 1e-12 for a seeded
+    density on C1; and for the GPU GMRES solution of the paper's RHS on C2 the interior
+    potential approaches the closed form f = 4x^2 - 3y^2 - z^2."""
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((64, 3)); X /= np.linalg.norm(X, axis=1)[:, None]
+    X *= rng.uniform(0.0, 0.6, size=(64, 1))
+    V1, T1 = icosphere(3)
+    H1 = _gpu(V1, T1)
+    R1 = O.Problem(V1, T1)
+    a = seeded_vector(T1.shape[0], 6)
+    ug = H1.potential(a, X)                                        # host buffers
+    uo = R1.potential(a, X)
+    assert np.linalg.norm(ug - uo) <= 1e-12 * np.linalg.norm(uo)
+    ud = H1.potential(torch_cuda.from_numpy(a).cuda(), torch_cuda.from_numpy(X).cuda())   # device buffers
+    assert np.linalg.norm(ud.cpu().numpy() - uo) <= 1e-12 * np.linalg.norm(uo)
+    H1.close()
+    V, T, H, R = c2
+    f = torch_cuda.from_numpy(H.assemble_rhs(1)).cuda()
+    sol, it, rr = H.solve(f, 1e-10)
+    u = H.potential(sol, torch_cuda.from_numpy(X).cuda()).cpu().numpy()
+    exact = 4 * X[:, 0] ** 2 - 3 * X[:, 1] ** 2 - X[:, 2] ** 2
+    assert np.abs(u - exact).max() < 2e-6 * 8        # L=5: ~8x below L=4 (1.3e-5, oracle pin)
