@@ -102,6 +102,9 @@ const char* hm_last_error(hm_ctx ctx);
  *   "mv_kernel"    small-leaf matvec pipeline: 4 (default) two CTA rings per SM, 2 x 48 KiB
  *                  stages each; 1 one ring of 4 x 48 KiB; 2 / 3 one ring of 8 x 24 / 6 x 32
  *                  KiB; 0 per-warp rings of 2 x 13 KiB.  Re-plans the matvec if set up.
+ *   "mv_large_u"   large low-rank U phase: 1 (default) 8 rows per lane in registers per tile,
+ *                  0 two rows per pass
+ *   "mv_large_v"   large low-rank V phase tiles: 1 (default) 16 columns x 1024 rows, 0 8 x 2048
  *   "mv_profile"   1: accumulate producer/consumer wait and work cycles of the CTA-ring
  *                  matvec (hm_get_stats "mv_prof_cycles"); diagnostic
  *   "mv_scramble"  1: DIAGNOSTIC ONLY, wrong products: spread the row bases of the CTA-ring

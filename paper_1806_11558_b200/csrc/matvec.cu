@@ -446,6 +446,107 @@ __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ 
   }
 }
 
+// Variant (option "mv_large_v" = 1): tile = (block, 16 columns l0.., 1024 rows j0..); all 16
+// column sums in registers, two rows per lane per pass (32 independent loads), one halving
+// butterfly for the 16 sums, one atomic per column.
+template <int KB>
+__device__ __forceinline__ void warp_reduce_halving(double (&v)[KB], int lane) {
+  constexpr int LV = KB == 16 ? 4 : 3;
+#pragma unroll
+  for (int lvl = 0; lvl < LV; ++lvl) {
+    const int o = 16 >> lvl, half = (KB >> 1) >> lvl;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < KB / 2; ++i)
+      if (i < half) {
+        const double send = up ? v[i] : v[i + half];
+        const double keep = up ? v[i + half] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+  }
+#pragma unroll
+  for (int o = 16 >> LV; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+}
+
+__global__ void __launch_bounds__(256) k_mv_large_v16(const MvTileV* __restrict__ tiles, int64_t ntiles,
+                                                      const MvLarge* __restrict__ L, const double* __restrict__ pool,
+                                                      const double* __restrict__ x, double* __restrict__ tbuf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < ntiles; i += nw) {
+    const MvTileV T = tiles[i];
+    const MvLarge B = L[T.blk];
+    const int kc = min(16, B.k - T.l);
+    const double* V = pool + B.off + (int64_t)B.m * B.k + (int64_t)T.l * B.n;
+    const double* xs = x + B.clo;
+    double acc[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) acc[l] = 0.0;
+    for (int j = T.j0 + lane; j < T.j1; j += 64) {
+      const bool two = j + 32 < T.j1;
+      const double xa = __ldg(xs + j), xb = two ? __ldg(xs + j + 32) : 0.0;
+      double va[16], vb[16];
+#pragma unroll
+      for (int l = 0; l < 16; ++l) {
+        va[l] = l < kc ? __ldg(V + j + (int64_t)l * B.n) : 0.0;
+        vb[l] = (l < kc && two) ? __ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
+      }
+#pragma unroll
+      for (int l = 0; l < 16; ++l) acc[l] = __fma_rn(vb[l], xb, __fma_rn(va[l], xa, acc[l]));
+    }
+    warp_reduce_halving<16>(acc, lane);
+    // lane L holds column 8*b4 + 4*b3 + 2*b2 + b1 (two lanes per column)
+    const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    if ((lane & 1) == 0 && col < kc) atomicAdd(tbuf + B.toff + T.l + col, acc[0]);
+  }
+}
+
+// Variant (option "mv_large_u" = 1): each lane keeps all 8 of its rows of the 256-row tile in
+// registers; per column l one broadcast t_l and 8 independent loads of U.
+__global__ void __launch_bounds__(256) k_mv_large_u8(const MvTileU* __restrict__ tiles, int64_t ntiles,
+                                                     const MvLarge* __restrict__ L, const double* __restrict__ pool,
+                                                     const double* __restrict__ tbuf, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < ntiles; i += nw) {
+    const MvTileU T = tiles[i];
+    const MvLarge B = L[T.blk];
+    const double* U = pool + B.off + T.t0 + lane;
+    const double* tl = tbuf + B.toff;
+    const int rows = T.t1 - T.t0;
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    int l = 0;
+    for (; l + 1 < B.k; l += 2) {
+      const double ta = __ldg(tl + l), tb = __ldg(tl + l + 1);
+      const double* Ua = U + (int64_t)l * B.m;
+      const double* Ub = Ua + B.m;
+      double ua[8], ub[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const bool ok = lane + 32 * q < rows;
+        ua[q] = ok ? __ldg(Ua + 32 * q) : 0.0;
+        ub[q] = ok ? __ldg(Ub + 32 * q) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = __fma_rn(ub[q], tb, __fma_rn(ua[q], ta, acc[q]));
+    }
+    if (l < B.k) {
+      const double ta = __ldg(tl + l);
+      const double* Ua = U + (int64_t)l * B.m;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (lane + 32 * q < rows) acc[q] = __fma_rn(__ldg(Ua + 32 * q), ta, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (lane + 32 * q < rows) atomicAdd(y + B.rlo + T.t0 + lane + 32 * q, acc[q]);
+  }
+}
+
 // dense blocks that do not fit a stage (large leaf_size only): warp per block, direct loads
 __global__ void k_mv_dense_direct(const MvLarge* __restrict__ L, int64_t nl, const double* __restrict__ store,
                                   const double* __restrict__ x, double* __restrict__ y) {
@@ -677,10 +778,11 @@ void plan_matvec(Context& C) {
     while (g + 1 < G) W.cta[++g] = (int32_t)nbat;
   }
   // tiles of the large low-rank blocks
+  const int vcols = C.mv_large_v == 1 ? 16 : 8, vrows = C.mv_large_v == 1 ? 1024 : 2048;
   size_t ntv = 0, ntu = 0;
   for (size_t i = 0; i < nlarge; ++i) {
     const MvLarge& B = W.large[i];
-    ntv += (size_t)((B.k + 7) / 8) * ((B.n + 2047) / 2048);
+    ntv += (size_t)((B.k + vcols - 1) / vcols) * ((B.n + vrows - 1) / vrows);
     ntu += (size_t)((B.m + 255) / 256);
   }
   W.tv.resize(ntv);
@@ -689,8 +791,8 @@ void plan_matvec(Context& C) {
     size_t a = 0, c = 0;
     for (size_t i = 0; i < nlarge; ++i) {
       const MvLarge& B = W.large[i];
-      for (int l0 = 0; l0 < B.k; l0 += 8)
-        for (int j0 = 0; j0 < B.n; j0 += 2048) W.tv[a++] = MvTileV{(int32_t)i, l0, j0, std::min(B.n, j0 + 2048)};
+      for (int l0 = 0; l0 < B.k; l0 += vcols)
+        for (int j0 = 0; j0 < B.n; j0 += vrows) W.tv[a++] = MvTileV{(int32_t)i, l0, j0, std::min(B.n, j0 + vrows)};
       for (int t0 = 0; t0 < B.m; t0 += 256) W.tu[c++] = MvTileU{(int32_t)i, t0, std::min(B.m, t0 + 256), 0};
     }
   }
@@ -792,11 +894,19 @@ void matvec_internal(Context& C, const double* x_int, double* y_int) {
     HM_CHECK_LAUNCH();
   }
   if (C.mv_n_tiles_v) {
-    k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
-                                          C.mv_tbuf.get());
+    if (C.mv_large_v == 1)
+      k_mv_large_v16<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
+                                              C.mv_tbuf.get());
+    else
+      k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
+                                            C.mv_tbuf.get());
     HM_CHECK_LAUNCH();
-    k_mv_large_u<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
-                                          C.mv_tbuf.get(), y_int);
+    if (C.mv_large_u == 1)
+      k_mv_large_u8<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
+                                             C.mv_tbuf.get(), y_int);
+    else
+      k_mv_large_u<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
+                                            C.mv_tbuf.get(), y_int);
     HM_CHECK_LAUNCH();
   }
   ks.reset();

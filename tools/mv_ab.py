@@ -22,7 +22,7 @@ st = H.stats()
 x = torch.randn(N, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(0))
 flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 ys = {}
-for kind in (1, 4, 2, 1, 4):
+for kind in (4, 1, 4):
     H.set_option("mv_kernel", kind)
     ts = []
     for r in range(23):
@@ -40,6 +40,20 @@ for kind in (1, 4, 2, 1, 4):
     print(json.dumps({"config": cfg, "mv_kernel": kind, "ms": round(ms, 4),
                       "GBps": round((st["stored_bytes"] + 40 * N) / (ms * 1e-3) / 1e9, 1),
                       "mv_batches": H.stats()["mv_batches"], "mv_segs": H.stats()["mv_segs"]}), flush=True)
+for lu, lv in ((1, 0), (0, 0), (1, 1), (1, 0), (1, 1)):
+    H.set_option("mv_kernel", 4)
+    H.set_option("mv_large_u", lu)
+    H.set_option("mv_large_v", lv)
+    ts = []
+    for r in range(23):
+        flush.fill_(r); torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); yl = H.matvec(x); b.record(); b.synchronize()
+        if r >= 3: ts.append(a.elapsed_time(b))
+    print(json.dumps({"mv_kernel": 4, "mv_large_u": lu, "mv_large_v": lv, "ms": round(statistics.median(ts), 4),
+                      "rel_diff": (torch.linalg.norm(yl - ys[4]) / torch.linalg.norm(ys[4])).item()}))
+H.set_option("mv_large_u", 1)
+H.set_option("mv_large_v", 0)
 H.set_option("mv_kernel", 1)
 H.set_option("mv_scramble", 1)
 for r in range(23):
