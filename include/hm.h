@@ -104,6 +104,8 @@ const char* hm_last_error(hm_ctx ctx);
  *                  KiB; 0 per-warp rings of 2 x 13 KiB.  Re-plans the matvec if set up.
  *   "mv_large_u"   large low-rank U phase: 1 (default) 8 rows per lane in registers per tile,
  *                  0 two rows per pass
+ *   "mv_small_max" low-rank leaves up to this many bytes (default 16384) go through the
+ *                  shared-memory pipeline, larger ones through the large-block kernels
  *   "mv_large_v"   large low-rank V phase tiles: 1 (default) 16 columns x 1024 rows, 0 8 x 2048
  *   "mv_profile"   1: accumulate producer/consumer wait and work cycles of the CTA-ring
  *                  matvec (hm_get_stats "mv_prof_cycles"); diagnostic

@@ -309,6 +309,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
       if (v == 1) { C.mv_prof.alloc(4); HM_CUDA(cudaMemsetAsync(C.mv_prof.get(), 0, 32, C.stream)); }
       else C.mv_prof.release();
     }
+    else if (k == "mv_small_max") { if (v < 0 || v > 49152) bad(); C.mv_small_max = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_large_u") { if (v != 0 && v != 1) bad(); C.mv_large_u = (int)v; }
     else if (k == "mv_large_v") { if (v != 0 && v != 1) bad(); C.mv_large_v = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_scramble") { if (v != 0 && v != 1) bad(); C.mv_scramble = (int)v; }

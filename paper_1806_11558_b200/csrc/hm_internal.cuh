@@ -264,6 +264,7 @@ struct Context {
   DBuf<double> mv_tbuf;
   int mv_grid = 0;
   DBuf<unsigned long long> mv_prof;   // option "mv_profile": [producer empty-wait, consumer full-wait, consumer work] cycles
+  int mv_small_max = 16384;    // option "mv_small_max": low-rank leaves up to this many bytes go through the pipeline
   int mv_large_u = 1;          // option "mv_large_u": 1 all 8 rows of the tile per lane (default), 0 two rows per pass
   int mv_large_v = 1;          // option "mv_large_v": 1 16 columns x 1024 rows tiles (default), 0 8 x 2048
   int mv_scramble = 0;         // diagnostic option "mv_scramble" (wrong results): see k_mv_batched

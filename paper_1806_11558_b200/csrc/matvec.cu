@@ -718,7 +718,7 @@ void plan_matvec(Context& C) {
         const Quad& q = C.h_adm[C.adm_begin + b];
         const int m = q.rhi - q.rlo, n = q.chi - q.clo, k = C.h_rank[b];
         const int64_t bytes = 8 * (int64_t)k * (m + n);
-        if (bytes <= std::min<int64_t>(kMvSmallMax, cap - 8 * n - 64) && m <= 2047 && n <= 2047 && k <= 1023)
+        if (bytes <= std::min<int64_t>(C.mv_small_max, cap - 8 * n - 64) && m <= 2047 && n <= 2047 && k <= 1023)
           P.items.push_back(Item{8 * C.h_foff[b], bytes, 1, q.rlo, q.clo, n,
                                  (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)});
         else

@@ -40,20 +40,20 @@ for kind in (4, 1, 4):
     print(json.dumps({"config": cfg, "mv_kernel": kind, "ms": round(ms, 4),
                       "GBps": round((st["stored_bytes"] + 40 * N) / (ms * 1e-3) / 1e9, 1),
                       "mv_batches": H.stats()["mv_batches"], "mv_segs": H.stats()["mv_segs"]}), flush=True)
-for lu, lv in ((1, 0), (0, 0), (1, 1), (1, 0), (1, 1)):
+for lu, lv, sm in ((1, 1, 16384), (1, 1, 24576), (1, 1, 32768), (1, 1, 40960), (1, 1, 16384), (1, 1, 32768)):
     H.set_option("mv_kernel", 4)
     H.set_option("mv_large_u", lu)
     H.set_option("mv_large_v", lv)
+    H.set_option("mv_small_max", sm)
     ts = []
     for r in range(23):
         flush.fill_(r); torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); yl = H.matvec(x); b.record(); b.synchronize()
         if r >= 3: ts.append(a.elapsed_time(b))
-    print(json.dumps({"mv_kernel": 4, "mv_large_u": lu, "mv_large_v": lv, "ms": round(statistics.median(ts), 4),
+    print(json.dumps({"mv_kernel": 4, "mv_large_u": lu, "mv_large_v": lv, "mv_small_max": sm, "ms": round(statistics.median(ts), 4),
                       "rel_diff": (torch.linalg.norm(yl - ys[4]) / torch.linalg.norm(ys[4])).item()}))
-H.set_option("mv_large_u", 1)
-H.set_option("mv_large_v", 0)
+H.set_option("mv_small_max", 16384)
 H.set_option("mv_kernel", 1)
 H.set_option("mv_scramble", 1)
 for r in range(23):
