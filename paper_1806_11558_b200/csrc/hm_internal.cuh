@@ -274,6 +274,7 @@ struct Context {
 
   // work vectors (internal order)
   DBuf<double> xin, yin, xapp, yapp, work, pot_x, pot_out;
+  DBuf<double> sh_x, sh_y, sh_sol;   // sharded Krylov (p > 1): gathered x, partial y, local solution
   DBuf<double> krylov;         // GMRES basis / CG vectors
   DBuf<double> red;            // reduction scratch
   double* h_red = nullptr;     // pinned host scratch for scalar read-back
@@ -317,7 +318,8 @@ void setup_nearfield(Context& C);
 void setup_aca(Context& C);
 // matvec.cu
 void plan_matvec(Context& C);
-void matvec_internal(Context& C, const double* x_int, double* y_int);   // y = H x (local part)
+void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce = true);   // y = H x (local
+                                                                                          // leaves; + global sum)
 void gather_perm(Context& C, const double* x_app, double* x_int);
 void scatter_perm(Context& C, const double* y_int, double* y_app);
 // solver.cu

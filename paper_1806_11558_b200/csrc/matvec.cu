@@ -851,7 +851,7 @@ void scatter_perm(Context& C, const double* y_int, double* y_app) {
 }
 
 // y_int = (local leaves of H) x_int, then summed over ranks
-void matvec_internal(Context& C, const double* x_int, double* y_int) {
+void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce) {
   cudaStream_t st = C.stream;
   // the staged x_sigma copies need a 16-B aligned x with one readable double past N (every
   // internal caller passes such a vector; anything else goes through an aligned copy)
@@ -910,7 +910,7 @@ void matvec_internal(Context& C, const double* x_int, double* y_int) {
     HM_CHECK_LAUNCH();
   }
   ks.reset();
-  if (C.world > 1) allreduce_sum(C, y_int, C.N);
+  if (C.world > 1 && reduce) allreduce_sum(C, y_int, C.N);
 }
 
 }  // namespace hm

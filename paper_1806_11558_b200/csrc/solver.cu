@@ -7,6 +7,7 @@
 // scalars and takes identical convergence decisions.  x0 = 0; stop at ||r|| <= tol ||b||.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 
 #include "entry.cuh"
@@ -105,21 +106,34 @@ __global__ void k_cg_p(double* __restrict__ p, const double* __restrict__ r, dou
     p[t] = r[t] + beta * p[t];
 }
 
+// Krylov vector layout.  One rank: the full internal-order vector.  p ranks: rank r owns the
+// slice [r S, r S + n) with S = ceil(N / p) (the last slice shorter); dot products are local
+// sums all-reduced over NCCL, and the matvec all-gathers x into a p*S buffer whose first N
+// entries are the internal-order x, applies the rank's leaves and reduce-scatters y back
+// into slices (same NVLink volume as the replicated all-reduce, but the orthogonalisation
+// work is split p ways).
+struct Layout {
+  int64_t n = 0, S = 0, off = 0;
+  bool sharded = false;
+};
+
 struct Red {
   Context& C;
+  const Layout& L;
   DBuf<double> part, out;
-  explicit Red(Context& c) : C(c) {}
-  // out[0..nv) = V[i]^T w on the device; returns device pointer
+  Red(Context& c, const Layout& l) : C(c), L(l) {}
+  // out[0..nv) = V[i]^T w (global) on the device; returns device pointer
   double* mdot(const double* Vb, int64_t ld, int nv, const double* w) {
     part.alloc((size_t)kRedBlocks * nv);
     out.alloc(nv + 8);
     { KScope ks_(C, KF_KRYLOV);
-    k_mdot<<<kRedBlocks, kRedThreads, 0, C.stream>>>(Vb, ld, nv, w, C.N, part.get());
+    k_mdot<<<kRedBlocks, kRedThreads, 0, C.stream>>>(Vb, ld, nv, w, L.n, part.get());
     }
     { KScope ks_(C, KF_KRYLOV);
     k_mdot_final<<<(nv + 127) / 128, 128, 0, C.stream>>>(part.get(), kRedBlocks, nv, out.get());
     }
     HM_CHECK_LAUNCH();
+    if (L.sharded) allreduce_sum(C, out.get(), nv);
     return out.get();
   }
   double dot(const double* a, const double* b) {
@@ -133,25 +147,30 @@ struct Red {
 
 unsigned vgrid(int64_t n) { return std::min<unsigned>(grid_for(n, 256), 148 * 16); }
 
-void apply(Context& C, const double* x, double* y) { matvec_internal(C, x, y); }
+void apply(Context& C, const Layout& L, const double* x, double* y) {
+  if (!L.sharded) { matvec_internal(C, x, y); return; }
+  HM_NCCL(ncclAllGather(x, C.sh_x.get(), (size_t)L.S, ncclDouble, C.comm, C.stream));
+  matvec_internal(C, C.sh_x.get(), C.sh_y.get(), /*reduce=*/false);
+  HM_NCCL(ncclReduceScatter(C.sh_y.get(), y, (size_t)L.S, ncclDouble, ncclSum, C.comm, C.stream));
+}
 
-double true_relres(Context& C, Red& R, const double* b, const double* x, double bn, double* tmp) {
-  apply(C, x, tmp);
+double true_relres(Context& C, const Layout& L, Red& R, const double* b, const double* x, double bn, double* tmp) {
+  apply(C, L, x, tmp);
   { KScope ks_(C, KF_KRYLOV);
-  k_sub<<<vgrid(C.N), 256, 0, C.stream>>>(b, tmp, tmp, C.N);
+  k_sub<<<vgrid(L.n), 256, 0, C.stream>>>(b, tmp, tmp, L.n);
   }
   HM_CHECK_LAUNCH();
   double rr = R.dot(tmp, tmp);
   return bn > 0 ? std::sqrt(rr) / bn : 0.0;
 }
 
-void cg(Context& C, const double* b, double* x, double tol, int* iters, double* relres) {
-  const int64_t N = C.N;
+void cg(Context& C, const Layout& L, const double* b, double* x, double tol, int* iters, double* relres) {
+  const int64_t N = L.n;
   cudaStream_t st = C.stream;
-  const int64_t ld = (N + 32) & ~int64_t(31);   // 256-B aligned vectors with slack (matvec x staging)
+  const int64_t ld = (L.S + 32) & ~int64_t(31);   // 256-B aligned vectors with slack (matvec x staging)
   C.krylov.alloc(3 * ld);
   double *r = C.krylov.get(), *p = r + ld, *Ap = p + ld;
-  Red R(C);
+  Red R(C, L);
   HM_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st));
   HM_CUDA(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
   HM_CUDA(cudaMemcpyAsync(p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -160,7 +179,7 @@ void cg(Context& C, const double* b, double* x, double tol, int* iters, double* 
   int it = 0;
   if (bn == 0.0) { *iters = 0; *relres = 0.0; return; }
   while (it < C.max_iter && std::sqrt(rr) > tol * bn) {
-    apply(C, p, Ap);
+    apply(C, L, p, Ap);
     const double pAp = R.dot(p, Ap);
     if (!(pAp > 0.0)) fail(HM_ERR_BREAKDOWN, "CG breakdown: p^T H p <= 0 at iteration " + std::to_string(it));
     const double alpha = rr / pAp;
@@ -178,18 +197,18 @@ void cg(Context& C, const double* b, double* x, double tol, int* iters, double* 
     ++it;
   }
   *iters = it;
-  *relres = true_relres(C, R, b, x, bn, Ap);
+  *relres = true_relres(C, L, R, b, x, bn, Ap);
 }
 
-void gmres(Context& C, const double* b, double* x, double tol, int* iters, double* relres) {
-  const int64_t N = C.N;
+void gmres(Context& C, const Layout& L, const double* b, double* x, double tol, int* iters, double* relres) {
+  const int64_t N = L.n;
   const int m = std::max(1, C.restart);
   cudaStream_t st = C.stream;
-  const int64_t ld = (N + 32) & ~int64_t(31);   // 256-B aligned basis vectors with slack (matvec x staging)
+  const int64_t ld = (L.S + 32) & ~int64_t(31);   // 256-B aligned basis vectors with slack (matvec x staging)
   C.krylov.alloc((size_t)(m + 2) * ld);
   double* Vb = C.krylov.get();
   double* w = Vb + (int64_t)(m + 1) * ld;
-  Red R(C);
+  Red R(C, L);
   DBuf<double> hdev, hsum;
   hdev.alloc(m + 8);
   std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), h(m + 1), h2(m + 1), y(m);
@@ -198,7 +217,7 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
   int total = 0;
   if (bn == 0.0) { *iters = 0; *relres = 0.0; return; }
   for (;;) {
-    apply(C, x, w);
+    apply(C, L, x, w);
     { KScope ks_(C, KF_KRYLOV);
     k_sub<<<vgrid(N), 256, 0, st>>>(b, w, w, N);
     }
@@ -215,7 +234,7 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
     int jend = 0;
     bool conv = false;
     for (int j = 0; j < m; ++j) {
-      apply(C, Vb + (int64_t)j * ld, w);
+      apply(C, L, Vb + (int64_t)j * ld, w);
       ++total;
       // CGS2
       double* d1 = R.mdot(Vb, ld, j + 1, w);
@@ -268,14 +287,39 @@ void gmres(Context& C, const double* b, double* x, double tol, int* iters, doubl
     if (total >= C.max_iter) break;
   }
   *iters = total;
-  *relres = true_relres(C, R, b, x, bn, w);
+  *relres = true_relres(C, L, R, b, x, bn, w);
 }
 
 }  // namespace
 
 void solve(Context& C, const double* rhs_int, double* sol_int, double tol, int* iters, double* relres) {
-  if (C.solver == 1) cg(C, rhs_int, sol_int, tol, iters, relres);
-  else gmres(C, rhs_int, sol_int, tol, iters, relres);
+  Layout L;
+  if (C.world == 1) {
+    L.n = L.S = C.N;
+    if (C.solver == 1) cg(C, L, rhs_int, sol_int, tol, iters, relres);
+    else gmres(C, L, rhs_int, sol_int, tol, iters, relres);
+    return;
+  }
+  // p ranks: sharded Krylov vectors (Layout), the replicated rhs is read in place
+  L.sharded = true;
+  L.S = (C.N + C.world - 1) / C.world;
+  L.off = std::min<int64_t>((int64_t)C.rank * L.S, C.N);
+  L.n = std::min<int64_t>(L.S, C.N - L.off);
+  const int64_t full = L.S * C.world;
+  if (C.sh_x.n < (size_t)full + 32) {
+    C.sh_x.alloc(full + 32);
+    C.sh_y.alloc(full + 32);
+    HM_CUDA(cudaMemsetAsync(C.sh_x.get(), 0, (full + 32) * sizeof(double), C.stream));
+    HM_CUDA(cudaMemsetAsync(C.sh_y.get(), 0, (full + 32) * sizeof(double), C.stream));   // padding stays 0
+  }
+  C.sh_sol.alloc(L.S + 32);
+  HM_CUDA(cudaMemsetAsync(C.sh_sol.get(), 0, (L.S + 32) * sizeof(double), C.stream));
+  if (C.solver == 1) cg(C, L, rhs_int + L.off, C.sh_sol.get(), tol, iters, relres);
+  else gmres(C, L, rhs_int + L.off, C.sh_sol.get(), tol, iters, relres);
+  // the full solution on every rank
+  HM_NCCL(ncclAllGather(C.sh_sol.get(), C.sh_x.get(), (size_t)L.S, ncclDouble, C.comm, C.stream));
+  HM_CUDA(cudaMemcpyAsync(sol_int, C.sh_x.get(), C.N * sizeof(double), cudaMemcpyDeviceToDevice, C.stream));
+  HM_CUDA(cudaStreamSynchronize(C.stream));
 }
 
 }  // namespace hm
