@@ -170,7 +170,8 @@ struct TreeWs {
   DBuf<Quad> admq, denq;
   DBuf<unsigned long long> ctr;
   DBuf<unsigned int> bad;
-  DBuf<int64_t> cost, pref;
+  DBuf<int64_t> cost, pref, bounds;
+  DBuf<unsigned long long> bout;
   DBuf<char> tmp;
 };
 struct EntryBatchWork;   // entry_batch.cuh

@@ -697,7 +697,8 @@ void plan_matvec(Context& C) {
   W.parts.resize(T);
   const int64_t* hoff = W.hoff.data();
   const bool wr = C.mv_kind == 0;
-  const int64_t cap = wr ? kWrStageBytes : (C.mv_kind == 1 || C.mv_kind == 4) ? 48 * 1024 : C.mv_kind == 2 ? 24 * 1024 : 32 * 1024;
+  const int64_t cap = wr ? kWrStageBytes : (C.mv_kind == 1 || C.mv_kind == 4) ? 48 * 1024
+                   : (C.mv_kind == 2 || C.mv_kind == 6) ? 24 * 1024 : 32 * 1024;
   auto work = [&](int t) {
     PlanPart& P = W.parts[t];
     P.clear();
@@ -762,7 +763,7 @@ void plan_matvec(Context& C) {
   // one persistent CTA per SM (warp rings)
   int sms = 148;
   HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, C.device));
-  const int G = wr ? sms * kWrWarps : std::max(1, std::min<int>(C.mv_kind == 4 ? 2 * sms : sms, (int)nbat));
+  const int G = wr ? sms * kWrWarps : std::max(1, std::min<int>(C.mv_kind >= 4 ? 2 * sms : sms, (int)nbat));
   W.cta.resize(G + 1);
   {
     double tot = 0;
@@ -834,6 +835,10 @@ void plan_matvec(Context& C) {
                                  256 + 6 * 32 * 1024));
     HM_CUDA(cudaFuncSetAttribute(k_mv_batched<2, 48 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  256 + 2 * 48 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<3, 32 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 3 * 32 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<4, 24 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 4 * 24 * 1024));
     HM_CUDA(cudaFuncSetAttribute(k_mv_warps, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  256 + kWrWarps * kWrStages * kWrStageBytes));
     attr = true;
@@ -875,6 +880,14 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
           (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
     } else if (C.mv_kind == 2) {
       k_mv_batched<8, 24 * 1024><<<C.mv_grid, kMvThreads, 256 + 8 * 24 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
+    } else if (C.mv_kind == 5) {
+      k_mv_batched<3, 32 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 3 * 32 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
+    } else if (C.mv_kind == 6) {
+      k_mv_batched<4, 24 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 4 * 24 * 1024, st>>>(
           C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
           (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
     } else if (C.mv_kind == 4) {

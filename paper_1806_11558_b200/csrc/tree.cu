@@ -269,6 +269,16 @@ void grow_copy(DBuf<Quad>& q, DBuf<uint64_t>& k, int64_t used, int64_t need, cud
   q.p = nq; q.n = cap; k.p = nk; k.n = cap;
 }
 
+// first leaf whose exclusive cost prefix is >= bound[b] (lower_bound on the non-decreasing
+// prefix), for the two bounds of this rank; out preset to n
+__global__ void k_prefix_bounds(const int64_t* __restrict__ pref, int64_t n, const int64_t* __restrict__ bound,
+                                unsigned long long* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int b = 0; b < 2; ++b)
+    if (pref[i] >= bound[b] && (i == 0 || pref[i - 1] < bound[b])) atomicMin(&out[b], (unsigned long long)i);
+}
+
 void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_t& begin, int64_t& end,
                     DBuf<char>& tmp) {
   if (C.world == 1 || n == 0) { begin = 0; end = n; return; }
@@ -279,18 +289,25 @@ void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_
   cub_call(tmp, [&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, cost.get(), pref.get(), n, C.stream);
   });
-  std::vector<int64_t> hp(n), hc(1);
-  HM_CUDA(cudaMemcpyAsync(hp.data(), pref.get(), n * sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
-  HM_CUDA(cudaMemcpyAsync(hc.data(), cost.get() + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
+  int64_t h[2];
+  HM_CUDA(cudaMemcpyAsync(&h[0], pref.get() + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
+  HM_CUDA(cudaMemcpyAsync(&h[1], cost.get() + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
   HM_CUDA(cudaStreamSynchronize(C.stream));
-  const int64_t total = hp[n - 1] + hc[0];
-  auto first_at = [&](int r) -> int64_t {   // first leaf whose exclusive prefix >= floor(rC/p)
-    if (r >= C.world) return n;
-    int64_t bound = (int64_t)(((__int128)r * total) / C.world);
-    return std::lower_bound(hp.begin(), hp.end(), bound) - hp.begin();
-  };
-  begin = C.rank == 0 ? 0 : first_at(C.rank);
-  end = C.rank + 1 >= C.world ? n : first_at(C.rank + 1);
+  const int64_t total = h[0] + h[1];
+  auto bound_of = [&](int r) -> int64_t { return (int64_t)(((__int128)r * total) / C.world); };
+  // rank r owns the leaves whose exclusive prefix lies in [floor(rC/p), floor((r+1)C/p)) (A18)
+  int64_t hb[2] = {bound_of(C.rank), bound_of(C.rank + 1)};
+  unsigned long long ho[2] = {(unsigned long long)n, (unsigned long long)n};
+  C.tws.bounds.alloc(2);
+  C.tws.bout.alloc(2);
+  HM_CUDA(cudaMemcpyAsync(C.tws.bounds.get(), hb, sizeof(hb), cudaMemcpyHostToDevice, C.stream));
+  HM_CUDA(cudaMemcpyAsync(C.tws.bout.get(), ho, sizeof(ho), cudaMemcpyHostToDevice, C.stream));
+  k_prefix_bounds<<<grid_for(n, 256), 256, 0, C.stream>>>(pref.get(), n, C.tws.bounds.get(), C.tws.bout.get());
+  HM_CHECK_LAUNCH();
+  HM_CUDA(cudaMemcpyAsync(ho, C.tws.bout.get(), sizeof(ho), cudaMemcpyDeviceToHost, C.stream));
+  HM_CUDA(cudaStreamSynchronize(C.stream));
+  begin = C.rank == 0 ? 0 : (int64_t)ho[0];
+  end = C.rank + 1 >= C.world ? n : (int64_t)ho[1];
 }
 
 }  // namespace
