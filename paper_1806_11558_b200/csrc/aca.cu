@@ -38,7 +38,7 @@ struct AcaWork {
   DBuf<AcaState> state;
   DBuf<int32_t> owned, piv, act, flag, pos, big, rtab, ctab;
   DBuf<int64_t> rsz, csz, rpre, cpre;
-  DBuf<double> Uw, Vw;
+  DBuf<double> ws;      // chunk workspace: [U: m*kws per block | V: n*kws per block]
   DBuf<uint32_t> bmap;
   DBuf<char> tmp;
   DBuf<unsigned long long> ev, cnt;
@@ -534,7 +534,9 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   W.ovf.alloc(nb); W.novf.alloc(1); W.h_tot.resize(4);
   if (nbig) HM_CUDA(cudaMemcpyAsync(W.big.get(), hbig.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   W.rsz.alloc(nb + 1); W.csz.alloc(nb + 1); W.rpre.alloc(nb + 1); W.cpre.alloc(nb + 1);
-  W.Uw.alloc(uo); W.Vw.alloc(vo); W.bmap.alloc(bo);
+  W.ws.alloc(uo + vo); W.bmap.alloc(bo);
+  double* const Uw = W.ws.get();          // one workspace buffer: U columns, then V columns
+  double* const Vw = Uw + uo;
   HM_CUDA(cudaMemcpyAsync(W.blk.get(), hb.data(), nb * sizeof(AcaBlk), cudaMemcpyHostToDevice, st));
   W.h_idsp.resize(nb);
   std::memcpy(W.h_idsp.data(), ids.data(), nb * sizeof(int32_t));
@@ -580,25 +582,25 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     HM_CHECK_LAUNCH();
     k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.cpre.get(), nact, 0, W.ctab.get());
     HM_CHECK_LAUNCH();
-    aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(), nb, W.Uw.get(), W.Vw.get()},
+    aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(), nb, Uw, Vw},
              tot[0], W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_pivot<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, W.Vw.get(),
+    k_aca_pivot<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, Vw,
                                                           W.bmap.get());
     HM_CHECK_LAUNCH();
     if (nbig) {
-      k_aca_pivot_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), W.Vw.get(), W.bmap.get());
+      k_aca_pivot_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Vw, W.bmap.get());
       HM_CHECK_LAUNCH();
     }
     ks.reset();
-    aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(), nb, W.Uw.get(), W.Vw.get()},
+    aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(), nb, Uw, Vw},
              tot[1], W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_update<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, W.Uw.get(),
-                                                           W.Vw.get(), W.bmap.get(), W.piv.get(), kws, C.eps_aca);
+    k_aca_update<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, Uw,
+                                                           Vw, W.bmap.get(), W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();
     if (nbig) {
-      k_aca_update_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), W.Uw.get(), W.Vw.get(),
+      k_aca_update_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Uw, Vw,
                                                        W.bmap.get(), W.piv.get(), kws, C.eps_aca);
       HM_CHECK_LAUNCH();
     }
@@ -623,7 +625,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   C.fpool.ensure((base + add) * sizeof(double) + 64);
   C.fpool.used = (base + add) * sizeof(double);
   k_aca_store<<<(unsigned)nb, 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(), base,
-                                           W.Uw.get(), W.Vw.get(), (double*)C.fpool.base, C.foff.get(), C.frank.get());
+                                           Uw, Vw, (double*)C.fpool.base, C.foff.get(), C.frank.get());
   HM_CHECK_LAUNCH();
   if (nov) {
     const size_t o0 = overflow.size();
@@ -660,7 +662,7 @@ void setup_aca(Context& C) {
   C.frank.alloc(nb + 1);
   HM_CUDA(cudaMemsetAsync(C.frank.get(), 0, (nb + 1) * sizeof(int32_t), st));
   C.fpool.used = 0;
-  C.aca_steps = 0; C.aca_chunks = 0; C.aca_overflow = 0;
+  C.aca_steps = 0; C.aca_chunks = 0; C.aca_overflow = 0; C.aca_releases = 0;
   for (double& t : C.times.aca_phase_ms) t = 0;
   C.entries_aca = 0;
   if (nb == 0) { C.factor_doubles = 0; C.evals_aca = 0; return; }
@@ -694,21 +696,37 @@ void setup_aca(Context& C) {
   // workspace per chunk: the option, capped by the device memory left at the start of the chunk
   // (the factor pool grows by ~k_mean/KWS of the workspace per chunk, so 0.45 of what is free
   // plus the current workspace leaves room for it)
+  // 4 GiB stay free for what follows setup (GMRES basis: (restart+2) N doubles, matvec plan)
+  constexpr double kAcaReserve = 4.0 * 1073741824.0;
+  // Free device memory is queried once (cudaMemGetInfo costs ~20 ms with a large VMM pool
+  // mapped) and then tracked: minus the factor pool's newly mapped bytes and the workspace's
+  // growth, plus what a workspace release returns.
+  size_t free0 = 0, total0 = 0;
+  HM_CUDA(cudaMemGetInfo(&free0, &total0));
+  const double mapped0 = (double)C.fpool.mapped;
+  const double ws0 = 8.0 * (double)W.ws.n;
+  // Chunk budget b (workspace bytes of one chunk): the workspace must fit in `room` (free
+  // memory + the current workspace), and a chunk's factor output (<= b) must fit in the pool's
+  // mapped-but-unused slack plus the memory beside the workspace.  In repeated setups the
+  // pool stays mapped (slack ~ all factors), so chunks can use most of the free memory.
+  // The allocated workspace is kept (no multi-GB free/malloc, tens to hundreds of ms) while
+  // it is at most twice the budget and the factor growth still fits in the free memory.
   auto chunk_budget = [&]() {
-    size_t free_b = 0, total_b = 0;
-    HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const double ws = 8.0 * (double)(W.Uw.n + W.Vw.n);
-    const double b = std::min(C.aca_chunk_mb * 1048576.0, 0.45 * ((double)free_b + ws));
-    // hysteresis: keep the allocated workspace while it is at most twice the budget (a chunk
-    // then uses at most the budget of it); re-allocating multi-GB buffers costs tens of ms
-    // and while the free memory still holds a full chunk's factor output (<= the budget)
-    if (ws > 2.0 * b || (double)free_b < b) { W.Uw.release(); W.Vw.release(); }
-    return std::max(b, 64.0 * 1048576.0);
+    const auto tb0 = clk::now();
+    struct Acc { double& t; clk::time_point a; ~Acc() { t += std::chrono::duration<double, std::milli>(clk::now() - a).count(); } };
+    Acc acc_{C.times.aca_phase_ms[7], tb0};
+    const double ws = 8.0 * (double)W.ws.n;
+    const double free_b = std::max(0.0, (double)free0 - ((double)C.fpool.mapped - mapped0) - (ws - ws0));
+    const double slack = std::max(0.0, (double)C.fpool.mapped - (double)C.fpool.used);
+    const double room = std::max(0.0, free_b + ws - kAcaReserve);   // keep room for the solve's Krylov basis
+    double b = std::min(C.aca_chunk_mb * 1048576.0, 0.9 * room);
+    if (b - slack > room - b) b = 0.5 * (room + slack);
+    b = std::max(std::min(b, 0.9 * room), 64.0 * 1048576.0);
+    if (ws > 2.0 * b || (ws > b && b - slack > free_b)) { W.ws.release(); C.aca_releases++; }
+    else if (ws >= 0.5 * b) b = std::min(b, ws);     // reuse the allocated workspace as it is
+    return b;
   };
-  C.times.aca_phase_ms[6] = ms_since(t0);
-  const auto tb = clk::now();
   double budget = chunk_budget();
-  C.times.aca_phase_ms[7] = ms_since(tb);
   std::vector<int32_t>& ids = W.h_ids;
   std::vector<int32_t> overflow;
   ids.clear();

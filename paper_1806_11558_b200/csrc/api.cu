@@ -591,7 +591,7 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
       << ",\"k_mean\":" << (C.h_rank.empty() ? 0.0 : ksum / C.h_rank.size()) << ",\"k_min\":" << kmin
       << ",\"k_max_seen\":" << kmax << ",\"evals_near\":" << C.evals_near << ",\"evals_aca\":" << C.evals_aca
       << ",\"entries_aca\":" << C.entries_aca << ",\"aca_steps\":" << C.aca_steps << ",\"aca_chunks\":" << C.aca_chunks
-      << ",\"aca_overflow\":" << C.aca_overflow << ",\"tree_ms\":" << C.times.tree_ms << ",\"tree_phase_ms\":[" << C.times.tree_phase_ms[0] << ","
+      << ",\"aca_overflow\":" << C.aca_overflow << ",\"aca_releases\":" << C.aca_releases << ",\"tree_ms\":" << C.times.tree_ms << ",\"tree_phase_ms\":[" << C.times.tree_phase_ms[0] << ","
       << C.times.tree_phase_ms[1] << "," << C.times.tree_phase_ms[2] << "," << C.times.tree_phase_ms[3] << ","
       << C.times.tree_phase_ms[4] << "," << C.times.tree_phase_ms[5] << "]"
       << ",\"plan_phase_ms\":[" << C.times.plan_phase_ms[0] << "," << C.times.plan_phase_ms[1] << ","

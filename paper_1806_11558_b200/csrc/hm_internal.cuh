@@ -252,7 +252,7 @@ struct Context {
   std::vector<int64_t> h_foff;
   int64_t dense_doubles = 0, factor_doubles = 0;
   double evals_near = 0, evals_aca = 0, entries_aca = 0;
-  int aca_steps = 0, aca_chunks = 0, aca_overflow = 0;
+  int aca_steps = 0, aca_chunks = 0, aca_overflow = 0, aca_releases = 0;
 
   // matvec plan (matvec.cu)
   DBuf<MvBatch> mv_batches;
