@@ -308,14 +308,16 @@ def _run_gpu(args, rank, world, local, dev, stream):
         roof = {"kernel": "entry evaluation (k_eval_* near-field + ACA rows/columns)", "bound": "alu",
                 "achieved": round(eval_rate / 1e9, 2), "peak": round(eval_peak / 1e9, 2), "unit": "Geval/s",
                 "frac": round(eval_rate / eval_peak, 4),
-                "traffic": traffic.get("eval_bytes_per_eval") if traffic else None,
+                "traffic": traffic.get("eval_bytes_per_launch") if traffic else None,
+                "traffic_note": traffic.get("eval_source") if traffic else None,
                 "peak_source": f"unit counts: {FP64_LANES_PER_SM} FP64 instr/clk/SM x {SMS} SMs x sm_max clock / "
                                f"{DP_INSTR_PER_EVAL} FP64 instr per evaluation (SASS)",
                 "share_of_step": round(eval_ms / ms, 4)}
     else:
         roof = {"kernel": "H-matvec (k_mv_batched + k_mv_large_v/u)", "bound": "hbm", "achieved": round(mv_gbs_live, 1),
                 "peak": hbm, "unit": "GB/s", "frac": round(mv_gbs_live / hbm, 4),
-                "traffic": traffic.get("matvec_bytes_per_launch") if traffic else None, "peak_source": hbm_src,
+                "traffic": traffic.get("matvec_bytes_per_launch") if traffic else None,
+                "traffic_note": traffic.get("matvec_source") if traffic else None, "peak_source": hbm_src,
                 "share_of_step": round(mv_kern_ms_step / ms, 4)}
     matvec_roof = {"bound": "hbm", "achieved": round(mv_gbs, 1), "peak": hbm, "unit": "GB/s",
                    "frac": round(mv_gbs / hbm, 4), "alg_bytes_per_launch": int(alg_bytes_rank), "peak_source": hbm_src,
