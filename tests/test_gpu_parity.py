@@ -269,3 +269,31 @@ def test_potential_parity_and_sphere_closed_form(O, torch_cuda, c2):
     u = H.potential(sol, torch_cuda.from_numpy(X).cuda()).cpu().numpy()
     exact = 4 * X[:, 0] ** 2 - 3 * X[:, 1] ** 2 - X[:, 2] ** 2
     assert np.abs(u - exact).max() < 2e-6 * 8        # L=5: ~8x below L=4 (1.3e-5, oracle pin)
+
+
+def test_lobed_surface_full_path(O, torch_cuda):
+    """The C5 stand-in geometry (non-convex lobed surface scaled to the gearwheel's box,
+    panels of varying shape) at geodesic nu = 20 (8000 triangles): tree
+    bit-exact, dense blocks and ACA pivots vs the oracle, H-matvec vs the exact Galerkin rows
+    (<= 10 eps_aca) and vs the oracle's H (<= 1e-12), GMRES solution vs the oracle (<= 1e-5)."""
+    V, T = lobed(20)
+    H = _gpu(V, T)
+    R = _compare_tree(O, H, V, T)
+    H.set_option("record_pivots", 1)
+    H.setup(EPS)
+    R.assemble(EPS)
+    _check_blocks(H, R)
+    N = T.shape[0]
+    rows = np.random.default_rng(7).permutation(N)[:128]
+    Arows = R.dense_rows(rows)
+    for x in [np.ones(N), seeded_vector(N, 2)]:
+        yg = H.matvec(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+        ye = Arows @ x
+        assert np.linalg.norm(yg[rows] - ye) <= 10 * EPS * np.linalg.norm(ye)
+        yo = R.matvec(x)
+        assert np.linalg.norm(yg - yo) <= 1e-12 * np.linalg.norm(yo)
+    f = R.rhs(1)
+    sol, it, rr = H.solve(torch_cuda.from_numpy(f).cuda(), tol=1e-10)
+    xo = R.gmres(f, tol=1e-10)[0]
+    assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-5 * np.linalg.norm(xo)
+    H.close()
