@@ -692,7 +692,9 @@ void plan_matvec(Context& C) {
   // block order = factor-pool order except for the few blocks re-run after a workspace
   // overflow (stored at the end): they just become separate bulk-copy runs, no sort needed
   const int64_t nlr = (int64_t)lr_order.size(), total = nd + nlr;
-  const int T = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()),
+  // planner threads: the host's cores shared by the ranks of this node (one process per GPU)
+  const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency() / std::max(1, C.world));
+  const int T = (int)std::max<int64_t>(1, std::min<int64_t>({hw,
                                                               16, total / 20000 + 1}));
   W.parts.resize(T);
   const int64_t* hoff = W.hoff.data();
