@@ -99,14 +99,10 @@ const char* hm_last_error(hm_ctx ctx);
  *   "kernel_timing" 1: record CUDA events on the context stream around every launch of
  *                  each kernel family (near-field evaluation, ACA evaluation, other ACA,
  *                  matvec, Krylov BLAS-1); totals in hm_get_stats "kt"; setting it resets them
- *   "mv_kernel"    small-leaf matvec pipeline: 4 (default) two CTA rings per SM, 2 x 48 KiB
- *                  stages each; 1 one ring of 4 x 48 KiB; 2 / 3 one ring of 8 x 24 / 6 x 32
- *                  KiB; 0 per-warp rings of 2 x 13 KiB.  Re-plans the matvec if set up.
- *   "mv_large_u"   large low-rank U phase: 1 (default) 8 rows per lane in registers per tile,
- *                  0 two rows per pass
+ *   "mv_kernel"    small-leaf matvec pipeline: 0 (default) two CTA rings per SM, 2 x 48 KiB
+ *                  stages each; 1 one ring of 4 x 48 KiB stages.  Re-plans the matvec if set up.
  *   "mv_small_max" low-rank leaves up to this many bytes (default 16384) go through the
  *                  shared-memory pipeline, larger ones through the large-block kernels
- *   "mv_large_v"   large low-rank V phase tiles: 1 (default) 16 columns x 1024 rows, 0 8 x 2048
  *   "mv_profile"   1: accumulate producer/consumer wait and work cycles of the CTA-ring
  *                  matvec (hm_get_stats "mv_prof_cycles"); diagnostic
  *   "mv_scramble"  1: DIAGNOSTIC ONLY, wrong products: spread the row bases of the CTA-ring

@@ -303,15 +303,13 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
     else if (k == "aca_kws") { if (v < 1 || v > 256) bad(); C.aca_kws = v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
-    else if (k == "mv_kernel") { if (v < 0 || v > 6 || v != (int)v) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
+    else if (k == "mv_kernel") { if (v != 0 && v != 1) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_profile") {
       if (v != 0 && v != 1) bad();
       if (v == 1) { C.mv_prof.alloc(4); HM_CUDA(cudaMemsetAsync(C.mv_prof.get(), 0, 32, C.stream)); }
       else C.mv_prof.release();
     }
     else if (k == "mv_small_max") { if (v < 0 || v > 49152) bad(); C.mv_small_max = (int)v; if (C.have_setup) hm::plan_matvec(C); }
-    else if (k == "mv_large_u") { if (v != 0 && v != 1) bad(); C.mv_large_u = (int)v; }
-    else if (k == "mv_large_v") { if (v != 0 && v != 1) bad(); C.mv_large_v = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_scramble") { if (v != 0 && v != 1) bad(); C.mv_scramble = (int)v; }
     else if (k == "kernel_timing") {
       if (v != 0 && v != 1) bad();

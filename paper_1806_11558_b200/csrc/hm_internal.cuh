@@ -266,10 +266,8 @@ struct Context {
   int mv_grid = 0;
   DBuf<unsigned long long> mv_prof;   // option "mv_profile": [producer empty-wait, consumer full-wait, consumer work] cycles
   int mv_small_max = 16384;    // option "mv_small_max": low-rank leaves up to this many bytes go through the pipeline
-  int mv_large_u = 1;          // option "mv_large_u": 1 all 8 rows of the tile per lane (default), 0 two rows per pass
-  int mv_large_v = 1;          // option "mv_large_v": 1 16 columns x 1024 rows tiles (default), 0 8 x 2048
   int mv_scramble = 0;         // diagnostic option "mv_scramble" (wrong results): see k_mv_batched
-  int mv_kind = 4;             // option "mv_kernel": 4 two CTA rings per SM, 2 x 48 KiB each (default); 1 one CTA ring 4 x 48 KiB; 2 / 3 one ring 8 x 24 / 6 x 32 KiB; 0 warp rings
+  int mv_kind = 0;             // option "mv_kernel": 0 two CTA rings per SM, 2 x 48 KiB each (default); 1 one ring of 4
   int64_t mv_nbatches = 0, mv_tlen = 0, mv_nsegs = 0;
   int64_t n_lr_small = 0, n_lr_large = 0;
 

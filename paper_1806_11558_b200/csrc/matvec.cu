@@ -4,18 +4,19 @@
 //
 // Memory-bound (0.25 flop/B): the stored H is streamed from HBM exactly once per product.
 //
-//   small leaves   (dense blocks and low-rank blocks with (m+n)k*8 <= 16 KiB, ~all leaves):
-//                  k_mv_batched — one persistent CTA per SM walks a contiguous, byte-balanced
-//                  range of "batches" (consecutive leaves filling <= 44 KiB).  One elected
-//                  thread streams each batch into shared memory with one cp.async.bulk (TMA
-//                  bulk copy, mbarrier completion) per contiguous run of leaves, 4 stages deep
-//                  (~176 KiB per SM in flight); warp 0 produces, 15 consumer warps compute
-//                  the staged batches out of shared memory (dense rows with s lanes per row,
-//                  low-rank t = V^T x then y += U t), releasing each stage through an "empty"
-//                  mbarrier.  One FP64 atomic per row into the L2-resident y.
+//   small leaves   (dense blocks and low-rank blocks with (m+n)k*8 <= 16 KiB, ~90% of leaves):
+//                  k_mv_batched — persistent CTAs (two per SM by default), each over a
+//                  contiguous, byte-balanced range of "batches" (48 KiB shared-memory stages:
+//                  task records | x_sigma ranges | leaf storage).  Warp 0 streams the batch /
+//                  segment descriptors through register windows and issues each batch's bulk
+//                  copies (cp.async.bulk, mbarrier completion) from its 32 lanes; the consumer
+//                  warps compute the staged batches entirely out of shared memory and release
+//                  each stage through an "empty" mbarrier.  One FP64 atomic per row into the
+//                  L2-resident y.
 //   large low-rank (blocks above 16 KiB): two barrier-free warp-task kernels with direct
-//                  coalesced loads, k_mv_large_v (t += V^T x over 8-column x 2048-row tiles,
-//                  atomics into t) then k_mv_large_u (y += U t, k independent loads per row).
+//                  coalesced loads, k_mv_large_v (t += V^T x over 16-column x 1024-row tiles,
+//                  one atomic per column into t) then k_mv_large_u (y += U t, 256-row tiles,
+//                  8 rows per lane in registers).
 //   dense blocks too big for a stage (only with large leaf_size): k_mv_dense_direct.
 #include <cub/cub.cuh>
 
@@ -29,13 +30,7 @@
 
 namespace hm {
 
-constexpr int kMvStages = 4;              // k_mv_batched (CTA ring): 4 x 48 KiB stages
-constexpr int kMvStageBytes = 48 * 1024;
-constexpr int kMvThreads = 512;
-constexpr int kWrWarps = 8;               // k_mv_warps (warp rings): 8 warps x 2 x 13 KiB stages
-constexpr int kWrStages = 2;
-constexpr int kWrStageBytes = 13 * 1024;
-constexpr int kMvSmallMax = 16 * 1024;
+constexpr int kMvStageBytes = 48 * 1024;   // one k_mv_batched pipeline stage (= one batch)
 constexpr int kMaxX = 12;         // x_sigma ranges (bulk copies) per batch
 constexpr int64_t kXGap = 64;     // doubles: merge x ranges closer than this
 
@@ -91,6 +86,7 @@ __device__ __forceinline__ void dense_block(const double* __restrict__ B, int m,
     double acc[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) acc[p] = 0.0;
+#pragma unroll 2
     for (int c = sub; c < n; c += S) {
       const double xc = xs[c];
 #pragma unroll
@@ -162,6 +158,7 @@ __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int
   double acc[KB];
 #pragma unroll
   for (int l = 0; l < KB; ++l) acc[l] = 0.0;
+#pragma unroll 2
   for (int j = lane; j < n; j += 32) {
     const double xj = xs[j];
 #pragma unroll
@@ -170,11 +167,13 @@ __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int
   }
   warp_allreduce_vec<KB>(acc, lane);
   for (int t = lane; t < m; t += 32) {
-    double s = 0.0;
+    double s0 = 0.0, s1 = 0.0;                  // two chains: half the dependent-FMA latency
 #pragma unroll
-    for (int l = 0; l < KB; ++l)
-      if (l < kc) s = __fma_rn(U[t + l * m], acc[l], s);
-    atomicAdd(y + t, s);
+    for (int l = 0; l < KB; l += 2) {
+      if (l < kc) s0 = __fma_rn(U[t + l * m], acc[l], s0);
+      if (l + 1 < kc) s1 = __fma_rn(U[t + (l + 1) * m], acc[l + 1], s1);
+    }
+    atomicAdd(y + t, s0 + s1);
   }
 }
 
@@ -220,7 +219,7 @@ struct RecWindow {
   }
 };
 
-template <int STAGES, int SBYTES, int THREADS = kMvThreads, int MINB = 1>
+template <int STAGES, int SBYTES, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_mv_batched(const MvBatch* __restrict__ batches, const MvSeg* __restrict__ segs, int64_t nsegs_total,
                  const int32_t* __restrict__ cta_first,
@@ -307,148 +306,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
   }
 }
 
-// Warp rings: every warp streams its own contiguous, byte-balanced range of batches through
-// its own kWrStages shared-memory stages — it issues the bulk copies of batch it + kWrStages
-// itself right after it has consumed batch it (32 lanes in parallel), so a slow task delays
-// only its own warp's stream and no stage waits for the slowest of many consumers.
-__global__ void __launch_bounds__(kWrWarps * 32, 1)
-    k_mv_warps(const MvBatch* __restrict__ batches, const MvSeg* __restrict__ segs, const int32_t* __restrict__ warp_first,
-               const char* __restrict__ base0, const char* __restrict__ base1, const char* __restrict__ base2,
-               const double* __restrict__ x, double* __restrict__ y) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem) + warp * kWrStages;
-  unsigned char* buf = smem + 256 + (size_t)warp * kWrStages * kWrStageBytes;
-  const int gw = blockIdx.x * kWrWarps + warp;
-  const int b0 = warp_first[gw], nb = warp_first[gw + 1] - b0;
-  if (lane == 0) {
-    for (int s = 0; s < kWrStages; ++s) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  // descriptors of the next batch to issue (and the lane's first segment of it) are loaded one
-  // batch ahead, off the critical path
-  MvBatch next = nb > 0 ? batches[b0] : MvBatch{0, 0, 0, 0};
-  MvSeg nseg0 = (nb > 0 && lane < next.nseg) ? segs[next.first_seg + lane] : MvSeg{0, 0, 0, 0, 0};
-  auto issue = [&](int it) {
-    const MvBatch B = next;
-    const MvSeg S0 = nseg0;
-    if (it + 1 < nb) {
-      next = batches[b0 + it + 1];
-      nseg0 = lane < next.nseg ? segs[next.first_seg + lane] : MvSeg{0, 0, 0, 0, 0};
-    }
-    const int st = it % kWrStages;
-    if (lane == 0) mbar_expect_tx(&full[st], (unsigned)B.bytes);
-    __syncwarp();
-    unsigned char* sb = buf + st * kWrStageBytes;
-    for (int s = lane; s < B.nseg; s += 32) {
-      const MvSeg S = s == lane ? S0 : segs[B.first_seg + s];
-      const char* base = S.base == 0 ? base0 : S.base == 1 ? base1 : S.base == 2 ? base2
-                                                             : reinterpret_cast<const char*>(x);
-      bulk_g2s(sb + S.dst, base + S.src, (unsigned)S.bytes, &full[st]);
-    }
-  };
-  for (int it = 0; it < kWrStages && it < nb; ++it) issue(it);
-  for (int it = 0; it < nb; ++it) {
-    const int st = it % kWrStages;
-    mbar_wait(&full[st], (unsigned)((it / kWrStages) & 1));
-    const unsigned char* sb = buf + st * kWrStageBytes;
-    const double* sd = reinterpret_cast<const double*>(sb);
-    const int4* rec = reinterpret_cast<const int4*>(sb);
-    const int count = rec[0].x;
-    for (int t = 0; t < count; ++t) {
-      const int4 T = rec[1 + t];
-      const uint32_t mnk = (uint32_t)T.w;
-      const int m = mnk & 2047, n = (mnk >> 11) & 2047, k = mnk >> 22;
-      if (k == 0) dense_any(sd + T.z, m, n, sd + T.y, y + T.x, lane);
-      else lowrank_any(sd + T.z, m, n, k, sd + T.y, y + T.x, lane);
-    }
-    __syncwarp();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads before the async refill
-    if (it + kWrStages < nb) issue(it + kWrStages);
-  }
-}
-
 // Large low-rank blocks (storage > 16 KiB), barrier-free warp tasks with direct coalesced loads.
-// Phase 1, tile = (block, 8 columns l0.., 2048 rows j0..): t[l] += sum_j V[j, l] x[clo + j];
-// each lane keeps 8 column sums (x_j loaded once per row, 8 independent loads in flight).
-__global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
-                                                    const MvLarge* __restrict__ L, const double* __restrict__ pool,
-                                                    const double* __restrict__ x, double* __restrict__ tbuf) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = w0; i < ntiles; i += nw) {
-    const MvTileV T = tiles[i];
-    const MvLarge B = L[T.blk];
-    const int kc = min(8, B.k - T.l);
-    const double* V = pool + B.off + (int64_t)B.m * B.k + (int64_t)T.l * B.n;
-    const double* xs = x + B.clo;
-    double acc[8];
-#pragma unroll
-    for (int l = 0; l < 8; ++l) acc[l] = 0.0;
-    for (int j = T.j0 + lane; j < T.j1; j += 64) {
-      const bool two = j + 32 < T.j1;
-      const double xa = __ldg(xs + j), xb = two ? __ldg(xs + j + 32) : 0.0;
-      double va[8], vb[8];
-#pragma unroll
-      for (int l = 0; l < 8; ++l) {
-        va[l] = l < kc ? __ldg(V + j + (int64_t)l * B.n) : 0.0;
-        vb[l] = (l < kc && two) ? __ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
-      }
-#pragma unroll
-      for (int l = 0; l < 8; ++l) acc[l] = __fma_rn(vb[l], xb, __fma_rn(va[l], xa, acc[l]));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int l = 0; l < 8; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], o);
-    if (lane < kc) {
-      double v = acc[0];
-#pragma unroll
-      for (int l = 1; l < 8; ++l) v = lane == l ? acc[l] : v;
-      atomicAdd(tbuf + B.toff + T.l + lane, v);
-    }
-  }
-}
-
-// Phase 2, tile = (block, 256 rows t0..): y[rlo + t] += sum_l U[t, l] t_l (k independent loads per row)
-__global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ tiles, int64_t ntiles,
-                                                    const MvLarge* __restrict__ L, const double* __restrict__ pool,
-                                                    const double* __restrict__ tbuf, double* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = w0; i < ntiles; i += nw) {
-    const MvTileU T = tiles[i];
-    const MvLarge B = L[T.blk];
-    const double* U = pool + B.off;
-    const double* tl = tbuf + B.toff;
-    for (int t = T.t0 + lane; t < T.t1; t += 64) {
-      const bool two = t + 32 < T.t1;
-      double s0 = 0.0, s1 = 0.0, r0 = 0.0, r1 = 0.0;
-      int l = 0;
-      for (; l + 1 < B.k; l += 2) {
-        const double ta = __ldg(tl + l), tb = __ldg(tl + l + 1);
-        const double u0 = __ldg(U + t + (int64_t)l * B.m), u1 = __ldg(U + t + (int64_t)(l + 1) * B.m);
-        const double w0 = two ? __ldg(U + t + 32 + (int64_t)l * B.m) : 0.0;
-        const double w1 = two ? __ldg(U + t + 32 + (int64_t)(l + 1) * B.m) : 0.0;
-        s0 = __fma_rn(u0, ta, s0); s1 = __fma_rn(u1, tb, s1); r0 = __fma_rn(w0, ta, r0); r1 = __fma_rn(w1, tb, r1);
-      }
-      if (l < B.k) {
-        const double ta = __ldg(tl + l);
-        s0 = __fma_rn(__ldg(U + t + (int64_t)l * B.m), ta, s0);
-        if (two) r0 = __fma_rn(__ldg(U + t + 32 + (int64_t)l * B.m), ta, r0);
-      }
-      atomicAdd(y + B.rlo + t, s0 + s1);
-      if (two) atomicAdd(y + B.rlo + t + 32, r0 + r1);
-    }
-  }
-}
-
-// Variant (option "mv_large_v" = 1): tile = (block, 16 columns l0.., 1024 rows j0..); all 16
-// column sums in registers, two rows per lane per pass (32 independent loads), one halving
-// butterfly for the 16 sums, one atomic per column.
+// Phase 1, tile = (block, 16 columns l0.., 1024 rows j0..): t[l] += sum_j V[j, l] x[clo + j];
+// all 16 column sums in registers, two rows per lane per pass (32 independent loads), one
+// halving butterfly for the 16 sums, one atomic per column.
 template <int KB>
 __device__ __forceinline__ void warp_reduce_halving(double (&v)[KB], int lane) {
   constexpr int LV = KB == 16 ? 4 : 3;
@@ -468,7 +329,7 @@ __device__ __forceinline__ void warp_reduce_halving(double (&v)[KB], int lane) {
   for (int o = 16 >> LV; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
 }
 
-__global__ void __launch_bounds__(256) k_mv_large_v16(const MvTileV* __restrict__ tiles, int64_t ntiles,
+__global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
                                                       const MvLarge* __restrict__ L, const double* __restrict__ pool,
                                                       const double* __restrict__ x, double* __restrict__ tbuf) {
   const int lane = threadIdx.x & 31;
@@ -502,9 +363,9 @@ __global__ void __launch_bounds__(256) k_mv_large_v16(const MvTileV* __restrict_
   }
 }
 
-// Variant (option "mv_large_u" = 1): each lane keeps all 8 of its rows of the 256-row tile in
-// registers; per column l one broadcast t_l and 8 independent loads of U.
-__global__ void __launch_bounds__(256) k_mv_large_u8(const MvTileU* __restrict__ tiles, int64_t ntiles,
+// Phase 2, tile = (block, 256 rows t0..): y[rlo + t] += sum_l U[t, l] t_l; each lane keeps its
+// 8 rows of the tile in registers: per column l one broadcast t_l and 8 independent loads of U.
+__global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ tiles, int64_t ntiles,
                                                      const MvLarge* __restrict__ L, const double* __restrict__ pool,
                                                      const double* __restrict__ tbuf, double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
@@ -698,9 +559,7 @@ void plan_matvec(Context& C) {
                                                               16, total / 20000 + 1}));
   W.parts.resize(T);
   const int64_t* hoff = W.hoff.data();
-  const bool wr = C.mv_kind == 0;
-  const int64_t cap = wr ? kWrStageBytes : (C.mv_kind == 1 || C.mv_kind == 4) ? 48 * 1024
-                   : (C.mv_kind == 2 || C.mv_kind == 6) ? 24 * 1024 : 32 * 1024;
+  const int64_t cap = kMvStageBytes;
   auto work = [&](int t) {
     PlanPart& P = W.parts[t];
     P.clear();
@@ -761,11 +620,10 @@ void plan_matvec(Context& C) {
     C.mv_tlen = tl;
   }
   const auto t2 = clk::now();
-  // byte-balanced contiguous batch ranges: one per persistent CTA (CTA ring) or per warp of
-  // one persistent CTA per SM (warp rings)
+  // byte-balanced contiguous batch ranges, one per persistent CTA (two or one per SM)
   int sms = 148;
   HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, C.device));
-  const int G = wr ? sms * kWrWarps : std::max(1, std::min<int>(C.mv_kind >= 4 ? 2 * sms : sms, (int)nbat));
+  const int G = std::max(1, std::min<int>(C.mv_kind == 0 ? 2 * sms : sms, (int)nbat));
   W.cta.resize(G + 1);
   {
     double tot = 0;
@@ -781,7 +639,7 @@ void plan_matvec(Context& C) {
     while (g + 1 < G) W.cta[++g] = (int32_t)nbat;
   }
   // tiles of the large low-rank blocks
-  const int vcols = C.mv_large_v == 1 ? 16 : 8, vrows = C.mv_large_v == 1 ? 1024 : 2048;
+  const int vcols = 16, vrows = 1024;
   size_t ntv = 0, ntu = 0;
   for (size_t i = 0; i < nlarge; ++i) {
     const MvLarge& B = W.large[i];
@@ -812,7 +670,7 @@ void plan_matvec(Context& C) {
   up(C.mv_dense_big, W.dense_big);
   up(C.mv_tiles_v, W.tv);
   up(C.mv_tiles_u, W.tu);
-  C.mv_grid = wr ? sms : G;
+  C.mv_grid = G;
   C.mv_nbatches = (int64_t)nbat;
   C.mv_nsegs = (int64_t)nseg;
   C.mv_tbuf.alloc(C.mv_tlen + 1);
@@ -829,20 +687,10 @@ void plan_matvec(Context& C) {
   C.times.plan_phase_ms[2] = std::chrono::duration<double, std::milli>(t3 - t2).count();
   static bool attr = false;
   if (!attr) {
-    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<4, 48 * 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 256 + 4 * 48 * 1024));
-    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<8, 24 * 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 256 + 8 * 24 * 1024));
-    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<6, 32 * 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 256 + 6 * 32 * 1024));
-    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<2, 48 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 256 + 2 * 48 * 1024));
-    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<3, 32 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 256 + 3 * 32 * 1024));
-    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<4, 24 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 256 + 4 * 24 * 1024));
-    HM_CUDA(cudaFuncSetAttribute(k_mv_warps, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 256 + kWrWarps * kWrStages * kWrStageBytes));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<2, kMvStageBytes, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 2 * kMvStageBytes));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<4, kMvStageBytes, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 4 * kMvStageBytes));
     attr = true;
   }
 }
@@ -872,35 +720,16 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
   if (C.mv_tlen) HM_CUDA(cudaMemsetAsync(C.mv_tbuf.get(), 0, C.mv_tlen * sizeof(double), st));
   const double* pool = (const double*)C.fpool.base;
   if (C.mv_nbatches) {
-    if (C.mv_kind == 0) {
-      k_mv_warps<<<C.mv_grid, kWrWarps * 32, 256 + kWrWarps * kWrStages * kWrStageBytes, st>>>(
-          C.mv_batches.get(), C.mv_segs.get(), C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int);
-    } else if (C.mv_kind == 1) {
-      k_mv_batched<4, 48 * 1024><<<C.mv_grid, kMvThreads, 256 + 4 * 48 * 1024, st>>>(
+    unsigned long long* prof = C.mv_prof.n ? C.mv_prof.get() : nullptr;
+    const int64_t scramble = C.mv_scramble ? C.N - 4096 : 0;
+    if (C.mv_kind == 0)      // two CTA rings per SM, 2 x 48 KiB stages, 7 consumer warps each
+      k_mv_batched<2, kMvStageBytes, 256, 2><<<C.mv_grid, 256, 256 + 2 * kMvStageBytes, st>>>(
           C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
-    } else if (C.mv_kind == 2) {
-      k_mv_batched<8, 24 * 1024><<<C.mv_grid, kMvThreads, 256 + 8 * 24 * 1024, st>>>(
+          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof);
+    else                     // one CTA ring per SM, 4 x 48 KiB stages, 15 consumer warps
+      k_mv_batched<4, kMvStageBytes, 512, 1><<<C.mv_grid, 512, 256 + 4 * kMvStageBytes, st>>>(
           C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
-    } else if (C.mv_kind == 5) {
-      k_mv_batched<3, 32 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 3 * 32 * 1024, st>>>(
-          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
-    } else if (C.mv_kind == 6) {
-      k_mv_batched<4, 24 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 4 * 24 * 1024, st>>>(
-          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
-    } else if (C.mv_kind == 4) {
-      k_mv_batched<2, 48 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 2 * 48 * 1024, st>>>(
-          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
-    } else {
-      k_mv_batched<6, 32 * 1024><<<C.mv_grid, kMvThreads, 256 + 6 * 32 * 1024, st>>>(
-          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int, C.mv_scramble ? C.N - 4096 : 0, C.mv_prof.n ? C.mv_prof.get() : nullptr);
-    }
+          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof);
     HM_CHECK_LAUNCH();
   }
   if (C.mv_n_dense_big) {
@@ -909,19 +738,11 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
     HM_CHECK_LAUNCH();
   }
   if (C.mv_n_tiles_v) {
-    if (C.mv_large_v == 1)
-      k_mv_large_v16<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
-                                              C.mv_tbuf.get());
-    else
-      k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
-                                            C.mv_tbuf.get());
+    k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
+                                          C.mv_tbuf.get());
     HM_CHECK_LAUNCH();
-    if (C.mv_large_u == 1)
-      k_mv_large_u8<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
-                                             C.mv_tbuf.get(), y_int);
-    else
-      k_mv_large_u<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
-                                            C.mv_tbuf.get(), y_int);
+    k_mv_large_u<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
+                                          C.mv_tbuf.get(), y_int);
     HM_CHECK_LAUNCH();
   }
   ks.reset();
