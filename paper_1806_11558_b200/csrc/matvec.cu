@@ -685,7 +685,8 @@ void plan_matvec(Context& C) {
   C.times.plan_phase_ms[0] = std::chrono::duration<double, std::milli>(t1 - t0).count();
   C.times.plan_phase_ms[1] = std::chrono::duration<double, std::milli>(t2 - t1).count();
   C.times.plan_phase_ms[2] = std::chrono::duration<double, std::milli>(t3 - t2).count();
-  static bool attr = false;
+  static bool attr_done[64] = {false};            // function attributes are per device
+  bool& attr = attr_done[C.device & 63];
   if (!attr) {
     HM_CUDA(cudaFuncSetAttribute(k_mv_batched<2, kMvStageBytes, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  256 + 2 * kMvStageBytes));
