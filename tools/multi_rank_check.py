@@ -5,7 +5,7 @@ lists; the matvec's partial products are all-reduced.  C
   * owned ranges of all ranks are disjoint and cover both lists (gathered to rank 0);
   * the p-rank H-matvec equals a 1-rank H-matvec built on rank 0's GPU to 1e-13 relative
     (same leaves, same factors; only the summation order of the global sum differs, A19);
-  * the p-rank GMRES solution equals the 1-rank solution to 1e-8 relative: both solves stop at
+  * the p-rank GMRES and CG solutions (sharded Krylov vectors) equal the 1-rank ones to 1e-8: both solves stop at
     relres <= 1e-10 with y differing by ~1e-15 per product (A19), so they can differ by up to
     cond(H) * 2e-10 (cond ~ 1e3 at C2, growing like 1/h); observed 4e-14 (C2), 1.3e-10 (C3).
 Prints one JSON line on rank 0 and exits non-zero on failure.
@@ -42,6 +42,9 @@ def main():
     y = H.matvec(x)
     f = torch.from_numpy(H.assemble_rhs(1)).cuda()
     sol, it, rr = H.solve(f, 1e-10)
+    H.set_option("solver", 1)                     # CG on the sharded Krylov vectors too
+    sol_cg, it_cg, rr_cg = H.solve(f, 1e-10)
+    H.set_option("solver", 0)
     torch.cuda.synchronize()
     own = torch.tensor(st["adm_owned"] + st["dense_owned"], dtype=torch.int64, device="cuda")
     allown = [torch.zeros_like(own) for _ in range(world)]
@@ -62,12 +65,16 @@ def main():
         R.setup(1e-6)
         y1 = R.matvec(x)
         s1, it1, rr1 = R.solve(f, 1e-10)
+        R.set_option("solver", 1)
+        s1cg, it1cg, _ = R.solve(f, 1e-10)
         torch.cuda.synchronize()
         dy = (torch.linalg.norm(y - y1) / torch.linalg.norm(y1)).item()
         ds = (torch.linalg.norm(sol - s1) / torch.linalg.norm(s1)).item()
-        res.update({"matvec_rel_diff": dy, "solve_rel_diff": ds, "iters": it, "iters_1rank": it1,
+        dcg = (torch.linalg.norm(sol_cg - s1cg) / torch.linalg.norm(s1cg)).item()
+        res.update({"matvec_rel_diff": dy, "solve_rel_diff": ds, "cg_rel_diff": dcg, "cg_iters": it_cg,
+                    "cg_iters_1rank": it1cg, "iters": it, "iters_1rank": it1,
                     "setup_ms_max": setup_ms.item(), "setup_ms_1rank": R.stats()["setup_ms"]})
-        ok &= dy <= 1e-13 and ds <= 1e-8
+        ok &= dy <= 1e-13 and ds <= 1e-8 and dcg <= 1e-8
         res["ok"] = bool(ok)
         print(json.dumps(res), flush=True)
         R.close()
