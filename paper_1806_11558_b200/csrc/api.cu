@@ -365,6 +365,7 @@ hm_status hm_setup(hm_ctx ctx, double eps_aca) {
       hm::setup_nearfield(C);
       C.times.near_ms = t.ms();
     }
+    hm::plan_dense_begin(C);
     {
       Timer t(C);
       hm::setup_aca(C);

@@ -519,7 +519,12 @@ struct PlanPart {
 
 struct PlanWs {
   std::vector<int64_t> hoff, lr_order;
-  std::vector<PlanPart> parts;
+  std::vector<PlanPart> parts;       // dense parts [0, nd_parts), then low-rank parts
+  int nd_parts = 0;
+  std::thread dense_thread;          // plans the dense leaves while ACA runs on the GPU
+  std::exception_ptr dense_err;
+  bool dense_started = false;
+  ~PlanWs() { if (dense_thread.joinable()) dense_thread.join(); }
   PinnedVec<MvBatch> batches;
   PinnedVec<MvSeg> segs;
   PinnedVec<MvTask> stream;
@@ -532,72 +537,115 @@ struct PlanWs {
 // The matvec plan, built on the host by T threads over contiguous slices of the item sequence
 // (owned dense leaves in list order, then owned low-rank leaves in factor-pool order); batches
 // never straddle two slices.
+namespace {
+// Items of the leaf sequence slice [i0, i1) -> one part's batches.  Dense leaves: sequence
+// position = owned dense index; low-rank leaves: position in lr_order.
+void plan_dense_part(Context& C, PlanWs& W, PlanPart& P, int64_t i0, int64_t i1) {
+  P.clear();
+  P.items.reserve(i1 - i0);
+  const int64_t cap = kMvStageBytes;
+  const int64_t* hoff = W.hoff.data();
+  for (int64_t b = i0; b < i1; ++b) {
+    const Quad& q = C.h_dense[C.dense_begin + b];
+    const int m = q.rhi - q.rlo, n = q.chi - q.clo;
+    const int64_t bytes = 8 * (int64_t)m * n;
+    if (bytes + 8 * n + 64 > cap || m > 2047 || n > 2047)
+      P.dense_big.push_back(MvLarge{q.rlo, q.clo, m, n, 0, 0, hoff[b], 0});
+    else
+      P.items.push_back(Item{8 * hoff[b], bytes, 0, q.rlo, q.clo, n, (uint32_t)m | ((uint32_t)n << 11)});
+  }
+  P.batch(cap);
+}
+void plan_lowrank_part(Context& C, PlanWs& W, PlanPart& P, int64_t i0, int64_t i1) {
+  P.clear();
+  P.items.reserve(i1 - i0);
+  const int64_t cap = kMvStageBytes;
+  for (int64_t i = i0; i < i1; ++i) {
+    const int64_t b = W.lr_order[i];
+    const Quad& q = C.h_adm[C.adm_begin + b];
+    const int m = q.rhi - q.rlo, n = q.chi - q.clo, k = C.h_rank[b];
+    const int64_t bytes = 8 * (int64_t)k * (m + n);
+    if (bytes <= std::min<int64_t>(C.mv_small_max, cap - 8 * n - 64) && m <= 2047 && n <= 2047 && k <= 1023)
+      P.items.push_back(Item{8 * C.h_foff[b], bytes, 1, q.rlo, q.clo, n,
+                             (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)});
+    else
+      P.large.push_back(MvLarge{q.rlo, q.clo, m, n, k, 0, C.h_foff[b], 0});
+  }
+  P.batch(cap);
+}
+// run f(t) for t in [0, T) on T host threads (the caller's thread included)
+template <class F>
+void run_threads(int T, F&& f) {
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(T);
+  for (int t = 1; t < T; ++t)
+    th.emplace_back([&, t]() { try { f(t); } catch (...) { err[t] = std::current_exception(); } });
+  try { f(0); } catch (...) { err[0] = std::current_exception(); }
+  for (auto& x : th) x.join();
+  for (auto& e : err) if (e) std::rethrow_exception(e);
+}
+int planner_threads(Context& C, int64_t work) {
+  // the host's cores shared by the ranks of this node (one process per GPU)
+  const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency() / std::max(1, C.world));
+  return (int)std::max<int64_t>(1, std::min<int64_t>({hw, 16, work / 20000 + 1}));
+}
+}  // namespace
+
+// Dense half of the matvec plan: depends only on the tree and the near-field offsets, so it
+// is planned on host threads while ACA runs on the GPU (joined by plan_matvec).
+void plan_dense_begin(Context& C) {
+  if (!C.plan_ws) C.plan_ws = std::make_shared<PlanWs>();
+  PlanWs& W = *C.plan_ws;
+  if (W.dense_thread.joinable()) W.dense_thread.join();
+  const int64_t nd = C.dense_end - C.dense_begin;
+  W.hoff.resize(nd + 1);
+  HM_CUDA(cudaMemcpyAsync(W.hoff.data(), C.doff.get(), (nd + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
+  if (C.h_dense.size() != (size_t)C.ndense) {
+    C.h_dense.resize(C.ndense);
+    HM_CUDA(cudaMemcpyAsync(C.h_dense.data(), C.dense.get(), C.ndense * sizeof(Quad), cudaMemcpyDeviceToHost, C.stream));
+  }
+  HM_CUDA(cudaStreamSynchronize(C.stream));
+  // leave cores for the setup thread that keeps launching ACA kernels meanwhile
+  const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency() / std::max(1, C.world));
+  const int Td = std::max(1, std::min<int>(planner_threads(C, nd), (int)hw - 2));
+  W.nd_parts = Td;
+  if (W.parts.size() < (size_t)Td) W.parts.resize(Td);
+  W.dense_err = nullptr;
+  W.dense_started = true;
+  Context* pc = &C;
+  W.dense_thread = std::thread([pc, &W, Td, nd]() {
+    try {
+      run_threads(Td, [&](int t) { plan_dense_part(*pc, W, W.parts[t], nd * t / Td, nd * (t + 1) / Td); });
+    } catch (...) {
+      W.dense_err = std::current_exception();
+    }
+  });
+}
+
+// The matvec plan, built on the host by threads over contiguous slices of the item sequence
+// (owned dense leaves in list order — planned during ACA by plan_dense_begin — then owned
+// low-rank leaves in block order); batches never straddle two slices.
 void plan_matvec(Context& C) {
   cudaStream_t st = C.stream;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   if (!C.plan_ws) C.plan_ws = std::make_shared<PlanWs>();
   PlanWs& W = *C.plan_ws;
-  const int64_t nd = C.dense_end - C.dense_begin, na = C.adm_end - C.adm_begin;
-  W.hoff.resize(nd + 1);
-  HM_CUDA(cudaMemcpyAsync(W.hoff.data(), C.doff.get(), (nd + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  if (C.h_dense.size() != (size_t)C.ndense) {
-    C.h_dense.resize(C.ndense);
-    HM_CUDA(cudaMemcpyAsync(C.h_dense.data(), C.dense.get(), C.ndense * sizeof(Quad), cudaMemcpyDeviceToHost, st));
-  }
-  HM_CUDA(cudaStreamSynchronize(st));
+  if (!W.dense_started) plan_dense_begin(C);        // re-plan (options) or no overlap
+  W.dense_thread.join();
+  W.dense_started = false;
+  if (W.dense_err) std::rethrow_exception(W.dense_err);
+  const int64_t na = C.adm_end - C.adm_begin;
   std::vector<int64_t>& lr_order = W.lr_order;
   lr_order.clear();
   for (int64_t b = 0; b < na; ++b)
     if (C.h_rank[b] > 0) lr_order.push_back(b);
   // block order = factor-pool order except for the few blocks re-run after a workspace
   // overflow (stored at the end): they just become separate bulk-copy runs, no sort needed
-  const int64_t nlr = (int64_t)lr_order.size(), total = nd + nlr;
-  // planner threads: the host's cores shared by the ranks of this node (one process per GPU)
-  const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency() / std::max(1, C.world));
-  const int T = (int)std::max<int64_t>(1, std::min<int64_t>({hw,
-                                                              16, total / 20000 + 1}));
+  const int64_t nlr = (int64_t)lr_order.size();
+  const int Td = W.nd_parts, Tl = planner_threads(C, nlr), T = Td + Tl;
   W.parts.resize(T);
-  const int64_t* hoff = W.hoff.data();
-  const int64_t cap = kMvStageBytes;
-  auto work = [&](int t) {
-    PlanPart& P = W.parts[t];
-    P.clear();
-    const int64_t i0 = total * t / T, i1 = total * (t + 1) / T;
-    P.items.reserve(i1 - i0);
-    for (int64_t i = i0; i < i1; ++i) {
-      if (i < nd) {
-        const int64_t b = i;
-        const Quad& q = C.h_dense[C.dense_begin + b];
-        const int m = q.rhi - q.rlo, n = q.chi - q.clo;
-        const int64_t bytes = 8 * (int64_t)m * n;
-        if (bytes + 8 * n + 64 > cap || m > 2047 || n > 2047)
-          P.dense_big.push_back(MvLarge{q.rlo, q.clo, m, n, 0, 0, hoff[b], 0});
-        else
-          P.items.push_back(Item{8 * hoff[b], bytes, 0, q.rlo, q.clo, n, (uint32_t)m | ((uint32_t)n << 11)});
-      } else {
-        const int64_t b = lr_order[i - nd];
-        const Quad& q = C.h_adm[C.adm_begin + b];
-        const int m = q.rhi - q.rlo, n = q.chi - q.clo, k = C.h_rank[b];
-        const int64_t bytes = 8 * (int64_t)k * (m + n);
-        if (bytes <= std::min<int64_t>(C.mv_small_max, cap - 8 * n - 64) && m <= 2047 && n <= 2047 && k <= 1023)
-          P.items.push_back(Item{8 * C.h_foff[b], bytes, 1, q.rlo, q.clo, n,
-                                 (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)});
-        else
-          P.large.push_back(MvLarge{q.rlo, q.clo, m, n, k, 0, C.h_foff[b], 0});
-      }
-    }
-    P.batch(cap);
-  };
-  {
-    std::vector<std::thread> th;
-    std::vector<std::exception_ptr> err(T);
-    for (int t = 1; t < T; ++t)
-      th.emplace_back([&, t]() { try { work(t); } catch (...) { err[t] = std::current_exception(); } });
-    try { work(0); } catch (...) { err[0] = std::current_exception(); }
-    for (auto& x : th) x.join();
-    for (auto& e : err) if (e) std::rethrow_exception(e);
-  }
+  run_threads(Tl, [&](int t) { plan_lowrank_part(C, W, W.parts[Td + t], nlr * t / Tl, nlr * (t + 1) / Tl); });
   const auto t1 = clk::now();
   // join the parts: shift segment indices and task-stream offsets
   size_t nbat = 0, nseg = 0, nstr = 0, nlarge = 0, nbig = 0;
@@ -607,17 +655,30 @@ void plan_matvec(Context& C) {
   }
   W.batches.resize(nbat); W.segs.resize(nseg); W.stream.resize(nstr); W.large.resize(nlarge); W.dense_big.resize(nbig);
   {
-    size_t ob = 0, os = 0, ot = 0, ol = 0, od = 0;
-    int64_t tl = 0;
-    for (auto& P : W.parts) {
-      for (const MvBatch& B : P.batches) { MvBatch b = B; b.first_seg += (int32_t)os; W.batches[ob++] = b; }
-      for (const MvSeg& S : P.segs) { MvSeg g = S; if (g.base == 2) g.src += 16 * (int64_t)ot; W.segs[os++] = g; }
-      std::memcpy(W.stream.data() + ot, P.stream.data(), P.stream.size() * sizeof(MvTask));
-      ot += P.stream.size();
-      for (MvLarge L : P.large) { L.toff = tl; tl += L.k; W.large[ol++] = L; }
-      for (const MvLarge& L : P.dense_big) W.dense_big[od++] = L;
+    // per-part output offsets (exclusive prefix), then the parts are copied in parallel
+    const size_t np = W.parts.size();
+    std::vector<size_t> ob(np + 1, 0), os(np + 1, 0), ot(np + 1, 0), ol(np + 1, 0), od(np + 1, 0);
+    std::vector<int64_t> tl(np + 1, 0);
+    for (size_t p = 0; p < np; ++p) {
+      const PlanPart& P = W.parts[p];
+      ob[p + 1] = ob[p] + P.batches.size(); os[p + 1] = os[p] + P.segs.size();
+      ot[p + 1] = ot[p] + P.stream.size(); ol[p + 1] = ol[p] + P.large.size();
+      od[p + 1] = od[p] + P.dense_big.size();
+      int64_t ks = 0;
+      for (const MvLarge& L : P.large) ks += L.k;
+      tl[p + 1] = tl[p] + ks;
     }
-    C.mv_tlen = tl;
+    run_threads((int)np, [&](int p) {
+      const PlanPart& P = W.parts[p];
+      size_t b = ob[p], g = os[p], l = ol[p], d = od[p];
+      int64_t t = tl[p];
+      for (const MvBatch& B : P.batches) { MvBatch x = B; x.first_seg += (int32_t)os[p]; W.batches[b++] = x; }
+      for (const MvSeg& S : P.segs) { MvSeg x = S; if (x.base == 2) x.src += 16 * (int64_t)ot[p]; W.segs[g++] = x; }
+      std::memcpy(W.stream.data() + ot[p], P.stream.data(), P.stream.size() * sizeof(MvTask));
+      for (MvLarge L : P.large) { L.toff = t; t += L.k; W.large[l++] = L; }
+      for (const MvLarge& L : P.dense_big) W.dense_big[d++] = L;
+    });
+    C.mv_tlen = tl[np];
   }
   const auto t2 = clk::now();
   // byte-balanced contiguous batch ranges, one per persistent CTA (two or one per SM)
