@@ -16,6 +16,8 @@
  *   CG / GMRES    P:646, A17
  *   partition     P:563-568, A18
  *   RHS           P:230-231, A16
+ *   potential     P:176-177, A23           direct sum over panels
+ *   fixed rank    P:776, A24 (ACA with eps = 0)
  *
  * Pins (tests/test_oracle_*.py, all -m "not gpu"):
  *   Morton/sort/CBC   SPEC worked examples S:124-126; invariants (C1)-(C4)
@@ -31,6 +33,8 @@
  *   matvec            eta = 0 / N = 320 -> H = A exactly; ||Hx-Ax|| <= 10 eps vs dense
  *   solvers           identity/diag cases; V u = 1 on the sphere -> u ~ 1; vs Cholesky
  *   partition         union/disjoint/bound invariants
+ *   fixed-rank ACA    exactly K terms, interpolation at the pivots, error decreasing in K
+ *   potential         closed-form triangle potential per band; sphere interior u = 1 / u = f
  * No function here is "parity unpinned".
  */
 #include "oracle.h"
