@@ -120,6 +120,23 @@ def mesh_for(cfg):
     return config_mesh(cfg)
 
 
+class StdoutToStderr:
+    """Route the process's fd 1 to fd 2 while libraries initialise (NCCL may print its version
+    line to stdout), so the only line on stdout is the JSON result."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 def dist_init(n_gpus):
     import torch
     import torch.distributed as dist
@@ -153,7 +170,8 @@ def barrier(world):
 # ------------------------------------------------------------------------------------------
 def run_gpu(args):
     import torch
-    rank, world, local = dist_init(args.gpus)
+    with StdoutToStderr():
+        rank, world, local = dist_init(args.gpus)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
@@ -168,13 +186,15 @@ def _run_gpu(args, rank, world, local, dev, stream):
     if world > 1:
         import torch.distributed as dist
         obj = [hm.hm_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
+        with StdoutToStderr():                       # torch's lazy NCCL init happens here
+            dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     V, T = mesh_for(args.config)
     N = T.shape[0]
     Vd = torch.from_numpy(V).to(dev)
     Td = torch.from_numpy(T).to(dev)
-    H = HMatrix(device=local, rank=rank, world_size=world, nccl_unique_id=nid, cuda_stream=stream.cuda_stream)
+    with StdoutToStderr():
+        H = HMatrix(device=local, rank=rank, world_size=world, nccl_unique_id=nid, cuda_stream=stream.cuda_stream)
     H.N = N
     H.set_option("solver", 0)
     H.set_option("restart", 100)
