@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(256) k_aca_update(const AcaBlk* __restrict__ B
 }
 
 // G = 8: one CTA per big block of the chunk (list fixed per chunk; finished blocks return)
-__global__ void __launch_bounds__(256) k_aca_update_big(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
+__global__ void __launch_bounds__(256, 3) k_aca_update_big(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
                                                         const int32_t* __restrict__ big, const double* __restrict__ Uw,
                                                         const double* __restrict__ Vw, const uint32_t* __restrict__ bmap,
                                                         int32_t* __restrict__ piv, int kws, double eps) {
@@ -674,10 +674,12 @@ void setup_aca(Context& C) {
   C.times.aca_phase_ms[8] = ms_since(t0);
   // reserve VA for the worst case (k_max terms per block), map on demand
   size_t worst = 0;
+  int64_t sum_mn = 0;
   for (int64_t b = C.adm_begin; b < C.adm_end; ++b) {
     const Quad& q = C.h_adm[b];
     int64_t m = q.rhi - q.rlo, n = q.chi - q.clo;
     worst += (size_t)std::min<int64_t>(std::min(m, n), C.k_max) * (m + n);
+    sum_mn += m + n;
   }
   const size_t need_va = worst * sizeof(double) + (64u << 20);
   if (!C.fpool.base || C.fpool.reserved < need_va) C.fpool.init(C.device, need_va);   // else reuse the mapped pool
@@ -711,6 +713,10 @@ void setup_aca(Context& C) {
   // pool stays mapped (slack ~ all factors), so chunks can use most of the free memory.
   // The allocated workspace is kept (no multi-GB free/malloc, tens to hundreds of ms) while
   // it is at most twice the budget and the factor growth still fits in the free memory.
+  // the same owned block list (signature) with the same ACA options as the previous setup
+  const bool steady = C.aca_prev_valid && C.aca_prev_eps == C.eps_aca && C.aca_prev_kmax == C.k_max &&
+                      C.aca_prev_sig[0] == nb && C.aca_prev_sig[1] == sum_mn;
+  const double prev_bytes = steady ? C.aca_prev_bytes : 0.0;   // deterministic ACA: the same factor bytes
   auto chunk_budget = [&]() {
     const auto tb0 = clk::now();
     struct Acc { double& t; clk::time_point a; ~Acc() { t += std::chrono::duration<double, std::milli>(clk::now() - a).count(); } };
@@ -722,8 +728,22 @@ void setup_aca(Context& C) {
     double b = std::min(C.aca_chunk_mb * 1048576.0, 0.9 * room);
     if (b - slack > room - b) b = 0.5 * (room + slack);
     b = std::max(std::min(b, 0.9 * room), 64.0 * 1048576.0);
-    if (ws > 2.0 * b || (ws > b && b - slack > free_b)) { W.ws.release(); C.aca_releases++; }
-    else if (ws >= 0.5 * b) b = std::min(b, ws);     // reuse the allocated workspace as it is
+    if (ws > 0) {
+      // Reuse the allocated workspace (freeing / allocating tens of GB costs ~1 s each): chunks
+      // of at most its size, provided their factor growth still fits in free memory beside it.
+      // Only a too-small buffer (< 1/4 of the budget) is regrown, and it is released only when
+      // the pool cannot grow otherwise.
+      const double bu = std::min(b, ws);
+      // factor growth still to be mapped: known exactly when this tree was set up before with
+      // the same options (ACA is deterministic), else bounded by the chunk's workspace bytes
+      const double growth = steady ? std::max(0.0, prev_bytes - (double)C.fpool.mapped) : bu - slack;
+      if (growth <= free_b) {
+        if (ws >= 0.25 * b) b = bu;
+      } else {
+        W.ws.release();
+        C.aca_releases++;
+      }
+    }
     return b;
   };
   double budget = chunk_budget();
@@ -779,6 +799,12 @@ void setup_aca(Context& C) {
   HM_CUDA(cudaStreamSynchronize(st));
   C.evals_aca = (double)hev;
   C.factor_doubles = (int64_t)(C.fpool.used / sizeof(double));
+  C.aca_prev_valid = true;
+  C.aca_prev_sig[0] = nb;
+  C.aca_prev_sig[1] = sum_mn;
+  C.aca_prev_bytes = (double)C.fpool.used;
+  C.aca_prev_eps = C.eps_aca;
+  C.aca_prev_kmax = C.k_max;
   C.times.aca_phase_ms[5] = ms_since(t5);
 }
 

@@ -253,6 +253,10 @@ struct Context {
   int64_t dense_doubles = 0, factor_doubles = 0;
   double evals_near = 0, evals_aca = 0, entries_aca = 0;
   int aca_steps = 0, aca_chunks = 0, aca_overflow = 0, aca_releases = 0;
+  bool aca_prev_valid = false;   // a previous hm_setup of the same owned block list: its pool size
+  int64_t aca_prev_sig[2] = {0, 0};
+  double aca_prev_bytes = 0, aca_prev_eps = -1;
+  int aca_prev_kmax = 0;
 
   // matvec plan (matvec.cu)
   DBuf<MvBatch> mv_batches;
