@@ -3,7 +3,11 @@
 // message retrievable with hm_last_error.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cstring>
+#include <exception>
+#include <thread>
 #include <sstream>
 
 #include "entry.cuh"
@@ -131,21 +135,56 @@ cudaEvent_t KTimer::get() {
   pool.pop_back();
   return e;
 }
+void KTimer::mark(cudaStream_t st) {
+  if (!on) return;
+  if (!ref) ref = get();
+  cudaEventRecord(ref, st);
+}
+void KTimer::adopt(KTimer& o) {
+  pend.insert(pend.end(), o.pend.begin(), o.pend.end());
+  o.pend.clear();
+}
 void KTimer::resolve() {
+  std::vector<std::pair<double, double>> ev;   // eval-family intervals from ref
+  double ev_sum = 0;
   for (auto& p : pend) {
     float t = 0;
-    if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) { ms[p.fam] += t; n[p.fam] += 1; }
-    else cudaGetLastError();
+    if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
+      ms[p.fam] += t;
+      n[p.fam] += 1;
+      if (p.fam == KF_EVAL_NEAR || p.fam == KF_EVAL_ACA) {
+        ev_sum += t;
+        float t0 = 0;
+        if (ref && cudaEventElapsedTime(&t0, ref, p.a) == cudaSuccess) ev.emplace_back(t0, (double)t0 + t);
+        else cudaGetLastError();
+      }
+    } else {
+      cudaGetLastError();
+    }
     pool.push_back(p.a);
     pool.push_back(p.b);
   }
   pend.clear();
+  if (ref && ev.size()) {   // union of the intervals
+    std::sort(ev.begin(), ev.end());
+    double u = 0, lo = ev[0].first, hi = ev[0].second;
+    for (auto& iv : ev) {
+      if (iv.first > hi) { u += hi - lo; lo = iv.first; hi = iv.second; }
+      else hi = std::max(hi, iv.second);
+    }
+    eval_union_ms += u + (hi - lo);
+  } else {
+    eval_union_ms += ev_sum;
+  }
+  if (ref) { pool.push_back(ref); ref = nullptr; }
 }
 void KTimer::reset() {
   for (int f = 0; f < KF_NUM; ++f) { ms[f] = 0; n[f] = 0; }
+  eval_union_ms = 0;
 }
 KTimer::~KTimer() {
   for (auto& p : pend) { pool.push_back(p.a); pool.push_back(p.b); }
+  if (ref) pool.push_back(ref);
   for (auto e : pool) cudaEventDestroy(e);
 }
 
@@ -284,6 +323,12 @@ hm_status hm_destroy(hm_ctx ctx) {
   if (ctx->C.comm) ncclCommDestroy(ctx->C.comm);
   bool own = ctx->C.own_stream;
   cudaStream_t st = ctx->C.stream;
+  {
+    hm::Context& C = ctx->C;
+    if (C.s_hi) { cudaStreamSynchronize(C.s_hi); cudaStreamDestroy(C.s_hi); }
+    if (C.s_lo) { cudaStreamSynchronize(C.s_lo); cudaStreamDestroy(C.s_lo); }
+    for (cudaEvent_t e : {C.ev_fork, C.ev_join[0], C.ev_join[1]}) if (e) cudaEventDestroy(e);
+  }
   delete ctx;
   if (own && st) cudaStreamDestroy(st);
   return HM_OK;
@@ -311,6 +356,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     }
     else if (k == "mv_small_max") { if (v < 0 || v > 49152) bad(); C.mv_small_max = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_scramble") { if (v != 0 && v != 1) bad(); C.mv_scramble = (int)v; }
+    else if (k == "setup_overlap") { if (v != 0 && v != 1) bad(); C.setup_overlap = (int)v; }
     else if (k == "kernel_timing") {
       if (v != 0 && v != 1) bad();
       HM_CUDA(cudaStreamSynchronize(C.stream));
@@ -335,6 +381,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "record_pivots") *v = C.record_pivots;
     else if (k == "kernel_timing") *v = C.kt.on ? 1 : 0;
     else if (k == "mv_kernel") *v = C.mv_kind;
+    else if (k == "setup_overlap") *v = C.setup_overlap;
     else hm::fail(HM_ERR_ARG, "hm_get_option: unknown key '" + k + "'");
   });
 }
@@ -353,6 +400,62 @@ hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double e
   });
 }
 
+// Near field beside ACA: the near-field evaluation (a few tens of launches of long FP64
+// kernels) runs on a least-priority stream from its own host thread while ACA's lock-step
+// loop drives a greatest-priority stream, so the near-field CTAs fill the SM time ACA leaves
+// idle (its pivot/update/compaction launches, host round trips and chunk tails) and yield
+// to every ACA launch.  Both write disjoint storage; results are identical to the serial
+// order.  near_ms is the near-field thread's own span, aca_ms ACA's.
+static void run_overlapped(Context& C) {
+  if (!C.s_hi) {
+    int least = 0, greatest = 0;
+    HM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    HM_CUDA(cudaStreamCreateWithPriority(&C.s_hi, cudaStreamNonBlocking, greatest));
+    HM_CUDA(cudaStreamCreateWithPriority(&C.s_lo, cudaStreamNonBlocking, least));
+    HM_CUDA(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
+    HM_CUDA(cudaEventCreateWithFlags(&C.ev_join[0], cudaEventDisableTiming));
+    HM_CUDA(cudaEventCreateWithFlags(&C.ev_join[1], cudaEventDisableTiming));
+  }
+  HM_CUDA(cudaEventRecord(C.ev_fork, C.stream));
+  HM_CUDA(cudaStreamWaitEvent(C.s_hi, C.ev_fork, 0));
+  HM_CUDA(cudaStreamWaitEvent(C.s_lo, C.ev_fork, 0));
+  C.kt.mark(C.stream);
+  C.kt_near.on = C.kt.on;
+  std::exception_ptr near_err;
+  std::thread th([&C, &near_err]() {
+    try {
+      HM_CUDA(cudaSetDevice(C.device));
+      const auto t0 = std::chrono::steady_clock::now();
+      hm::near_eval(C, C.s_lo, C.kt_near);
+      C.near_eval_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    } catch (...) {
+      near_err = std::current_exception();
+    }
+  });
+  cudaStream_t user = C.stream;
+  C.stream = C.s_hi;
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    hm::setup_aca(C);
+  } catch (...) {
+    C.stream = user;
+    th.join();
+    cudaStreamSynchronize(C.s_lo);
+    throw;
+  }
+  HM_CUDA(cudaStreamSynchronize(C.s_hi));
+  C.times.aca_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  C.stream = user;
+  th.join();
+  if (near_err) std::rethrow_exception(near_err);
+  C.times.near_ms = C.near_eval_ms;
+  HM_CUDA(cudaEventRecord(C.ev_join[0], C.s_hi));
+  HM_CUDA(cudaEventRecord(C.ev_join[1], C.s_lo));
+  HM_CUDA(cudaStreamWaitEvent(C.stream, C.ev_join[0], 0));
+  HM_CUDA(cudaStreamWaitEvent(C.stream, C.ev_join[1], 0));
+  C.kt.adopt(C.kt_near);
+}
+
 hm_status hm_setup(hm_ctx ctx, double eps_aca) {
   return guarded(ctx, [&](Context& C) {
     need_tree(C);
@@ -360,17 +463,21 @@ hm_status hm_setup(hm_ctx ctx, double eps_aca) {
     C.have_setup = false;
     C.eps_aca = eps_aca;
     Timer all(C);
-    {
-      Timer t(C);
-      hm::setup_nearfield(C);
-      C.times.near_ms = t.ms();
-    }
+    hm::near_prepare(C);
     hm::plan_dense_begin(C);
-    {
+    if (C.setup_overlap && C.dense_doubles > 0) {
+      run_overlapped(C);
+    } else {
+      {
+        Timer t(C);
+        hm::near_eval(C, C.stream, C.kt);
+        C.times.near_ms = t.ms();
+      }
       Timer t(C);
       hm::setup_aca(C);
       C.times.aca_ms = t.ms();
     }
+    hm::near_check(C);
     {
       Timer t(C);
       hm::plan_matvec(C);
@@ -614,7 +721,7 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
     const char* fam[hm::KF_NUM] = {"eval_near", "eval_aca", "aca_other", "matvec", "krylov"};
     for (int f = 0; f < hm::KF_NUM; ++f)
       o << ",\"" << fam[f] << "_ms\":" << C.kt.ms[f] << ",\"" << fam[f] << "_n\":" << C.kt.n[f];
-    o << "}}";
+    o << ",\"eval_union_ms\":" << C.kt.eval_union_ms << "}}";
     std::string s = o.str();
     if (!buf || len < (int64_t)s.size() + 1)
       hm::fail(HM_ERR_ARG, "hm_get_stats: buffer too small, need " + std::to_string(s.size() + 1));

@@ -257,11 +257,11 @@ struct EntryBatchWork {
   unsigned long long hcnt[kNumClass];
 };
 
-// Evaluate all `total` entries of mapping m; returns the number of kernel evaluations.
+// Evaluate all `total` entries of mapping m on stream st; returns the number of kernel
+// evaluations.  Allocates only when W is smaller than this batch (near_prepare pre-sizes it).
 template <class M>
-double eval_batched(Context& C, const M& m, int64_t total, EntryBatchWork& W) {
+double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t st, KTimer& kt) {
   if (total <= 0) return 0.0;
-  cudaStream_t st = C.stream;
   W.cnt.alloc(kNumClass);
   W.cursor.alloc(kNumClass);
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, kNumClass * sizeof(unsigned long long), st));
@@ -278,7 +278,7 @@ double eval_batched(Context& C, const M& m, int64_t total, EntryBatchWork& W) {
   const EntryRef* L = W.list.get();
   double evals = 0;
   // heavy classes first so that the light ones fill the tail
-  KScope ks(C, KF_EVAL_NEAR);
+  KScope ks(kt, st, KF_EVAL_NEAR);
   if (W.hcnt[1]) { k_eval_touching<1, M><<<grid_for(W.hcnt[1], 64), 64, 0, st>>>(m, L + base[1], W.hcnt[1]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[2]) { k_eval_touching<2, M><<<grid_for(W.hcnt[2], 64), 64, 0, st>>>(m, L + base[2], W.hcnt[2]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[6]) { k_eval_regular<6, M><<<grid_for(W.hcnt[6], 128), 128, 0, st>>>(m, L + base[6], W.hcnt[6]); HM_CHECK_LAUNCH(); }

@@ -191,17 +191,24 @@ struct PhaseTimes {
 };
 
 // Per-kernel-family device timing (option "kernel_timing"): CUDA events recorded on the
-// library stream around every launch of a family, resolved at the next synchronous point.
+// launching stream around every launch of a family, resolved at the next synchronous point.
+// When the near field runs beside ACA (option setup_overlap) the two evaluation families
+// overlap in time; eval_union_ms is the length of the union of their intervals, measured
+// against a reference event recorded before the streams fork (mark()).
 enum KFam { KF_EVAL_NEAR = 0, KF_EVAL_ACA = 1, KF_ACA_OTHER = 2, KF_MATVEC = 3, KF_KRYLOV = 4, KF_NUM = 5 };
 struct KTimer {
   bool on = false;
   std::vector<cudaEvent_t> pool;
   struct P { int fam; cudaEvent_t a, b; };
   std::vector<P> pend;
+  cudaEvent_t ref = nullptr;   // set by mark(): intervals of this batch measured from it
   double ms[KF_NUM] = {0, 0, 0, 0, 0};
   int64_t n[KF_NUM] = {0, 0, 0, 0, 0};
+  double eval_union_ms = 0;
   cudaEvent_t get();
-  void resolve();   // caller has synchronised the stream
+  void mark(cudaStream_t st);
+  void adopt(KTimer& o);   // move o's pending intervals into this timer (o's thread has joined)
+  void resolve();   // caller has synchronised the streams
   void reset();
   ~KTimer();
 };
@@ -288,6 +295,14 @@ struct Context {
   DBuf<int32_t> near_tab;
   DBuf<char> near_tmp;
   std::shared_ptr<EntryBatchWork> near_ws;
+  std::vector<int64_t> near_hoff;   // host copy of doff (near_prepare)
+  // near field beside ACA (option setup_overlap): ACA on s_hi (greatest priority), the
+  // near-field evaluation on s_lo (least priority) from its own host thread and timer
+  int setup_overlap = 0;
+  cudaStream_t s_hi = nullptr, s_lo = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  KTimer kt_near;
+  double near_eval_ms = 0;          // host time of the near-field evaluation (its own thread)
   std::shared_ptr<AcaWork> aca_ws;
   std::shared_ptr<PlanWs> plan_ws;
   int64_t mv_n_large = 0, mv_n_dense_big = 0, mv_n_tiles_v = 0, mv_n_tiles_u = 0;
@@ -299,24 +314,28 @@ struct Context {
 
 // scope = one timed launch (or a group of launches) of family f on the library stream
 struct KScope {
-  Context& C;
+  KTimer& kt;
+  cudaStream_t st;
   int f;
   cudaEvent_t a = nullptr;
-  KScope(Context& c, int fam) : C(c), f(fam) {
-    if (C.kt.on) { a = C.kt.get(); cudaEventRecord(a, C.stream); }
+  KScope(KTimer& t, cudaStream_t s, int fam) : kt(t), st(s), f(fam) {
+    if (kt.on) { a = kt.get(); cudaEventRecord(a, st); }
   }
+  KScope(Context& c, int fam) : KScope(c.kt, c.stream, fam) {}
   ~KScope() {
     if (!a) return;
-    cudaEvent_t b = C.kt.get();
-    cudaEventRecord(b, C.stream);
-    C.kt.pend.push_back(KTimer::P{f, a, b});
+    cudaEvent_t b = kt.get();
+    cudaEventRecord(b, st);
+    kt.pend.push_back(KTimer::P{f, a, b});
   }
 };
 
 // tree.cu
 void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta);
 // nearfield.cu
-void setup_nearfield(Context& C);
+void near_prepare(Context& C);                                 // sizes, offsets, storage (synchronous)
+void near_eval(Context& C, cudaStream_t st, KTimer& kt);       // evaluation, no allocation; syncs st
+void near_check(Context& C);                                   // non-finite check (C.stream)
 // aca.cu
 void setup_aca(Context& C);
 // matvec.cu

@@ -51,7 +51,14 @@ __global__ void k_check_finite(const double* __restrict__ a, int64_t n, unsigned
 
 }  // namespace
 
-void setup_nearfield(Context& C) {
+// Chunks of at most 2^26 entries (at least one leaf each) over the owned dense leaves.
+static constexpr int64_t kNearChunk = 1LL << 26;
+static int64_t near_chunk_end(const std::vector<int64_t>& hoff, int64_t nb, int64_t b0) {
+  int64_t b1 = std::upper_bound(hoff.begin() + b0 + 1, hoff.begin() + nb + 1, hoff[b0] + kNearChunk) - hoff.begin() - 1;
+  return std::max(b1, b0 + 1);
+}
+
+void near_prepare(Context& C) {
   cudaStream_t st = C.stream;
   const int64_t nb = C.dense_end - C.dense_begin;
   const Quad* q = C.dense.get() + C.dense_begin;
@@ -68,7 +75,8 @@ void setup_nearfield(Context& C) {
   HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sz.get(), C.doff.get(), nb + 1, st));
   tmp.alloc(bytes);
   HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, sz.get(), C.doff.get(), nb + 1, st));
-  std::vector<int64_t> hoff(nb + 1);
+  std::vector<int64_t>& hoff = C.near_hoff;
+  hoff.assign(nb + 1, 0);
   HM_CUDA(cudaMemcpyAsync(hoff.data(), C.doff.get(), (nb + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
   const int64_t total = hoff[nb];
@@ -76,20 +84,45 @@ void setup_nearfield(Context& C) {
   C.dstore.alloc(total);
   C.evals_near = 0;
   if (total == 0) return;
+  // pre-size the evaluation workspace for the largest chunk, so that the evaluation (which
+  // may run on its own thread beside ACA) never allocates
+  int64_t maxc = 0;
+  for (int64_t b0 = 0; b0 < nb;) {
+    const int64_t b1 = near_chunk_end(hoff, nb, b0);
+    maxc = std::max(maxc, hoff[b1] - hoff[b0]);
+    b0 = b1;
+  }
   if (!C.near_ws) C.near_ws = std::make_shared<EntryBatchWork>();
   EntryBatchWork& W = *C.near_ws;
-  const int64_t chunk = 1LL << 26;
+  W.cnt.alloc(kNumClass);
+  W.cursor.alloc(kNumClass);
+  W.list.alloc(maxc);
+  C.near_tab.alloc(maxc / 32 + 2);
+}
+
+void near_eval(Context& C, cudaStream_t st, KTimer& kt) {
+  const int64_t nb = C.dense_end - C.dense_begin;
+  const std::vector<int64_t>& hoff = C.near_hoff;
+  if (nb == 0 || hoff[nb] == 0) return;
+  const Quad* q = C.dense.get() + C.dense_begin;
+  EntryBatchWork& W = *C.near_ws;
+  double evals = 0;
   for (int64_t b0 = 0; b0 < nb;) {
-    // leaves [b0, b1) with at most `chunk` entries (at least one leaf)
-    int64_t b1 = std::upper_bound(hoff.begin() + b0 + 1, hoff.begin() + nb + 1, hoff[b0] + chunk) - hoff.begin() - 1;
-    b1 = std::max(b1, b0 + 1);
-    C.near_tab.alloc((hoff[b1] - hoff[b0]) / 32 + 2);
+    const int64_t b1 = near_chunk_end(hoff, nb, b0);
     k_seg_table<<<grid_for(b1 - b0, 256), 256, 0, st>>>(C.doff.get() + b0, b1 - b0, hoff[b0], C.near_tab.get());
     HM_CHECK_LAUNCH();
     NearMap m{C.panel.get(), q, C.doff.get(), b0, b1 - b0, hoff[b0], C.dstore.get(), C.near_tab.get()};
-    C.evals_near += eval_batched(C, m, hoff[b1] - hoff[b0], W);
+    evals += eval_batched(m, hoff[b1] - hoff[b0], W, st, kt);
     b0 = b1;
   }
+  HM_CUDA(cudaStreamSynchronize(st));
+  C.evals_near = evals;
+}
+
+void near_check(Context& C) {
+  cudaStream_t st = C.stream;
+  const int64_t total = C.dense_doubles;
+  if (total == 0) return;
   DBuf<unsigned long long> bad;
   bad.alloc(1);
   HM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), st));

@@ -227,6 +227,35 @@ def test_c2_solve_vs_oracle(c2):
     assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-5 * np.linalg.norm(xo)
 
 
+def test_setup_overlap_bit_identical(c2):
+    # near field beside ACA (option setup_overlap, default off) vs the serial order: every
+    # stored entry and factor identical, and the kernel-timing union of the two evaluation
+    # families no longer than their sum and no shorter than either
+    V, T, H, R = c2
+    G = _gpu(V, T)
+    assert G.get_option("setup_overlap") == 0
+    G.set_option("setup_overlap", 1)
+    G.setup(EPS)
+    H, G = G, H          # H: overlapped, G: serial (the fixture's)
+    dense, _ = H.leaves(1)
+    for b, q in enumerate(dense):
+        shape = (q[1] - q[0], q[3] - q[2])
+        assert np.array_equal(H.dense_block(b, shape), G.dense_block(b, shape)), f"dense block {b}"
+    adm, _ = H.leaves(0)
+    for b in range(0, len(adm), max(1, len(adm) // 200)):
+        m, n = adm[b][1] - adm[b][0], adm[b][3] - adm[b][2]
+        U1, W1 = H.lowrank(b, m, n)
+        U0, W0 = G.lowrank(b, m, n)
+        assert np.array_equal(U1, U0) and np.array_equal(W1, W0), f"low-rank block {b}"
+    H.set_option("kernel_timing", 1)
+    H.setup(EPS)
+    kt = H.stats()["kt"]
+    H.set_option("kernel_timing", 0)
+    s = kt["eval_near_ms"] + kt["eval_aca_ms"]
+    assert max(kt["eval_near_ms"], kt["eval_aca_ms"]) * 0.999 <= kt["eval_union_ms"] <= s * 1.001
+    H.close()
+
+
 def test_c3_full_size_sampled_rows(O, torch_cuda):
     # configs[2] at full size, in the launch configuration bench.py times
     import torch

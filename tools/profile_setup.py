@@ -12,8 +12,12 @@ H = HMatrix(device=0)
 H.build_tree(V, T, 32, 1.0)
 if os.environ.get("HM_KT"):
     H.set_option("kernel_timing", 1)
+if os.environ.get("HM_OVERLAP"):
+    H.set_option("setup_overlap", int(os.environ["HM_OVERLAP"]))
 for _ in range(int(os.environ.get("HM_SETUPS", "1"))):
     H.setup(1e-6)
+    st = H.stats()
+    print("setup_ms", st["setup_ms"], "near_ms", st["near_ms"], "aca_ms", st["aca_ms"], flush=True)
 x = torch.randn(T.shape[0], dtype=torch.float64, device="cuda")
 for _ in range(nmv):
     y = H.matvec(x)
