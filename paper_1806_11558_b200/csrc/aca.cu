@@ -317,21 +317,21 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
   const double* u = U + (int64_t)st.k * b.m;
   const double* v = V + (int64_t)st.k * b.n;
   const int t0 = gw * 32 + lane, stride = G * 32;
-  double uu = 0.0;
-  for (int t = t0; t < b.m; t += stride) uu = fma(u[t], u[t], uu);
-  uu = warp_sum(uu);
+  double uu = 0.0;   // ||u_k||^2, accumulated in the first pass over u (one pass also when k = 0)
   double cross = 0.0;
-  for (int l0 = 0; l0 < st.k; l0 += 8) {
+  for (int l0 = 0; l0 < max(st.k, 1); l0 += 8) {
     const int kc = min(8, st.k - l0);
     double acc[16];
 #pragma unroll
     for (int l = 0; l < 16; ++l) acc[l] = 0.0;
     for (int t = t0; t < b.m; t += stride) {
       const double ut = u[t];
+      if (l0 == 0) uu = fma(ut, ut, uu);
 #pragma unroll
       for (int l = 0; l < 8; ++l)
         if (l < kc) acc[l] = fma(ut, U[t + (int64_t)(l0 + l) * b.m], acc[l]);
     }
+    if (kc <= 0) break;
     for (int j = t0; j < b.n; j += stride) {
       const double vj = v[j];
 #pragma unroll
@@ -356,6 +356,7 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
       cross += warp_sum(part);
     }
   }
+  uu = warp_sum(uu);
   if (G > 1) {
     if (lane == 0) red[gw * 17 + 16] = uu;
     __syncthreads();
@@ -399,7 +400,7 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
 }
 
 // G = 1: one warp per active block (small blocks; big ones are skipped), act[] = compact list
-__global__ void __launch_bounds__(256) k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
+__global__ void __launch_bounds__(64, 16) k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
                                                     const int32_t* __restrict__ act, int64_t nact,
                                                     const double* __restrict__ Uw, const double* __restrict__ Vw,
                                                     const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv,
@@ -409,15 +410,15 @@ __global__ void __launch_bounds__(256) k_aca_update(const AcaBlk* __restrict__ B
   if (a >= nact) return;
   const int64_t c = act[a];
   AcaState st = S[c];
-  if (st.status != 0 || st.skip) return;
   const AcaBlk b = B[c];
+  if (st.status != 0 || st.skip) return;
   if (b.m + b.n >= kBigMN) return;
   aca_update_block<1>(b, st, Uw, Vw, bmap, piv, c, kws, eps, 0, lane, nullptr);
   if (lane == 0) S[c] = st;
 }
 
 // G = 8: one CTA per big block of the chunk (list fixed per chunk; finished blocks return)
-__global__ void __launch_bounds__(256, 3) k_aca_update_big(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
+__global__ void __launch_bounds__(256, 4) k_aca_update_big(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
                                                         const int32_t* __restrict__ big, const double* __restrict__ Uw,
                                                         const double* __restrict__ Vw, const uint32_t* __restrict__ bmap,
                                                         int32_t* __restrict__ piv, int kws, double eps) {
@@ -596,7 +597,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(), nb, Uw, Vw},
              tot[1], W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_update<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, Uw,
+    k_aca_update<<<grid_for(nact * 32, 64), 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, Uw,
                                                            Vw, W.bmap.get(), W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();
     if (nbig) {
