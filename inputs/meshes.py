@@ -16,6 +16,10 @@ Meshes:
   * lobed(nu)       - geodesic(nu) pushed out radially by six Gaussian lobes
                       and stretched to the gearwheel's bounding box
                       (configs[4]: nu = 244 -> 1,190,720).
+  * cube(L)         - surface of the unit cube [0,1]^3 (the paper's model geometry,
+                      PAPER.md §4), every face split into 2^L x 2^L squares:
+                      N = 6*4^L QUADRILATERALS, int32 [N, 4] in cyclic order
+                      (the paper's N = 1536 ... 1,572,864 for L = 4 ... 9; "C6" = L = 9).
 All meshes are vertex-deduplicated (the entry classification of PAPER.md
 §4.1 "Duffy trick" needs shared vertex *indices*) and consistently oriented
 (outward normals), vertices float64 [n_v, 3], triangles int32 [N, 3].
@@ -24,7 +28,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["icosahedron", "icosphere", "geodesic", "lobed", "config_mesh",
+__all__ = ["icosahedron", "icosphere", "geodesic", "lobed", "cube", "config_mesh",
            "seeded_vector", "CONFIGS"]
 
 
@@ -139,19 +143,59 @@ def lobed(nu: int):
     return np.ascontiguousarray(x, dtype=np.float64), f
 
 
-# BASELINE.json configs -> mesh recipe
+def cube(level: int):
+    """Unit cube surface, 6 faces x (2^L)^2 squares; vertices i/2^L (exact binary), shared
+    along the cube edges; quads (q0,q1,q2,q3) counter-clockwise seen from outside."""
+    n = 2 ** level
+    g = np.arange(n + 1)
+    quads, keys = [], []
+    for axis in range(3):
+        for side in (0, n):
+            u, v = np.meshgrid(g[:-1], g[:-1], indexing="ij")
+            u, v = u.ravel(), v.ravel()
+            corners = [(u, v), (u + 1, v), (u + 1, v + 1), (u, v + 1)]
+            pts = []
+            for cu, cv in corners:
+                ijk = np.empty((u.size, 3), dtype=np.int64)
+                ijk[:, axis] = side
+                ijk[:, (axis + 1) % 3] = cu
+                ijk[:, (axis + 2) % 3] = cv
+                pts.append(ijk)
+            q = np.stack(pts, axis=1)                        # [nq, 4, 3] lattice points
+            # outward: normal of (q0,q1,q2) along +axis on side n, -axis on side 0
+            e1, e2 = q[:, 1] - q[:, 0], q[:, 2] - q[:, 0]
+            nrm = np.cross(e1, e2)[:, axis]
+            if (nrm[0] > 0) != (side == n):
+                q = q[:, ::-1]
+            quads.append(q)
+    q = np.concatenate(quads, axis=0)
+    key = (q[..., 0] * (n + 1) + q[..., 1]) * (n + 1) + q[..., 2]
+    uk, inv = np.unique(key.ravel(), return_inverse=True)
+    k = uk.copy()
+    z = k % (n + 1); k //= n + 1
+    y = k % (n + 1); x = k // (n + 1)
+    verts = np.stack([x, y, z], axis=1).astype(np.float64) / n
+    return np.ascontiguousarray(verts), np.ascontiguousarray(inv.reshape(-1, 4), dtype=np.int32)
+
+
+# BASELINE.json configs -> mesh recipe (SURVEY.md §8(d)); C6 = the paper's own model case
+# (SURVEY.md §8(f) rank 1), outside BASELINE.json's list
 CONFIGS = {
     "C1": ("icosphere", 3),      # 1,280 triangles
     "C2": ("icosphere", 5),      # 20,480
     "C3": ("icosphere", 7),      # 327,680
     "C4": ("geodesic", 280),     # 1,568,000
     "C5": ("lobed", 244),        # 1,190,720
+    "C6": ("cube", 9),           # 1,572,864 quadrilaterals
 }
 
 
 def config_mesh(name: str):
+    """Config name -> mesh; also "cube<L>" for the cube convergence study (L = 0 ... 9)."""
+    if name.startswith("cube"):
+        return cube(int(name[4:]))
     kind, p = CONFIGS[name]
-    return {"icosphere": icosphere, "geodesic": geodesic, "lobed": lobed}[kind](p)
+    return {"icosphere": icosphere, "geodesic": geodesic, "lobed": lobed, "cube": cube}[kind](p)
 
 
 def seeded_vector(n: int, seed: int):

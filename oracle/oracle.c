@@ -18,6 +18,7 @@
  *   RHS           P:230-231, A16
  *   potential     P:176-177, A23           direct sum over panels
  *   fixed rank    P:776, A24 (ACA with eps = 0)
+ *   quad panels   P:700, A25 (each quad = two triangles; sums of their entries)
  *
  * Pins (tests/test_oracle_*.py, all -m "not gpu"):
  *   Morton/sort/CBC   SPEC worked examples S:124-126; invariants (C1)-(C4)
@@ -35,6 +36,9 @@
  *   partition         union/disjoint/bound invariants
  *   fixed-rank ACA    exactly K terms, interpolation at the pivots, error decreasing in K
  *   potential         closed-form triangle potential per band; sphere interior u = 1 / u = f
+ *   quad panels       unit-square self integral (closed form); square pairs vs the exact
+ *                     rectangle potential + graded outer rule; exact f integrals; cube
+ *                     interior u = f at the paper's convergence rate N^-1.3
  * No function here is "parity unpinned".
  */
 #include "oracle.h"
@@ -86,6 +90,11 @@ struct or_problem {
   int32_t** piv;      /* per adm leaf, 2k */
   int* rank;          /* per adm leaf, -1 if not owned */
   double counters[4];
+  /* quadrilateral meshes (A25): Q = N*4 vertex ids; tri = the split triangle problem
+   * (2N triangles, quad i -> triangles 2i = (q0,q1,q2) and 2i+1 = (q0,q2,q3)) that
+   * evaluates the entries, right-hand side and potential; NULL for triangle meshes */
+  int32_t* Q;
+  or_problem* tri;
 };
 
 /* ------------------------------------------------------------------ */
@@ -229,21 +238,68 @@ static void build_block(or_problem* P, int32_t t, int32_t s) {
   }
 }
 
-or_problem* or_create(const double* V, int64_t n_v, const int32_t* T, int64_t N,
-                      int leaf_size, double eta) {
+static or_problem* alloc_problem(const double* V, int64_t n_v, int64_t N, int leaf_size, double eta) {
   or_problem* P = (or_problem*)calloc(1, sizeof(or_problem));
   P->N = N; P->nv = n_v; P->leaf_size = leaf_size; P->eta = eta;
-  P->V = (double*)malloc((size_t)n_v * 3 * sizeof(double));
+  P->V = (double*)malloc((size_t)(n_v > 0 ? n_v : 1) * 3 * sizeof(double));
   memcpy(P->V, V, (size_t)n_v * 3 * sizeof(double));
-  P->T = (int32_t*)malloc((size_t)(N > 0 ? N : 1) * 3 * sizeof(int32_t));
-  if (N > 0) memcpy(P->T, T, (size_t)N * 3 * sizeof(int32_t));
   P->cen = (double*)malloc((size_t)(N > 0 ? N : 1) * 3 * sizeof(double));
   P->area = (double*)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
   P->h = (double*)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
   P->code = (uint64_t*)malloc((size_t)(N > 0 ? N : 1) * sizeof(uint64_t));
   P->perm = (int32_t*)malloc((size_t)(N > 0 ? N : 1) * sizeof(int32_t));
+  return P;
+}
+
+static void order_and_trees(or_problem* P, int build_trees);
+
+or_problem* or_create(const double* V, int64_t n_v, const int32_t* T, int64_t N,
+                      int leaf_size, double eta) {
+  or_problem* P = alloc_problem(V, n_v, N, leaf_size, eta);
+  P->T = (int32_t*)malloc((size_t)(N > 0 ? N : 1) * 3 * sizeof(int32_t));
+  if (N > 0) memcpy(P->T, T, (size_t)N * 3 * sizeof(int32_t));
   for (int64_t i = 0; i < N; ++i)
     panel_geometry(vtx(P, i, 0), vtx(P, i, 1), vtx(P, i, 2), P->cen + 3 * i, P->area + i, P->h + i);
+  order_and_trees(P, 1);
+  return P;
+}
+
+/* Quadrilateral panels (A25; the paper's model case): each quad
+ * (q0,q1,q2,q3), vertices in cyclic order, is the union of the triangles (q0,q1,q2) and
+ * (q0,q2,q3).  Node = the vertex average ((q0 + q1) + (q2 + q3)) * 0.25,
+ * |Q_i| = |T_2i| + |T_2i+1|, h_i = max(h_2i, h_2i+1).  The piecewise-constant basis
+ * function of Q_i is the sum of those of its two triangles, so every Galerkin integral over
+ * Q_i x Q_j is the sum of the four triangle-pair integrals. */
+or_problem* or_create_quads(const double* V, int64_t n_v, const int32_t* Qv, int64_t N,
+                            int leaf_size, double eta) {
+  or_problem* P = alloc_problem(V, n_v, N, leaf_size, eta);
+  P->Q = (int32_t*)malloc((size_t)(N > 0 ? N : 1) * 4 * sizeof(int32_t));
+  if (N > 0) memcpy(P->Q, Qv, (size_t)N * 4 * sizeof(int32_t));
+  int32_t* T2 = (int32_t*)malloc((size_t)(N > 0 ? N : 1) * 6 * sizeof(int32_t));
+  for (int64_t i = 0; i < N; ++i) {
+    const int32_t* q = Qv + 4 * i;
+    T2[6 * i + 0] = q[0]; T2[6 * i + 1] = q[1]; T2[6 * i + 2] = q[2];
+    T2[6 * i + 3] = q[0]; T2[6 * i + 4] = q[2]; T2[6 * i + 5] = q[3];
+  }
+  P->tri = alloc_problem(V, n_v, 2 * N, leaf_size, eta);
+  P->tri->T = T2;
+  for (int64_t t = 0; t < 2 * N; ++t)
+    panel_geometry(vtx(P->tri, t, 0), vtx(P->tri, t, 1), vtx(P->tri, t, 2), P->tri->cen + 3 * t,
+                   P->tri->area + t, P->tri->h + t);
+  order_and_trees(P->tri, 0);
+  for (int64_t i = 0; i < N; ++i) {
+    const double *a = P->V + 3 * (int64_t)Qv[4 * i], *b = P->V + 3 * (int64_t)Qv[4 * i + 1];
+    const double *c = P->V + 3 * (int64_t)Qv[4 * i + 2], *d = P->V + 3 * (int64_t)Qv[4 * i + 3];
+    for (int k = 0; k < 3; ++k) P->cen[3 * i + k] = ((a[k] + b[k]) + (c[k] + d[k])) * 0.25;
+    P->area[i] = P->tri->area[2 * i] + P->tri->area[2 * i + 1];
+    P->h[i] = P->tri->h[2 * i] > P->tri->h[2 * i + 1] ? P->tri->h[2 * i] : P->tri->h[2 * i + 1];
+  }
+  order_and_trees(P, 1);
+  return P;
+}
+
+static void order_and_trees(or_problem* P, int build_trees) {
+  const int64_t N = P->N;
   /* global centroid bounding box and Morton codes */
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t i = 0; i < N; ++i)
@@ -260,7 +316,7 @@ or_problem* or_create(const double* V, int64_t n_v, const int32_t* T, int64_t N,
   int32_t* tmp = (int32_t*)malloc((size_t)(N > 0 ? N : 1) * sizeof(int32_t));
   merge_sort(P->perm, tmp, P->code, N);
   free(tmp);
-  if (N > 0) {
+  if (N > 0 && build_trees) {
     build_cluster(P, 0, (int32_t)N, 0);
     build_block(P, 0, 0);
   }
@@ -270,7 +326,6 @@ or_problem* or_create(const double* V, int64_t n_v, const int32_t* T, int64_t N,
   P->piv = (int32_t**)calloc((size_t)(P->nadm + 1), sizeof(int32_t*));
   P->rank = (int*)malloc((size_t)(P->nadm + 1) * sizeof(int));
   for (int64_t b = 0; b < P->nadm; ++b) P->rank[b] = -1;
-  return P;
 }
 
 static void free_assembly(or_problem* P) {
@@ -287,6 +342,8 @@ void or_destroy(or_problem* P) {
   free(P->dblk); free(P->U); free(P->Vf); free(P->piv); free(P->rank);
   free(P->V); free(P->T); free(P->cen); free(P->area); free(P->h); free(P->code);
   free(P->perm); free(P->cl); free(P->adm); free(P->dense);
+  free(P->Q);
+  or_destroy(P->tri);
   free(P);
 }
 
@@ -547,12 +604,17 @@ static int classify(const or_problem* P, int64_t i, int64_t j) {
   return 3;
 }
 
-int or_entry_class(const or_problem* P, int64_t i, int64_t j) { return classify(P, i, j); }
+int or_entry_class(const or_problem* P, int64_t i, int64_t j) { return P->tri ? -1 : classify(P, i, j); }
 
 static const int64_t ss_evals[3] = {0, 5 * 1296, 2 * 1296};
 
 static double entry_app(const or_problem* P, int64_t i, int64_t j, double* evals) {
   int64_t x = i < j ? i : j, y = i < j ? j : i;    /* canonical: lower application index outer */
+  if (P->tri) {                                    /* quads (A25): four triangle pairs, fixed order */
+    double e00 = entry_app(P->tri, 2 * x, 2 * y, evals), e01 = entry_app(P->tri, 2 * x, 2 * y + 1, evals);
+    double e10 = entry_app(P->tri, 2 * x + 1, 2 * y, evals), e11 = entry_app(P->tri, 2 * x + 1, 2 * y + 1, evals);
+    return ((e00 + e01) + e10) + e11;
+  }
   int cls = classify(P, x, y);
   if (cls == 0) {
     if (evals) *evals += 0;
@@ -842,6 +904,13 @@ void or_matvec(const or_problem* P, const double* x, double* y) {
 static double paper_f(const double* x) { return (4.0 * x[0] * x[0] - 3.0 * x[1] * x[1]) - x[2] * x[2]; }
 
 void or_rhs(const or_problem* P, int kind, double* f) {
+  if (P->tri) {                                    /* quads (A25): f_i = f_2i + f_2i+1 */
+    double* f2 = (double*)malloc((size_t)(2 * P->N > 0 ? 2 * P->N : 1) * sizeof(double));
+    or_rhs(P->tri, kind, f2);
+    for (int64_t i = 0; i < P->N; ++i) f[i] = f2[2 * i] + f2[2 * i + 1];
+    free(f2);
+    return;
+  }
   for (int64_t i = 0; i < P->N; ++i) {
     if (kind == 0) { f[i] = P->area[i]; continue; }
     const double *a = vtx(P, i, 0), *b = vtx(P, i, 1), *c = vtx(P, i, 2);
@@ -1019,6 +1088,13 @@ double or_panel_potential(const double* x, const double* tri, int n) {
 }
 
 void or_potential(const or_problem* P, const double* alpha, int64_t M, const double* X, double* out) {
+  if (P->tri) {                                    /* quads (A25): both triangles carry alpha_i */
+    double* a2 = (double*)malloc((size_t)(2 * P->N > 0 ? 2 * P->N : 1) * sizeof(double));
+    for (int64_t i = 0; i < P->N; ++i) a2[2 * i] = a2[2 * i + 1] = alpha[i];
+    or_potential(P->tri, a2, M, X, out);
+    free(a2);
+    return;
+  }
   reftab_t R[4];
   for (int n = 3; n <= 6; ++n) R[n - 3] = make_reftab(n);
 #pragma omp parallel for schedule(dynamic, 1)

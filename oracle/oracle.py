@@ -35,6 +35,8 @@ def lib():
         ptr = C.c_void_p
         L.or_create.restype = P
         L.or_create.argtypes = [ptr, i64, ptr, i64, i32, d]
+        L.or_create_quads.restype = P
+        L.or_create_quads.argtypes = [ptr, i64, ptr, i64, i32, d]
         L.or_destroy.argtypes = [P]
         L.or_n.restype = i64; L.or_n.argtypes = [P]
         L.or_get_perm.argtypes = [P, ptr]
@@ -146,7 +148,8 @@ class Problem:
         self.V = np.ascontiguousarray(V, dtype=np.float64)
         self.T = np.ascontiguousarray(T, dtype=np.int32)
         self.N = self.T.shape[0]
-        self._h = lib().or_create(_p(self.V), self.V.shape[0], _p(self.T), self.N, leaf_size, float(eta))
+        create = lib().or_create_quads if self.T.shape[1] == 4 else lib().or_create   # quads: A25
+        self._h = create(_p(self.V), self.V.shape[0], _p(self.T), self.N, leaf_size, float(eta))
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:

@@ -9,6 +9,12 @@
   Gauss rule on a uniform 4^level subdivision of Tx.  The integrand is continuous
   (bounded potential), so this converges to the exact value as level grows,
   independently of any Duffy/Sauter-Schwab transformation.
+* square_pair_integral(A, B): int_A int_B 1/|x-y| for two squares (origin, e1, e2 with
+  e1 _|_ e2, |e1| = |e2|): the inner integral is the closed-form potential of a uniform
+  rectangle (antiderivative X asinh(Y/sqrt(X^2+z^2)) + Y asinh(X/sqrt(Y^2+z^2))
+  - z atan(XY/(zR)) at the four corners, Durand 1964), the outer one a tensor Gauss rule
+  graded geometrically toward all four edges of B.  Never splits a square into
+  triangles, so it is independent of the quadrilateral reading A25.
 * gauss_legendre_decimal(n, digits): Gauss-Legendre nodes/weights on [0,1] by
   Newton iteration in Python's decimal module, correctly rounded to binary64.
 """
@@ -107,3 +113,45 @@ def gauss_legendre_decimal(n, digits=60):
         weights.append(float(1 / ((1 - t * t) * dp * dp)))
     del pi
     return np.array(nodes), np.array(weights)
+
+
+def _rect_antiderivative(X, Y, z):
+    R = np.sqrt(X * X + Y * Y + z * z)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t1 = np.where(X == 0, 0.0, X * np.arcsinh(Y / np.sqrt(X * X + z * z)))
+        t2 = np.where(Y == 0, 0.0, Y * np.arcsinh(X / np.sqrt(Y * Y + z * z)))
+        t3 = np.where(z == 0, 0.0, z * np.arctan2(X * Y, z * R))
+    return t1 + t2 - t3
+
+
+def square_potential(P, o, e1, e2):
+    """int over the square {o + a e1 + b e2 : a, b in [0,1]} of 1/|p - y| for points P [M, 3]."""
+    P = np.atleast_2d(np.asarray(P, dtype=np.float64))
+    s = np.linalg.norm(e1)
+    u1, u2 = e1 / s, e2 / s
+    n = np.cross(u1, u2)
+    d = P - o
+    px, py, pz = d @ u1, d @ u2, np.abs(d @ n)
+    F = _rect_antiderivative
+    return F(s - px, s - py, pz) - F(-px, s - py, pz) - F(s - px, -py, pz) + F(-px, -py, pz)
+
+
+def _graded01(levels, pts):
+    g, w = np.polynomial.legendre.leggauss(pts)
+    g, w = (g + 1) / 2, w / 2
+    edges = [0.0] + [0.5 * 2.0 ** (-k) for k in range(levels, 0, -1)] + [0.5]
+    a, b = np.array(edges[:-1]), np.array(edges[1:])
+    x = (a[:, None] + (b - a)[:, None] * g[None, :]).ravel()
+    ww = ((b - a)[:, None] * w[None, :]).ravel()
+    return np.concatenate([x, 1 - x[::-1]]), np.concatenate([ww, ww[::-1]])
+
+
+def square_pair_integral(A, B, levels=22, pts=10):
+    """int_A int_B 1/|x - y| dy dx, A and B = (origin, e1, e2) squares."""
+    oA, e1A, e2A = (np.asarray(v, dtype=np.float64) for v in A)
+    oB, e1B, e2B = (np.asarray(v, dtype=np.float64) for v in B)
+    x, w = _graded01(levels, pts)
+    S, T = np.meshgrid(x, x, indexing="ij")
+    P = (oB[None, None, :] + S[..., None] * e1B + T[..., None] * e2B).reshape(-1, 3)
+    val = square_potential(P, oA, e1A, e2A)
+    return float((val * np.outer(w, w).ravel()).sum() * np.linalg.norm(np.cross(e1B, e2B)))
