@@ -57,9 +57,12 @@ typedef enum {
 
 #define HM_NCCL_UNIQUE_ID_BYTES 128
 
-/* Surface mesh of flat triangles (nodes = element centroids).
- * vertices: n_vertices*3 doubles, xyz row-major.  triangles: n_triangles*3 int32, 0-based
- * vertex ids; vertices must be deduplicated (singular-entry classification compares ids).
+/* Surface mesh of flat panels (nodes = element centres).
+ * vertices: n_vertices*3 doubles, xyz row-major.  triangles: n_triangles*panel_vertices
+ * int32, 0-based vertex ids; vertices must be deduplicated (singular-entry classification
+ * compares ids).  panel_vertices: 3 (or 0) = triangles; 4 = planar quadrilaterals in cyclic
+ * vertex order (the paper's cube), each evaluated as the triangles (q0,q1,q2) and
+ * (q0,q2,q3) (A25); N = n_triangles panels either way.
  * memory: 0 = both arrays in host memory, 1 = both in device memory on the ctx device. */
 typedef struct {
   const double* vertices;
@@ -67,6 +70,7 @@ typedef struct {
   const int32_t* triangles;
   int64_t n_triangles;
   int memory;
+  int panel_vertices;
 } hm_mesh;
 
 /* Create a context on CUDA device `device` for rank `rank` of `world_size` ranks.

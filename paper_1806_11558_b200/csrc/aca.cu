@@ -492,6 +492,11 @@ void aca_eval(Context& C, const M& m, int64_t total, AcaWork& W) {
   W.cnt.alloc(2);
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 2 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
+  if (C.quad) {                     // quadrilaterals (A25): four triangle pairs per entry
+    k_eval_quad<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.ev.get());
+    HM_CHECK_LAUNCH();
+    return;
+  }
   k_eval_class3<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(total, 128), 148 * 16);

@@ -391,8 +391,12 @@ hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double e
     if (!mesh || !mesh->vertices || !mesh->triangles) hm::fail(HM_ERR_ARG, "hm_build_tree: null mesh");
     if (leaf_size < 1) hm::fail(HM_ERR_ARG, "hm_build_tree: leaf_size < 1");
     if (!(eta >= 0) || !std::isfinite(eta)) hm::fail(HM_ERR_ARG, "hm_build_tree: eta must be finite and >= 0");
+    if (mesh->panel_vertices != 0 && mesh->panel_vertices != 3 && mesh->panel_vertices != 4)
+      hm::fail(HM_ERR_ARG, "hm_build_tree: panel_vertices must be 0, 3 or 4");
     if (mesh->n_triangles < 1 || mesh->n_triangles > (1LL << 30) || mesh->n_vertices < 3)
       hm::fail(HM_ERR_ARG, "hm_build_tree: bad mesh sizes");
+    if (mesh->panel_vertices == 4 && mesh->n_triangles > (1LL << 29))
+      hm::fail(HM_ERR_ARG, "hm_build_tree: at most 2^29 quadrilaterals");
     C.have_setup = false;
     Timer t(C);
     hm::build_tree(C, *mesh, leaf_size, eta);

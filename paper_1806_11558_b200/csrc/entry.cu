@@ -48,16 +48,17 @@ void upload_quadrature_tables() {
 }
 
 __global__ void k_eval_pairs(const Panel* __restrict__ P, const int32_t* __restrict__ iperm,
-                             const int64_t* __restrict__ pairs, int64_t n, double* __restrict__ out) {
+                             const int64_t* __restrict__ pairs, int64_t n, bool quad, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n) return;
   int s = iperm[pairs[2 * e]], t = iperm[pairs[2 * e + 1]];
-  out[e] = entry_st(P, s, t);
+  unsigned long long ev = 0;
+  out[e] = quad ? quad_entry(P, s, t, ev) : entry_st(P, s, t);
 }
 
 void eval_entries(Context& C, int64_t n, const int64_t* d_pairs, double* d_out) {
   if (n == 0) return;
-  k_eval_pairs<<<grid_for(n, 128), 128, 0, C.stream>>>(C.panel.get(), C.iperm.get(), d_pairs, n, d_out);
+  k_eval_pairs<<<grid_for(n, 128), 128, 0, C.stream>>>(C.panel.get(), C.iperm.get(), d_pairs, n, C.quad, d_out);
   HM_CHECK_LAUNCH();
 }
 
@@ -67,10 +68,7 @@ __device__ __forceinline__ double paper_f(double x, double y, double z) {
   return dsub(dsub(dmul(dmul(4.0, x), x), dmul(dmul(3.0, y), y)), dmul(z, z));
 }
 
-__global__ void k_rhs(const Panel* __restrict__ P, int64_t N, int kind, double* __restrict__ f_app) {
-  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= N) return;
-  const Panel& T = P[s];
+__device__ __forceinline__ double panel_rhs(const Panel& T, int kind) {
   double v;
   if (kind == 0) {
     v = T.area;
@@ -85,11 +83,19 @@ __global__ void k_rhs(const Panel* __restrict__ P, int64_t N, int kind, double* 
                            paper_f(m[2][0], m[2][1], m[2][2]));
     v = dmul(ddiv(T.area, 3.0), s3);
   }
-  f_app[T.app] = v;
+  return v;
+}
+
+// node s: triangles -> its panel; quads (A25) -> f_2i + f_2i+1 of its two triangles
+__global__ void k_rhs(const Panel* __restrict__ P, int64_t N, int kind, bool quad, double* __restrict__ f_app) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= N) return;
+  if (quad) f_app[P[2 * s].app >> 1] = dadd(panel_rhs(P[2 * s], kind), panel_rhs(P[2 * s + 1], kind));
+  else f_app[P[s].app] = panel_rhs(P[s], kind);
 }
 
 void assemble_rhs(Context& C, int kind, double* f_app) {
-  k_rhs<<<grid_for(C.N, 256), 256, 0, C.stream>>>(C.panel.get(), C.N, kind, f_app);
+  k_rhs<<<grid_for(C.N, 256), 256, 0, C.stream>>>(C.panel.get(), C.N, kind, C.quad, f_app);
   HM_CHECK_LAUNCH();
 }
 

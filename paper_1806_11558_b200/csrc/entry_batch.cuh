@@ -251,6 +251,24 @@ __global__ void __launch_bounds__(128) k_eval_rest(M m, const EntryRef* __restri
   if (ev) atomicAdd(evals, ev);
 }
 
+// Quadrilateral meshes (A25): one thread per entry, the four triangle pairs of quad_entry
+// with their own rules (no class buckets: in far-field blocks the four pairs mostly share
+// one order, near-field warps diverge over the classes).
+template <class M>
+__global__ void __launch_bounds__(128) k_eval_quad(M m, int64_t total, unsigned long long* __restrict__ evals) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  EntryRef r;
+  unsigned long long ev = 0;
+  if (m.locate(e, e < total, r)) {
+    int s, t;
+    m.pair(r, s, t);
+    m.put(r, quad_entry(m.P, s, t, ev));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+  if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
+}
+
 struct EntryBatchWork {
   DBuf<unsigned long long> cnt, cursor;
   DBuf<EntryRef> list;
@@ -260,10 +278,21 @@ struct EntryBatchWork {
 // Evaluate all `total` entries of mapping m on stream st; returns the number of kernel
 // evaluations.  Allocates only when W is smaller than this batch (near_prepare pre-sizes it).
 template <class M>
-double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t st, KTimer& kt) {
+double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t st, KTimer& kt, bool quad) {
   if (total <= 0) return 0.0;
   W.cnt.alloc(kNumClass);
   W.cursor.alloc(kNumClass);
+  if (quad) {
+    HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, sizeof(unsigned long long), st));
+    {
+      KScope ks(kt, st, KF_EVAL_NEAR);
+      k_eval_quad<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.cnt.get());
+      HM_CHECK_LAUNCH();
+    }
+    HM_CUDA(cudaMemcpyAsync(W.hcnt, W.cnt.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaStreamSynchronize(st));
+    return (double)W.hcnt[0];
+  }
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, kNumClass * sizeof(unsigned long long), st));
   k_class_count<M><<<grid_for(total, 256), 256, 0, st>>>(m, total, W.cnt.get());
   HM_CHECK_LAUNCH();

@@ -164,6 +164,7 @@ struct MvTileU { int32_t blk, t0, t1, pad; };
 // Persistent scratch of hm_build_tree (grow-only: reused across calls, no allocation churn)
 struct TreeWs {
   DBuf<double> cen, area, hh, part, gbox;
+  DBuf<double> tcen, tarea, th;   // quads: geometry of the 2N split triangles
   DBuf<uint64_t> code_sorted, ksorted, admk, denk, fk[2];
   DBuf<int32_t> idx, flag, scan;
   DBuf<int2> fr[2];
@@ -231,6 +232,9 @@ struct Context {
   int64_t N = 0, nv = 0;
   int leaf_size = 32;
   double eta = 1.0;
+  bool quad = false;           // quadrilateral panels (A25): 2 triangle panels per node
+  int64_t npanel = 0;          // triangle panels: N, or 2N for quads (panel 2s+a of node s)
+  DBuf<double> ncen;           // quads: node centroids, internal order (cluster boxes)
   DBuf<Panel> panel;           // internal order
   DBuf<int32_t> perm, iperm;   // perm[s] = app index; iperm[app] = s
   DBuf<uint64_t> codes_app;    // Morton codes, application order

@@ -112,7 +112,7 @@ void near_eval(Context& C, cudaStream_t st, KTimer& kt) {
     k_seg_table<<<grid_for(b1 - b0, 256), 256, 0, st>>>(C.doff.get() + b0, b1 - b0, hoff[b0], C.near_tab.get());
     HM_CHECK_LAUNCH();
     NearMap m{C.panel.get(), q, C.doff.get(), b0, b1 - b0, hoff[b0], C.dstore.get(), C.near_tab.get()};
-    evals += eval_batched(m, hoff[b1] - hoff[b0], W, st, kt);
+    evals += eval_batched(m, hoff[b1] - hoff[b0], W, st, kt, C.quad);
     b0 = b1;
   }
   HM_CUDA(cudaStreamSynchronize(st));

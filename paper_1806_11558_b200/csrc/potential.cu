@@ -18,8 +18,10 @@ namespace {
 
 constexpr int kPts = 8;
 
+// panels s < NP; the density of panel s is alpha_int[s >> qshift] (quads: both triangles of
+// node s >> 1 carry alpha, A25)
 __global__ void __launch_bounds__(256) k_potential(const Panel* __restrict__ P, const double* __restrict__ alpha_int,
-                                                   int64_t N, const double* __restrict__ X, int64_t M,
+                                                   int64_t N, int qshift, const double* __restrict__ X, int64_t M,
                                                    double* __restrict__ out) {
   __shared__ double sx[kPts][3];
   __shared__ double red[kPts][8];
@@ -38,7 +40,7 @@ __global__ void __launch_bounds__(256) k_potential(const Panel* __restrict__ P, 
     load_panel_vertices(P, (int)s, V);
     const double cx = __ldg(&P[s].c[0]), cy = __ldg(&P[s].c[1]), cz = __ldg(&P[s].c[2]);
     const double h = __ldg(&P[s].h), h2 = dmul(h, h);
-    const double a = __ldg(alpha_int + s), two_area = dmul(2.0, __ldg(&P[s].area));
+    const double a = __ldg(alpha_int + (s >> qshift)), two_area = dmul(2.0, __ldg(&P[s].area));
     const double e1x = dsub(V[3], V[0]), e1y = dsub(V[4], V[1]), e1z = dsub(V[5], V[2]);
     const double e2x = dsub(V[6], V[3]), e2y = dsub(V[7], V[4]), e2z = dsub(V[8], V[5]);
     for (int q = 0; q < kPts; ++q) {
@@ -91,8 +93,8 @@ void potential(Context& C, const double* alpha_app, int64_t M, const double* X_d
   gather_perm(C, alpha_app, C.xin.get());
   HM_CUDA(cudaMemsetAsync(out_dev, 0, M * sizeof(double), st));
   if (M == 0) return;
-  const dim3 grid(grid_for(C.N, 256), (unsigned)((M + kPts - 1) / kPts));
-  k_potential<<<grid, 256, 0, st>>>(C.panel.get(), C.xin.get(), C.N, X_dev, M, out_dev);
+  const dim3 grid(grid_for(C.npanel, 256), (unsigned)((M + kPts - 1) / kPts));
+  k_potential<<<grid, 256, 0, st>>>(C.panel.get(), C.xin.get(), C.npanel, C.quad ? 1 : 0, X_dev, M, out_dev);
   HM_CHECK_LAUNCH();
   k_scale_inplace<<<grid_for(M, 256), 256, 0, st>>>(out_dev, M, kInv4Pi);
   HM_CHECK_LAUNCH();

@@ -37,6 +37,47 @@ __global__ void k_geometry(const double* __restrict__ V, const int32_t* __restri
   hh[i] = m > l2 ? m : l2;
 }
 
+// Quadrilateral panels (A25): quad i = (q0,q1,q2,q3) -> triangles 2i = (q0,q1,q2), 2i+1 =
+// (q0,q2,q3) with the triangle geometry of k_geometry (same operation order); node =
+// ((q0 + q1) + (q2 + q3)) * 0.25, |Q| = |T_2i| + |T_2i+1|, h = max(h_2i, h_2i+1).
+__global__ void k_geometry_quad(const double* __restrict__ V, const int32_t* __restrict__ Qv, int64_t N,
+                                int64_t nv, double* __restrict__ cen, double* __restrict__ area,
+                                double* __restrict__ hh, double* __restrict__ tcen, double* __restrict__ tarea,
+                                double* __restrict__ th, unsigned int* bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int32_t id[4];
+  for (int r = 0; r < 4; ++r) {
+    id[r] = Qv[4 * i + r];
+    if (id[r] < 0 || id[r] >= nv) { atomicOr(bad, 1u); return; }
+  }
+  double q[4][3];
+  for (int r = 0; r < 4; ++r)
+    for (int k = 0; k < 3; ++k) q[r][k] = V[3 * (int64_t)id[r] + k];
+  const int tv[2][3] = {{0, 1, 2}, {0, 2, 3}};
+  for (int a = 0; a < 2; ++a) {
+    const double* v0 = q[tv[a][0]];
+    const double* v1 = q[tv[a][1]];
+    const double* v2 = q[tv[a][2]];
+    const int64_t t = 2 * i + a;
+    for (int k = 0; k < 3; ++k) tcen[3 * t + k] = ddiv(dadd(dadd(v0[k], v1[k]), v2[k]), 3.0);
+    double e01[3], e02[3];
+    for (int k = 0; k < 3; ++k) { e01[k] = dsub(v1[k], v0[k]); e02[k] = dsub(v2[k], v0[k]); }
+    const double cx = dsub(dmul(e01[1], e02[2]), dmul(e01[2], e02[1]));
+    const double cy = dsub(dmul(e01[2], e02[0]), dmul(e01[0], e02[2]));
+    const double cz = dsub(dmul(e01[0], e02[1]), dmul(e01[1], e02[0]));
+    const double ar = dmul(0.5, __dsqrt_rn(dadd(dadd(dmul(cx, cx), dmul(cy, cy)), dmul(cz, cz))));
+    tarea[t] = ar;
+    if (!(ar > 0.0)) atomicOr(bad, 2u);
+    const double l0 = edge_length(v0, v1), l1 = edge_length(v1, v2), l2 = edge_length(v2, v0);
+    const double m = l0 > l1 ? l0 : l1;
+    th[t] = m > l2 ? m : l2;
+  }
+  for (int k = 0; k < 3; ++k) cen[3 * i + k] = dmul(dadd(dadd(q[0][k], q[1][k]), dadd(q[2][k], q[3][k])), 0.25);
+  area[i] = dadd(tarea[2 * i], tarea[2 * i + 1]);
+  hh[i] = th[2 * i] > th[2 * i + 1] ? th[2 * i] : th[2 * i + 1];
+}
+
 // global centroid box: per-block partial min/max, then one block finishes
 __global__ void k_minmax(const double* __restrict__ cen, int64_t N, double* __restrict__ part) {
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -120,6 +161,37 @@ __global__ void k_gather_panels(const double* __restrict__ V, const int32_t* __r
   iperm[i] = (int32_t)s;
 }
 
+// quads: panel p = 2s + a is triangle a of the quad at internal position s (application
+// triangle 2 perm[s] + a); node centroids in internal order for the cluster boxes
+__global__ void k_gather_panels_quad(const double* __restrict__ V, const int32_t* __restrict__ Qv,
+                                     const double* __restrict__ cen, const double* __restrict__ tcen,
+                                     const double* __restrict__ tarea, const double* __restrict__ th,
+                                     const int32_t* __restrict__ perm, int64_t N, Panel* __restrict__ P,
+                                     int32_t* __restrict__ iperm, double* __restrict__ ncen) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= 2 * N) return;
+  const int64_t s = p >> 1;
+  const int a = (int)(p & 1);
+  const int32_t i = perm[s];
+  const int tv[2][3] = {{0, 1, 2}, {0, 2, 3}};
+  const int64_t t = 2 * (int64_t)i + a;
+  Panel pn;
+  for (int r = 0; r < 3; ++r) {
+    const int32_t vid = Qv[4 * (int64_t)i + tv[a][r]];
+    pn.vid[r] = vid;
+    for (int k = 0; k < 3; ++k) pn.v[3 * r + k] = V[3 * (int64_t)vid + k];
+  }
+  for (int k = 0; k < 3; ++k) pn.c[k] = tcen[3 * t + k];
+  pn.area = tarea[t];
+  pn.h = th[t];
+  pn.app = (int32_t)t;
+  P[p] = pn;
+  if (a == 0) {
+    iperm[i] = (int32_t)s;
+    for (int k = 0; k < 3; ++k) ncen[3 * s + k] = cen[3 * (int64_t)i + k];
+  }
+}
+
 // ---- cluster tree (level order): node c at level l splits iff |c| > C_leaf ------------
 __global__ void k_split_flags(const int32_t* __restrict__ lo, const int32_t* __restrict__ hi, int64_t b,
                               int64_t e, int leaf, int32_t* __restrict__ flag) {
@@ -143,16 +215,18 @@ __global__ void k_split_emit(int32_t* __restrict__ lo, int32_t* __restrict__ hi,
 }
 
 // boxes bottom-up: leaves from their points, inner nodes from their two children (exact)
-__global__ void k_boxes(const Panel* __restrict__ P, const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
-                        const int32_t* __restrict__ child, int64_t b, int64_t e, double* __restrict__ box,
-                        double* __restrict__ diam2) {
+// node centroid of internal position s: cb[cstride * s + k] (triangles: the panels' c,
+// quads: the node array)
+__global__ void k_boxes(const double* __restrict__ cb, int cstride, const int32_t* __restrict__ lo,
+                        const int32_t* __restrict__ hi, const int32_t* __restrict__ child, int64_t b, int64_t e,
+                        double* __restrict__ box, double* __restrict__ diam2) {
   int64_t c = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= e) return;
   double m[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
   if (child[c] < 0) {
     for (int32_t s = lo[c]; s < hi[c]; ++s)
       for (int k = 0; k < 3; ++k) {
-        double x = P[s].c[k];
+        double x = cb[(int64_t)cstride * s + k];
         if (x < m[k]) m[k] = x;
         if (x > m[3 + k]) m[3 + k] = x;
       }
@@ -323,18 +397,28 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   upload_quadrature_tables();
   // ---- a1: mesh upload + panel geometry
   C.vert.alloc(nv * 3);
-  C.tri.alloc(N * 3);
+  C.quad = mesh.panel_vertices == 4;
+  const int pv = C.quad ? 4 : 3;
+  C.npanel = C.quad ? 2 * N : N;
+  C.tri.alloc(N * pv);
   cudaMemcpyKind kind = mesh.memory ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   HM_CUDA(cudaMemcpyAsync(C.vert.get(), mesh.vertices, nv * 3 * sizeof(double), kind, st));
-  HM_CUDA(cudaMemcpyAsync(C.tri.get(), mesh.triangles, N * 3 * sizeof(int32_t), kind, st));
+  HM_CUDA(cudaMemcpyAsync(C.tri.get(), mesh.triangles, N * pv * sizeof(int32_t), kind, st));
   TreeWs& ws = C.tws;
   DBuf<double>& cen = ws.cen; DBuf<double>& area = ws.area; DBuf<double>& hh = ws.hh;
   cen.alloc(N * 3); area.alloc(N); hh.alloc(N);
   DBuf<unsigned int>& bad = ws.bad;
   bad.alloc(1);
   HM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned int), st));
-  k_geometry<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), N, nv, cen.get(), area.get(),
-                                                 hh.get(), bad.get());
+  if (C.quad) {
+    ws.tcen.alloc(2 * N * 3); ws.tarea.alloc(2 * N); ws.th.alloc(2 * N);
+    k_geometry_quad<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), N, nv, cen.get(), area.get(),
+                                                        hh.get(), ws.tcen.get(), ws.tarea.get(), ws.th.get(),
+                                                        bad.get());
+  } else {
+    k_geometry<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), N, nv, cen.get(), area.get(),
+                                                   hh.get(), bad.get());
+  }
   HM_CHECK_LAUNCH();
   unsigned int hbad = 0;
   HM_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
@@ -347,8 +431,8 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   k_minmax_final<<<1, 32, 0, st>>>(part.get(), nb, gbox.get());
   HM_CHECK_LAUNCH();
   HM_CUDA(cudaStreamSynchronize(st));
-  if (hbad & 1u) fail(HM_ERR_ARG, "hm_build_tree: a triangle references a vertex id out of range");
-  if (hbad & 2u) fail(HM_ERR_ARG, "hm_build_tree: a triangle has zero area (degenerate)");
+  if (hbad & 1u) fail(HM_ERR_ARG, "hm_build_tree: a panel references a vertex id out of range");
+  if (hbad & 2u) fail(HM_ERR_ARG, "hm_build_tree: a panel (or half of a quad) has zero area (degenerate)");
   DBuf<uint64_t>& code_sorted = ws.code_sorted;
   DBuf<int32_t>& idx = ws.idx;
   C.codes_app.alloc(N);
@@ -361,9 +445,16 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
     return cub::DeviceRadixSort::SortPairs(t, b, C.codes_app.get(), code_sorted.get(), idx.get(),
                                            C.perm.get(), (int)N, 0, 63, st);
   });
-  C.panel.alloc(N);
-  k_gather_panels<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), cen.get(), area.get(), hh.get(),
-                                                     C.perm.get(), N, C.panel.get(), C.iperm.get());
+  C.panel.alloc(C.npanel);
+  if (C.quad) {
+    C.ncen.alloc(N * 3);
+    k_gather_panels_quad<<<grid_for(2 * N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), cen.get(), ws.tcen.get(),
+                                                                 ws.tarea.get(), ws.th.get(), C.perm.get(), N,
+                                                                 C.panel.get(), C.iperm.get(), C.ncen.get());
+  } else {
+    k_gather_panels<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), cen.get(), area.get(), hh.get(),
+                                                       C.perm.get(), N, C.panel.get(), C.iperm.get());
+  }
   HM_CHECK_LAUNCH();
   HM_CUDA(cudaEventRecord(ev[2], st));
   // ---- a3: cluster tree, level order
@@ -401,7 +492,11 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   C.cl_box.alloc(6 * C.ncl); C.cl_diam2.alloc(C.ncl);
   for (int level = nlev - 1; level >= 0; --level) {
     int64_t b = lev[level], e = lev[level + 1];
-    k_boxes<<<grid_for(e - b, 128), 128, 0, st>>>(C.panel.get(), C.cl_lo.get(), C.cl_hi.get(), C.cl_child.get(),
+    const double* cb = C.quad ? C.ncen.get()
+                              : reinterpret_cast<const double*>(reinterpret_cast<const char*>(C.panel.get()) +
+                                                                offsetof(Panel, c));
+    const int cstride = C.quad ? 3 : (int)(sizeof(Panel) / sizeof(double));
+    k_boxes<<<grid_for(e - b, 128), 128, 0, st>>>(cb, cstride, C.cl_lo.get(), C.cl_hi.get(), C.cl_child.get(),
                                                    b, e, C.cl_box.get(), C.cl_diam2.get());
     HM_CHECK_LAUNCH();
   }

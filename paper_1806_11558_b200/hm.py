@@ -31,7 +31,8 @@ class HMError(RuntimeError):
 
 class _Mesh(C.Structure):
     _fields_ = [("vertices", C.c_void_p), ("n_vertices", C.c_int64),
-                ("triangles", C.c_void_p), ("n_triangles", C.c_int64), ("memory", C.c_int)]
+                ("triangles", C.c_void_p), ("n_triangles", C.c_int64), ("memory", C.c_int),
+                ("panel_vertices", C.c_int)]
 
 
 _lib = None
@@ -136,7 +137,8 @@ def hm_build_tree(ctx, vertices, triangles, leaf_size=32, eta=1.0):
     dev = _is_cuda(vertices)
     if dev != _is_cuda(triangles):
         raise ValueError("vertices and triangles must both be host or both device")
-    m = _Mesh(_ptr(vertices), int(vertices.shape[0]), _ptr(triangles), int(triangles.shape[0]), 1 if dev else 0)
+    m = _Mesh(_ptr(vertices), int(vertices.shape[0]), _ptr(triangles), int(triangles.shape[0]), 1 if dev else 0,
+              int(triangles.shape[1]))
     _check(ctx, lib().hm_build_tree(ctx, C.byref(m), int(leaf_size), float(eta)))
 
 
