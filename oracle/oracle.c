@@ -18,7 +18,8 @@
  *   RHS           P:230-231, A16
  *   potential     P:176-177, A23           direct sum over panels
  *   fixed rank    P:776, A24 (ACA with eps = 0)
- *   quad panels   P:700, A25 (each quad = two triangles; sums of their entries)
+ *   quad panels   P:700, A25 (parallelograms: tensor Gauss when separated,
+ *                 the two-triangle split when touching)
  *
  * Pins (tests/test_oracle_*.py, all -m "not gpu"):
  *   Morton/sort/CBC   SPEC worked examples S:124-126; invariants (C1)-(C4)
@@ -574,11 +575,28 @@ double or_ss_reference_monomial(int kind, int nq, int pa, int pb, int pc, int pd
 /* ------------------------------------------------------------------ */
 /* Galerkin entry a_ij (P:224-228 per A1; classification A14)          */
 /* ------------------------------------------------------------------ */
-static reftab_t g_tab[7];
+/* tensor-Gauss table of order n on the unit square (quads, A25): s = g_a, t = g_b,
+ * w = w_a * w_b, q = a*n + b */
+static reftab_t make_reftab_square(int n) {
+  reftab_t R;
+  double g[32], gw[32];
+  or_gauss_legendre01(n, g, gw);
+  R.n = n;
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b) {
+      int q = a * n + b;
+      R.s[q] = g[a];
+      R.t[q] = g[b];
+      R.w[q] = gw[a] * gw[b];
+    }
+  return R;
+}
+
+static reftab_t g_tab[7], g_qtab[7];
 static int g_tab_init = 0;
 static void init_tables(void) {
   if (g_tab_init) return;
-  for (int n = 3; n <= 6; ++n) g_tab[n] = make_reftab(n);
+  for (int n = 3; n <= 6; ++n) { g_tab[n] = make_reftab(n); g_qtab[n] = make_reftab_square(n); }
   g_tab_init = 1;
 }
 
@@ -610,10 +628,31 @@ static const int64_t ss_evals[3] = {0, 5 * 1296, 2 * 1296};
 
 static double entry_app(const or_problem* P, int64_t i, int64_t j, double* evals) {
   int64_t x = i < j ? i : j, y = i < j ? j : i;    /* canonical: lower application index outer */
-  if (P->tri) {                                    /* quads (A25): four triangle pairs, fixed order */
-    double e00 = entry_app(P->tri, 2 * x, 2 * y, evals), e01 = entry_app(P->tri, 2 * x, 2 * y + 1, evals);
-    double e10 = entry_app(P->tri, 2 * x + 1, 2 * y, evals), e11 = entry_app(P->tri, 2 * x + 1, 2 * y + 1, evals);
-    return ((e00 + e01) + e10) + e11;
+  if (P->tri) {                                    /* quadrilaterals (A25) */
+    const int32_t* qx = P->Q + 4 * x;
+    const int32_t* qy = P->Q + 4 * y;
+    int shared = 0;
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) shared += (qx[a] == qy[b]);
+    if (shared) {                                  /* touching: four triangle pairs, fixed order */
+      double e00 = entry_app(P->tri, 2 * x, 2 * y, evals), e01 = entry_app(P->tri, 2 * x, 2 * y + 1, evals);
+      double e10 = entry_app(P->tri, 2 * x + 1, 2 * y, evals), e11 = entry_app(P->tri, 2 * x + 1, 2 * y + 1, evals);
+      return ((e00 + e01) + e10) + e11;
+    }
+    /* separated: tensor Gauss n x n on each parallelogram, chi(s,t) = q0 + s(q1-q0) + t(q2-q1),
+     * n from the node distance in the bands of A14 with h = max of the two triangles' h */
+    const double* ci = P->cen + 3 * x;
+    const double* cj = P->cen + 3 * y;
+    double dx = ci[0] - cj[0], dy = ci[1] - cj[1], dz = ci[2] - cj[2];
+    double dc2 = (dx * dx + dy * dy) + dz * dz;
+    double hm = P->h[x] > P->h[y] ? P->h[x] : P->h[y];
+    double hm2 = hm * hm;
+    int n = dc2 < 4.0 * hm2 ? 6 : dc2 < 16.0 * hm2 ? 5 : dc2 < 64.0 * hm2 ? 4 : 3;
+    tri_t X = make_tri(P->V + 3 * qx[0], P->V + 3 * qx[1], P->V + 3 * qx[2]);
+    tri_t Y = make_tri(P->V + 3 * qy[0], P->V + 3 * qy[1], P->V + 3 * qy[2]);
+    if (evals) *evals += (double)(n * n * n * n);
+    double I = regular_sum(&X, &Y, &g_qtab[n]);
+    return (I * (P->area[x] * P->area[y])) * INV4PI;
   }
   int cls = classify(P, x, y);
   if (cls == 0) {

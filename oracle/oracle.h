@@ -29,9 +29,11 @@ typedef struct or_problem or_problem;
  * (P:256-306).  V: n_v*3 doubles, T: N*3 int32.  Copies inputs. */
 or_problem* or_create(const double* V, int64_t n_v, const int32_t* T, int64_t N,
                       int leaf_size, double eta);
-/* Quadrilateral panels (A25): Q = N*4 int32 vertex ids in cyclic order; quad i is the
- * union of triangles (q0,q1,q2), (q0,q2,q3); entries, right-hand side and potential are
- * the sums over those triangles.  or_entry_class returns -1 for quad problems. */
+/* Quadrilateral panels (A25): Q = N*4 int32 vertex ids in cyclic order, planar
+ * parallelograms; quad i is the union of triangles (q0,q1,q2), (q0,q2,q3).  Entries of
+ * quads sharing a vertex are the sums over the four triangle pairs; separated quads use a
+ * tensor Gauss rule on each parallelogram (A14 bands).  Right-hand side and potential are
+ * sums over the two triangles.  or_entry_class returns -1 for quad problems. */
 or_problem* or_create_quads(const double* V, int64_t n_v, const int32_t* Q, int64_t N,
                             int leaf_size, double eta);
 void or_destroy(or_problem* P);
