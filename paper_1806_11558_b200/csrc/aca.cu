@@ -95,9 +95,12 @@ __global__ void k_step_totals(const int64_t* __restrict__ rpre, const int64_t* _
 // for entry_batch.cuh.  put() applies the rank-one corrections of the previous k steps in
 // ascending l, each product and difference separately rounded (A15), and stores the residual
 // into column k of the block's V (row step) or U (column step) workspace.
-template <bool ROW>
+template <bool ROW, bool QUAD = false>
 struct AcaMap {
-  const Panel* P;
+  static constexpr bool kQuad = QUAD;
+  const Panel* P;       // triangle panels, or node panels of a quadrilateral mesh (A25)
+  const Panel* PT;      // quads: the split triangles
+  const int4* QV;       // quads: vertex ids
   const AcaBlk* B;
   const AcaState* S;
   const int64_t* pre;   // nb + 1 prefix of this step's row (or column) lengths, active blocks first
@@ -492,11 +495,6 @@ void aca_eval(Context& C, const M& m, int64_t total, AcaWork& W) {
   W.cnt.alloc(2);
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 2 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
-  if (C.quad) {                     // quadrilaterals (A25): four triangle pairs per entry
-    k_eval_quad<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.ev.get());
-    HM_CHECK_LAUNCH();
-    return;
-  }
   k_eval_class3<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(total, 128), 148 * 16);
@@ -551,6 +549,8 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   k_init_state<<<grid_for(nb, 256), 256, 0, st>>>(W.state.get(), nb);
   HM_CHECK_LAUNCH();
   const Panel* P = C.panel.get();
+  const Panel* Pn = C.qnode.get();
+  const int4* QV = C.qv.get();
   C.times.aca_phase_ms[0] += ms_since(t0);
   const auto t1 = clk::now();
   for (int step = 0;; ++step) {
@@ -588,8 +588,12 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     HM_CHECK_LAUNCH();
     k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.cpre.get(), nact, 0, W.ctab.get());
     HM_CHECK_LAUNCH();
-    aca_eval(C, AcaMap<true>{P, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(), nb, Uw, Vw},
-             tot[0], W);
+    if (C.quad)
+      aca_eval(C, AcaMap<true, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(),
+                                     nb, Uw, Vw}, tot[0], W);
+    else
+      aca_eval(C, AcaMap<true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
+                               W.rtab.get(), nb, Uw, Vw}, tot[0], W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
     k_aca_pivot<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, Vw,
                                                           W.bmap.get());
@@ -599,8 +603,12 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
       HM_CHECK_LAUNCH();
     }
     ks.reset();
-    aca_eval(C, AcaMap<false>{P, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(), nb, Uw, Vw},
-             tot[1], W);
+    if (C.quad)
+      aca_eval(C, AcaMap<false, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(),
+                                      nb, Uw, Vw}, tot[1], W);
+    else
+      aca_eval(C, AcaMap<false>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(),
+                                W.ctab.get(), nb, Uw, Vw}, tot[1], W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
     k_aca_update<<<grid_for(nact * 32, 64), 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, Uw,
                                                            Vw, W.bmap.get(), W.piv.get(), kws, C.eps_aca);

@@ -8,6 +8,9 @@ namespace hm {
 __constant__ double c_rs[4][36];
 __constant__ double c_rt[4][36];
 __constant__ double c_rw[4][36];
+__constant__ double c_qs[4][36];
+__constant__ double c_qt[4][36];
+__constant__ double c_qw[4][36];
 __constant__ double c_g6[6];
 __constant__ double c_w6[6];
 
@@ -24,7 +27,7 @@ void upload_quadrature_tables() {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && done[dev]) return;
-  double rs[4][36] = {}, rt[4][36] = {}, rw[4][36] = {};
+  double rs[4][36] = {}, rt[4][36] = {}, rw[4][36] = {}, qs[4][36] = {}, qt[4][36] = {}, qw[4][36] = {};
   for (int n = 3; n <= 6; ++n) {
     const double* g = kGaussNodes01[n];
     const double* w = kGaussWeights01[n];
@@ -37,28 +40,37 @@ void upload_quadrature_tables() {
         volatile double ww = w[a] * w[b];
         volatile double w3 = ww * g[a];
         rw[n - 3][q] = w3;
+        qs[n - 3][q] = g[a];              // unit square, tensor (A25)
+        qt[n - 3][q] = g[b];
+        volatile double wq = w[a] * w[b];
+        qw[n - 3][q] = wq;
       }
   }
   HM_CUDA(cudaMemcpyToSymbol(c_rs, rs, sizeof(rs)));
   HM_CUDA(cudaMemcpyToSymbol(c_rt, rt, sizeof(rt)));
   HM_CUDA(cudaMemcpyToSymbol(c_rw, rw, sizeof(rw)));
+  HM_CUDA(cudaMemcpyToSymbol(c_qs, qs, sizeof(qs)));
+  HM_CUDA(cudaMemcpyToSymbol(c_qt, qt, sizeof(qt)));
+  HM_CUDA(cudaMemcpyToSymbol(c_qw, qw, sizeof(qw)));
   HM_CUDA(cudaMemcpyToSymbol(c_g6, kGaussNodes01[6], 6 * sizeof(double)));
   HM_CUDA(cudaMemcpyToSymbol(c_w6, kGaussWeights01[6], 6 * sizeof(double)));
   if (dev < 64) done[dev] = true;
 }
 
-__global__ void k_eval_pairs(const Panel* __restrict__ P, const int32_t* __restrict__ iperm,
-                             const int64_t* __restrict__ pairs, int64_t n, bool quad, double* __restrict__ out) {
+__global__ void k_eval_pairs(const Panel* __restrict__ P, const Panel* __restrict__ Pn, const int4* __restrict__ QV,
+                             const int32_t* __restrict__ iperm, const int64_t* __restrict__ pairs, int64_t n,
+                             double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n) return;
   int s = iperm[pairs[2 * e]], t = iperm[pairs[2 * e + 1]];
   unsigned long long ev = 0;
-  out[e] = quad ? quad_entry(P, s, t, ev) : entry_st(P, s, t);
+  out[e] = Pn ? quad_entry(Pn, P, QV, s, t, ev) : entry_st(P, s, t);
 }
 
 void eval_entries(Context& C, int64_t n, const int64_t* d_pairs, double* d_out) {
   if (n == 0) return;
-  k_eval_pairs<<<grid_for(n, 128), 128, 0, C.stream>>>(C.panel.get(), C.iperm.get(), d_pairs, n, C.quad, d_out);
+  k_eval_pairs<<<grid_for(n, 128), 128, 0, C.stream>>>(C.panel.get(), C.quad ? C.qnode.get() : nullptr,
+                                                        C.qv.get(), C.iperm.get(), d_pairs, n, d_out);
   HM_CHECK_LAUNCH();
 }
 

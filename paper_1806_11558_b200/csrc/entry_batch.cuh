@@ -11,6 +11,9 @@
 //   bool locate(int64_t e, bool valid, EntryRef& r)  flattened entry -> reference (warp-collective)
 //   void pair(EntryRef r, int& s, int& t)            internal row / column indices of the entry
 //   void put(EntryRef r, double a)                   consume the value (store / residual update)
+//   kQuad, P (node panels), PT, QV                   quadrilateral meshes (A25): class 0 = touching
+//                                                    quads (four triangle pairs over PT), classes
+//                                                    3..6 = separated quads, tensor rule on P
 #pragma once
 #include "entry.cuh"
 
@@ -29,6 +32,37 @@ __device__ __forceinline__ int canonical_class(const Panel* __restrict__ P, int 
   return entry_class(P[xs], P[ys]);
 }
 
+// mapping-level class and regular entry (triangles: A14/A15 on the panels; quads: A25)
+template <class M>
+__device__ __forceinline__ int map_class(const M& m, int s, int t, int& xs, int& ys) {
+  if constexpr (M::kQuad) return quad_class(m.P, m.QV, s, t, xs, ys);
+  else return canonical_class(m.P, s, t, xs, ys);
+}
+template <int n, class M>
+__device__ __forceinline__ double map_regular(const M& m, int xs, int ys) {
+  if constexpr (M::kQuad) {
+    return quad_regular_entry<n>(m.P, xs, ys);
+  } else {
+    double X[9], Y[9];
+    load_panel_vertices(m.P, xs, X);
+    load_panel_vertices(m.P, ys, Y);
+    const double I = regular_sum<n>(X, Y);
+    return dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi);
+  }
+}
+// any class (rare-rest paths); evals += the rule's kernel evaluations
+template <class M>
+__device__ __forceinline__ double map_entry(const M& m, int s, int t, unsigned long long& evals) {
+  if constexpr (M::kQuad) {
+    return quad_entry(m.P, m.PT, m.QV, s, t, evals);
+  } else {
+    int cls;
+    const double v = entry_st(m.P, s, t, &cls);
+    evals += (unsigned long long)rule_evals(cls);
+    return v;
+  }
+}
+
 template <class M>
 __global__ void k_class_count(M m, int64_t total, unsigned long long* __restrict__ cnt) {
   __shared__ unsigned int sc[kNumClass];
@@ -39,7 +73,7 @@ __global__ void k_class_count(M m, int64_t total, unsigned long long* __restrict
   if (m.locate(e, e < total, r)) {
     int s, t, xs, ys;
     m.pair(r, s, t);
-    atomicAdd(&sc[canonical_class(m.P, s, t, xs, ys)], 1u);
+    atomicAdd(&sc[map_class(m, s, t, xs, ys)], 1u);
   }
   __syncthreads();
   if (threadIdx.x < kNumClass && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
@@ -59,7 +93,7 @@ __global__ void k_class_scatter(M m, int64_t total, unsigned long long* __restri
   if (m.locate(e, e < total, r)) {
     int s, t, xs, ys;
     m.pair(r, s, t);
-    cls = canonical_class(m.P, s, t, xs, ys);
+    cls = map_class(m, s, t, xs, ys);
     pos = atomicAdd(&sc[cls], 1u);
   }
   __syncthreads();
@@ -75,17 +109,30 @@ __global__ void __launch_bounds__(128) k_eval_regular(M m, const EntryRef* __res
   const EntryRef r = list[k];
   int s, t, xs, ys;
   m.pair(r, s, t);
-  canonical_class(m.P, s, t, xs, ys);
-  double X[9], Y[9];
-  load_panel_vertices(m.P, xs, X);
-  load_panel_vertices(m.P, ys, Y);
-  const double I = regular_sum<n>(X, Y);
-  m.put(r, dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi));
+  map_class(m, s, t, xs, ys);
+  m.put(r, map_regular<n>(m, xs, ys));
 }
 
+// triangles: KIND 0 identical, 1 edge, 2 vertex; quads: KIND 0 = touching quads (the four
+// triangle pairs; their evaluations are counted into qev)
 template <int KIND, class M>
-__global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __restrict__ list, int64_t cnt) {
+__global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __restrict__ list, int64_t cnt,
+                                                      unsigned long long* __restrict__ qev) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if constexpr (M::kQuad) {
+    unsigned long long ev = 0;
+    if (k < cnt) {
+      const EntryRef r = list[k];
+      int s, t, xs, ys;
+      m.pair(r, s, t);
+      map_class(m, s, t, xs, ys);
+      m.put(r, quad_split_entry(m.PT, xs, ys, ev));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    if ((threadIdx.x & 31) == 0 && ev) atomicAdd(qev, ev);
+    return;
+  }
   if (k >= cnt) return;
   const EntryRef r = list[k];
   int s, t, xs, ys;
@@ -105,69 +152,6 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
   m.put(r, v);
 }
 
-// Fused single-pass variant for batches dominated by cheap regular classes (ACA rows and
-// columns: admissible blocks are far apart, so nearly every entry is order 3 or 4): a CTA of
-// 256 threads classifies its 256 entries, counting-sorts them by class in shared memory and
-// then evaluates in sorted order, so warps are uniform except at class boundaries.  No
-// global lists, no host round trip.
-template <class M>
-__global__ void __launch_bounds__(256) k_eval_fused(M m, int64_t total, unsigned long long* __restrict__ evals) {
-  __shared__ unsigned int cnt[kNumClass + 1];
-  __shared__ EntryRef sref[256];
-  __shared__ unsigned char scls[256];
-  if (threadIdx.x <= kNumClass) cnt[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  EntryRef r;
-  int cls = kNumClass;                       // kNumClass = no work
-  if (m.locate(e, e < total, r)) {
-    int s, t, xs, ys;
-    m.pair(r, s, t);
-    cls = canonical_class(m.P, s, t, xs, ys);
-  }
-  // counting sort of (cls, ref), heavy classes first: order 6,5,4,3, edge, vertex, identical, none
-  const int key = cls == kNumClass ? 7 : cls >= 3 ? 6 - cls : cls == 1 ? 4 : cls == 2 ? 5 : 6;
-  const unsigned pos = atomicAdd(&cnt[key], 1u);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned acc = 0;
-    for (int k = 0; k <= kNumClass; ++k) { unsigned c = cnt[k]; cnt[k] = acc; acc += c; }
-  }
-  __syncthreads();
-  sref[cnt[key] + pos] = r;
-  scls[cnt[key] + pos] = (unsigned char)cls;
-  __syncthreads();
-  const int my = scls[threadIdx.x];
-  unsigned long long ev = 0;
-  if (my < kNumClass) {
-    const EntryRef rr = sref[threadIdx.x];
-    int s, t, xs, ys;
-    m.pair(rr, s, t);
-    canonical_class(m.P, s, t, xs, ys);
-    double v;
-    if (my >= 3) {
-      double X[9], Y[9], I;
-      load_panel_vertices(m.P, xs, X);
-      load_panel_vertices(m.P, ys, Y);
-      switch (my) {
-        case 3: I = regular_sum<3>(X, Y); break;
-        case 4: I = regular_sum<4>(X, Y); break;
-        case 5: I = regular_sum<5>(X, Y); break;
-        default: I = regular_sum<6>(X, Y); break;
-      }
-      v = dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi);
-    } else {
-      v = entry_st(m.P, s, t);
-    }
-    ev = (unsigned long long)rule_evals(my);
-    m.put(rr, v);
-  }
-  // evaluation count, one atomic per warp
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
-  if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
-}
-
 // Three-kernel, host-sync-free variant for ACA rows / columns (nearly all entries are order 3,
 // most of the rest order 4):
 //   k_eval_class3   evaluates the order-3 entries in place (others exit at once) and appends
@@ -184,7 +168,7 @@ __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, int64_t total, Entr
   if (m.locate(e, e < total, r)) {
     int s, t;
     m.pair(r, s, t);
-    cls = canonical_class(m.P, s, t, xs, ys);
+    cls = map_class(m, s, t, xs, ys);
   }
   const unsigned mask = __activemask();
   const int lane = threadIdx.x & 31;
@@ -202,11 +186,7 @@ __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, int64_t total, Entr
   else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
   unsigned long long ev = 0;
   if (cls == 3) {
-    double X[9], Y[9];
-    load_panel_vertices(m.P, xs, X);
-    load_panel_vertices(m.P, ys, Y);
-    const double I = regular_sum<3>(X, Y);
-    m.put(r, dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi));
+    m.put(r, map_regular<3>(m, xs, ys));
     ev = 81;
   }
 #pragma unroll
@@ -223,12 +203,8 @@ __global__ void __launch_bounds__(128) k_eval_list(M m, const EntryRef* __restri
     const EntryRef r = list[k];
     int s, t, xs, ys;
     m.pair(r, s, t);
-    canonical_class(m.P, s, t, xs, ys);
-    double X[9], Y[9];
-    load_panel_vertices(m.P, xs, X);
-    load_panel_vertices(m.P, ys, Y);
-    const double I = regular_sum<n>(X, Y);
-    m.put(r, dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi));
+    map_class(m, s, t, xs, ys);
+    m.put(r, map_regular<n>(m, xs, ys));
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(evals, (unsigned long long)(n * n * n * n) * (unsigned long long)c);
 }
@@ -242,35 +218,15 @@ __global__ void __launch_bounds__(128) k_eval_rest(M m, const EntryRef* __restri
   unsigned long long ev = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < c; k += (int64_t)gridDim.x * blockDim.x) {
     const EntryRef r = lists[total - 1 - k];
-    int s, t, xs, ys;
+    int s, t;
     m.pair(r, s, t);
-    const int cls = canonical_class(m.P, s, t, xs, ys);
-    m.put(r, entry_st(m.P, s, t));
-    ev += (unsigned long long)rule_evals(cls);
+    m.put(r, map_entry(m, s, t, ev));
   }
   if (ev) atomicAdd(evals, ev);
 }
 
-// Quadrilateral meshes (A25): one thread per entry, the four triangle pairs of quad_entry
-// with their own rules (no class buckets: in far-field blocks the four pairs mostly share
-// one order, near-field warps diverge over the classes).
-template <class M>
-__global__ void __launch_bounds__(128) k_eval_quad(M m, int64_t total, unsigned long long* __restrict__ evals) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  EntryRef r;
-  unsigned long long ev = 0;
-  if (m.locate(e, e < total, r)) {
-    int s, t;
-    m.pair(r, s, t);
-    m.put(r, quad_entry(m.P, s, t, ev));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
-  if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
-}
-
 struct EntryBatchWork {
-  DBuf<unsigned long long> cnt, cursor;
+  DBuf<unsigned long long> cnt, cursor, qev;   // qev: evaluations of touching quads (device)
   DBuf<EntryRef> list;
   unsigned long long hcnt[kNumClass];
 };
@@ -278,21 +234,11 @@ struct EntryBatchWork {
 // Evaluate all `total` entries of mapping m on stream st; returns the number of kernel
 // evaluations.  Allocates only when W is smaller than this batch (near_prepare pre-sizes it).
 template <class M>
-double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t st, KTimer& kt, bool quad) {
+double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t st, KTimer& kt) {
   if (total <= 0) return 0.0;
   W.cnt.alloc(kNumClass);
   W.cursor.alloc(kNumClass);
-  if (quad) {
-    HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, sizeof(unsigned long long), st));
-    {
-      KScope ks(kt, st, KF_EVAL_NEAR);
-      k_eval_quad<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.cnt.get());
-      HM_CHECK_LAUNCH();
-    }
-    HM_CUDA(cudaMemcpyAsync(W.hcnt, W.cnt.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    HM_CUDA(cudaStreamSynchronize(st));
-    return (double)W.hcnt[0];
-  }
+  W.qev.alloc(1);
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, kNumClass * sizeof(unsigned long long), st));
   k_class_count<M><<<grid_for(total, 256), 256, 0, st>>>(m, total, W.cnt.get());
   HM_CHECK_LAUNCH();
@@ -308,13 +254,14 @@ double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t s
   double evals = 0;
   // heavy classes first so that the light ones fill the tail
   KScope ks(kt, st, KF_EVAL_NEAR);
-  if (W.hcnt[1]) { k_eval_touching<1, M><<<grid_for(W.hcnt[1], 64), 64, 0, st>>>(m, L + base[1], W.hcnt[1]); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[2]) { k_eval_touching<2, M><<<grid_for(W.hcnt[2], 64), 64, 0, st>>>(m, L + base[2], W.hcnt[2]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[1]) { k_eval_touching<1, M><<<grid_for(W.hcnt[1], 64), 64, 0, st>>>(m, L + base[1], W.hcnt[1], W.qev.get()); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[2]) { k_eval_touching<2, M><<<grid_for(W.hcnt[2], 64), 64, 0, st>>>(m, L + base[2], W.hcnt[2], W.qev.get()); HM_CHECK_LAUNCH(); }
   if (W.hcnt[6]) { k_eval_regular<6, M><<<grid_for(W.hcnt[6], 128), 128, 0, st>>>(m, L + base[6], W.hcnt[6]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[5]) { k_eval_regular<5, M><<<grid_for(W.hcnt[5], 128), 128, 0, st>>>(m, L + base[5], W.hcnt[5]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[4]) { k_eval_regular<4, M><<<grid_for(W.hcnt[4], 128), 128, 0, st>>>(m, L + base[4], W.hcnt[4]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[3]) { k_eval_regular<3, M><<<grid_for(W.hcnt[3], 128), 128, 0, st>>>(m, L + base[3], W.hcnt[3]); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[0]) { k_eval_touching<0, M><<<grid_for(W.hcnt[0], 64), 64, 0, st>>>(m, L + base[0], W.hcnt[0]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[0]) { k_eval_touching<0, M><<<grid_for(W.hcnt[0], 64), 64, 0, st>>>(m, L + base[0], W.hcnt[0], W.qev.get()); HM_CHECK_LAUNCH(); }
+  // (quads: class 0 = touching quads, counted on the device into W.qev, read by the caller)
   const double per[kNumClass] = {0, 6480, 2592, 81, 256, 625, 1296};
   for (int c = 0; c < kNumClass; ++c) evals += per[c] * (double)W.hcnt[c];
   return evals;

@@ -234,7 +234,8 @@ struct Context {
   double eta = 1.0;
   bool quad = false;           // quadrilateral panels (A25): 2 triangle panels per node
   int64_t npanel = 0;          // triangle panels: N, or 2N for quads (panel 2s+a of node s)
-  DBuf<double> ncen;           // quads: node centroids, internal order (cluster boxes)
+  DBuf<Panel> qnode;           // quads: node panels (v = q0,q1,q2; c, h, area, app of the node)
+  DBuf<int4> qv;               // quads: the four vertex ids per node, internal order
   DBuf<Panel> panel;           // internal order
   DBuf<int32_t> perm, iperm;   // perm[s] = app index; iperm[app] = s
   DBuf<uint64_t> codes_app;    // Morton codes, application order

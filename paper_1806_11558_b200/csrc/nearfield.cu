@@ -18,9 +18,14 @@ __global__ void k_dense_sizes(const Quad* __restrict__ q, int64_t n, int64_t* __
   sz[b] = (int64_t)(q[b].rhi - q[b].rlo) * (q[b].chi - q[b].clo);
 }
 
-// leaves [b0, b0 + nseg) of the owned dense list; flattened entry e counts from off[b0]
+// leaves [b0, b0 + nseg) of the owned dense list; flattened entry e counts from off[b0].
+// QUAD: quadrilateral mesh (P = node panels, PT = split triangles, QV = vertex ids; A25)
+template <bool QUAD>
 struct NearMap {
+  static constexpr bool kQuad = QUAD;
   const Panel* P;
+  const Panel* PT;
+  const int4* QV;
   const Quad* q;
   const int64_t* off;    // owned-list offsets (nb + 1)
   int64_t b0, nseg;      // first leaf of the chunk, leaves in the chunk
@@ -96,6 +101,7 @@ void near_prepare(Context& C) {
   EntryBatchWork& W = *C.near_ws;
   W.cnt.alloc(kNumClass);
   W.cursor.alloc(kNumClass);
+  W.qev.alloc(1);
   W.list.alloc(maxc);
   C.near_tab.alloc(maxc / 32 + 2);
 }
@@ -106,17 +112,27 @@ void near_eval(Context& C, cudaStream_t st, KTimer& kt) {
   if (nb == 0 || hoff[nb] == 0) return;
   const Quad* q = C.dense.get() + C.dense_begin;
   EntryBatchWork& W = *C.near_ws;
+  HM_CUDA(cudaMemsetAsync(W.qev.get(), 0, sizeof(unsigned long long), st));
   double evals = 0;
   for (int64_t b0 = 0; b0 < nb;) {
     const int64_t b1 = near_chunk_end(hoff, nb, b0);
     k_seg_table<<<grid_for(b1 - b0, 256), 256, 0, st>>>(C.doff.get() + b0, b1 - b0, hoff[b0], C.near_tab.get());
     HM_CHECK_LAUNCH();
-    NearMap m{C.panel.get(), q, C.doff.get(), b0, b1 - b0, hoff[b0], C.dstore.get(), C.near_tab.get()};
-    evals += eval_batched(m, hoff[b1] - hoff[b0], W, st, kt, C.quad);
+    if (C.quad) {
+      NearMap<true> m{C.qnode.get(), C.panel.get(), C.qv.get(), q, C.doff.get(), b0, b1 - b0, hoff[b0],
+                      C.dstore.get(), C.near_tab.get()};
+      evals += eval_batched(m, hoff[b1] - hoff[b0], W, st, kt);
+    } else {
+      NearMap<false> m{C.panel.get(), nullptr, nullptr, q, C.doff.get(), b0, b1 - b0, hoff[b0], C.dstore.get(),
+                       C.near_tab.get()};
+      evals += eval_batched(m, hoff[b1] - hoff[b0], W, st, kt);
+    }
     b0 = b1;
   }
+  unsigned long long qev = 0;
+  HM_CUDA(cudaMemcpyAsync(&qev, W.qev.get(), sizeof(qev), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
-  C.evals_near = evals;
+  C.evals_near = evals + (double)qev;
 }
 
 void near_check(Context& C) {

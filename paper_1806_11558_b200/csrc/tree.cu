@@ -166,8 +166,9 @@ __global__ void k_gather_panels(const double* __restrict__ V, const int32_t* __r
 __global__ void k_gather_panels_quad(const double* __restrict__ V, const int32_t* __restrict__ Qv,
                                      const double* __restrict__ cen, const double* __restrict__ tcen,
                                      const double* __restrict__ tarea, const double* __restrict__ th,
+                                     const double* __restrict__ area, const double* __restrict__ hh,
                                      const int32_t* __restrict__ perm, int64_t N, Panel* __restrict__ P,
-                                     int32_t* __restrict__ iperm, double* __restrict__ ncen) {
+                                     int32_t* __restrict__ iperm, Panel* __restrict__ Pn, int4* __restrict__ QV) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= 2 * N) return;
   const int64_t s = p >> 1;
@@ -188,7 +189,19 @@ __global__ void k_gather_panels_quad(const double* __restrict__ V, const int32_t
   P[p] = pn;
   if (a == 0) {
     iperm[i] = (int32_t)s;
-    for (int k = 0; k < 3; ++k) ncen[3 * s + k] = cen[3 * (int64_t)i + k];
+    const int4 q = reinterpret_cast<const int4*>(Qv)[i];
+    QV[s] = q;
+    Panel nd;
+    const int32_t ids[3] = {q.x, q.y, q.z};
+    for (int r = 0; r < 3; ++r) {
+      nd.vid[r] = ids[r];
+      for (int k = 0; k < 3; ++k) nd.v[3 * r + k] = V[3 * (int64_t)ids[r] + k];
+    }
+    for (int k = 0; k < 3; ++k) nd.c[k] = cen[3 * (int64_t)i + k];
+    nd.area = area[i];
+    nd.h = hh[i];
+    nd.app = i;
+    Pn[s] = nd;
   }
 }
 
@@ -447,10 +460,12 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   });
   C.panel.alloc(C.npanel);
   if (C.quad) {
-    C.ncen.alloc(N * 3);
+    C.qnode.alloc(N);
+    C.qv.alloc(N);
     k_gather_panels_quad<<<grid_for(2 * N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), cen.get(), ws.tcen.get(),
-                                                                 ws.tarea.get(), ws.th.get(), C.perm.get(), N,
-                                                                 C.panel.get(), C.iperm.get(), C.ncen.get());
+                                                                 ws.tarea.get(), ws.th.get(), area.get(), hh.get(),
+                                                                 C.perm.get(), N, C.panel.get(), C.iperm.get(),
+                                                                 C.qnode.get(), C.qv.get());
   } else {
     k_gather_panels<<<grid_for(N, 256), 256, 0, st>>>(C.vert.get(), C.tri.get(), cen.get(), area.get(), hh.get(),
                                                        C.perm.get(), N, C.panel.get(), C.iperm.get());
@@ -492,10 +507,9 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   C.cl_box.alloc(6 * C.ncl); C.cl_diam2.alloc(C.ncl);
   for (int level = nlev - 1; level >= 0; --level) {
     int64_t b = lev[level], e = lev[level + 1];
-    const double* cb = C.quad ? C.ncen.get()
-                              : reinterpret_cast<const double*>(reinterpret_cast<const char*>(C.panel.get()) +
-                                                                offsetof(Panel, c));
-    const int cstride = C.quad ? 3 : (int)(sizeof(Panel) / sizeof(double));
+    const Panel* nodes = C.quad ? C.qnode.get() : C.panel.get();
+    const double* cb = reinterpret_cast<const double*>(reinterpret_cast<const char*>(nodes) + offsetof(Panel, c));
+    const int cstride = (int)(sizeof(Panel) / sizeof(double));
     k_boxes<<<grid_for(e - b, 128), 128, 0, st>>>(cb, cstride, C.cl_lo.get(), C.cl_hi.get(), C.cl_child.get(),
                                                    b, e, C.cl_box.get(), C.cl_diam2.get());
     HM_CHECK_LAUNCH();
