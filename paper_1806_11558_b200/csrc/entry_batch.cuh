@@ -15,6 +15,8 @@
 //                                                    quads (four triangle pairs over PT), classes
 //                                                    3..6 = separated quads, tensor rule on P
 #pragma once
+#include <cub/cub.cuh>
+
 #include "entry.cuh"
 
 namespace hm {
@@ -225,8 +227,29 @@ __global__ void __launch_bounds__(128) k_eval_rest(M m, const EntryRef* __restri
   if (ev) atomicAdd(evals, ev);
 }
 
+// Touching quads (A25) sorted by the classes of their four triangle pairs (3 bits each), so
+// that the warps of k_eval_touching<0> run one rule sequence.
+template <class M>
+__global__ void k_quad_sig(M m, const EntryRef* __restrict__ list, int64_t cnt, uint16_t* __restrict__ key,
+                           unsigned long long* __restrict__ ref) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  const EntryRef r = list[k];
+  int s, t, xs, ys;
+  m.pair(r, s, t);
+  map_class(m, s, t, xs, ys);
+  unsigned sig = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sig |= (unsigned)entry_class(m.PT[2 * xs + (q >> 1)], m.PT[2 * ys + (q & 1)]) << (3 * q);
+  key[k] = (uint16_t)sig;
+  ref[k] = reinterpret_cast<const unsigned long long&>(r);
+}
+
 struct EntryBatchWork {
   DBuf<unsigned long long> cnt, cursor, qev;   // qev: evaluations of touching quads (device)
+  DBuf<uint16_t> qkey[2];                      // touching quads: signature sort
+  DBuf<unsigned long long> qref[2];
+  DBuf<char> qtmp;
   DBuf<EntryRef> list;
   unsigned long long hcnt[kNumClass];
 };
@@ -254,13 +277,30 @@ double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t s
   double evals = 0;
   // heavy classes first so that the light ones fill the tail
   KScope ks(kt, st, KF_EVAL_NEAR);
+  if constexpr (M::kQuad) {        // touching quads first, sorted by their sub-pair classes
+    const int64_t c0 = (int64_t)W.hcnt[0];
+    if (c0) {
+      for (int b = 0; b < 2; ++b) { W.qkey[b].alloc(c0); W.qref[b].alloc(c0); }
+      k_quad_sig<M><<<grid_for(c0, 256), 256, 0, st>>>(m, L + base[0], c0, W.qkey[0].get(), W.qref[0].get());
+      HM_CHECK_LAUNCH();
+      size_t tb = 0;
+      HM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, W.qkey[0].get(), W.qkey[1].get(), W.qref[0].get(),
+                                              W.qref[1].get(), (int)c0, 0, 12, st));
+      W.qtmp.alloc(tb);
+      HM_CUDA(cub::DeviceRadixSort::SortPairs(W.qtmp.get(), tb, W.qkey[0].get(), W.qkey[1].get(), W.qref[0].get(),
+                                              W.qref[1].get(), (int)c0, 0, 12, st));
+      const EntryRef* Ls = reinterpret_cast<const EntryRef*>(W.qref[1].get());
+      k_eval_touching<0, M><<<grid_for(c0, 64), 64, 0, st>>>(m, Ls, c0, W.qev.get());
+      HM_CHECK_LAUNCH();
+    }
+  }
   if (W.hcnt[1]) { k_eval_touching<1, M><<<grid_for(W.hcnt[1], 64), 64, 0, st>>>(m, L + base[1], W.hcnt[1], W.qev.get()); HM_CHECK_LAUNCH(); }
   if (W.hcnt[2]) { k_eval_touching<2, M><<<grid_for(W.hcnt[2], 64), 64, 0, st>>>(m, L + base[2], W.hcnt[2], W.qev.get()); HM_CHECK_LAUNCH(); }
   if (W.hcnt[6]) { k_eval_regular<6, M><<<grid_for(W.hcnt[6], 128), 128, 0, st>>>(m, L + base[6], W.hcnt[6]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[5]) { k_eval_regular<5, M><<<grid_for(W.hcnt[5], 128), 128, 0, st>>>(m, L + base[5], W.hcnt[5]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[4]) { k_eval_regular<4, M><<<grid_for(W.hcnt[4], 128), 128, 0, st>>>(m, L + base[4], W.hcnt[4]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[3]) { k_eval_regular<3, M><<<grid_for(W.hcnt[3], 128), 128, 0, st>>>(m, L + base[3], W.hcnt[3]); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[0]) { k_eval_touching<0, M><<<grid_for(W.hcnt[0], 64), 64, 0, st>>>(m, L + base[0], W.hcnt[0], W.qev.get()); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[0] && !M::kQuad) { k_eval_touching<0, M><<<grid_for(W.hcnt[0], 64), 64, 0, st>>>(m, L + base[0], W.hcnt[0], W.qev.get()); HM_CHECK_LAUNCH(); }
   // (quads: class 0 = touching quads, counted on the device into W.qev, read by the caller)
   const double per[kNumClass] = {0, 6480, 2592, 81, 256, 625, 1296};
   for (int c = 0; c < kNumClass; ++c) evals += per[c] * (double)W.hcnt[c];
