@@ -97,7 +97,8 @@ const char* hm_last_error(hm_ctx ctx);
  *   "max_iter"     Krylov iteration cap (total matvecs), default 10000
  *   "aca_chunk_mb" ACA workspace budget per chunk in MiB, default 32768, capped before every
  *                  chunk at 0.45 x (free device memory + current workspace)
- *   "aca_kws"      ACA workspace columns per block before the overflow re-run, default 12
+ *   "aca_kws"      ACA workspace columns per block before the overflow re-run (blocks that
+ *                  fill it restart with twice the columns, up to k_max), default 16
  *   "record_pivots" keep each block's ACA pivot sequence for hm_get_lowrank: 1 on, 0 off,
  *                  -1 (default) on iff N <= 25000
  *   "kernel_timing" 1: record CUDA events on the context stream around every launch of

@@ -784,23 +784,28 @@ void setup_aca(Context& C) {
     if (b < nb) { ids.push_back((int32_t)b); used += need; }
   }
   C.aca_overflow = (int)overflow.size();
-  if (!overflow.empty()) {          // re-run with the full rank budget, chunked by the same budget
-    std::vector<int32_t> none, part;
+  // re-run blocks that filled the workspace from scratch (ACA is deterministic: same pivots,
+  // same factors) with twice the columns, until the full rank budget k_max; a smaller
+  // workspace per block keeps the re-run chunks few (C6: 203k blocks overflow 12 columns,
+  // none 24)
+  for (int kw = std::min(C.k_max, 2 * kws); !overflow.empty(); kw = std::min(C.k_max, 2 * kw)) {
+    std::vector<int32_t> again, part;
     double u2 = 0;
     for (size_t x = 0; x <= overflow.size(); ++x) {
       double need = 0;
       if (x < overflow.size()) {
         const Quad& q = C.h_adm[C.adm_begin + overflow[x]];
-        need = 8.0 * C.k_max * ((q.rhi - q.rlo) + (q.chi - q.clo)) + 64.0;
+        need = 8.0 * kw * ((q.rhi - q.rlo) + (q.chi - q.clo)) + 64.0;
       }
       if (x == overflow.size() || (!part.empty() && u2 + need > budget)) {
-        if (!part.empty()) { run_chunk(C, W, part, C.k_max, none, rec ? &pivots : nullptr); budget = chunk_budget(); }
+        if (!part.empty()) { run_chunk(C, W, part, kw, again, rec ? &pivots : nullptr); budget = chunk_budget(); }
         part.clear();
         u2 = 0;
       }
       if (x < overflow.size()) { part.push_back(overflow[x]); u2 += need; }
     }
-    if (!none.empty()) fail(HM_ERR_CUDA, "ACA overflow re-run did not converge within k_max");
+    if (!again.empty() && kw >= C.k_max) fail(HM_ERR_CUDA, "ACA overflow re-run did not converge within k_max");
+    overflow.swap(again);
   }
   const auto t5 = clk::now();
   C.h_rank.resize(nb);

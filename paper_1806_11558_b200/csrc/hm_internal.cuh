@@ -225,7 +225,7 @@ struct Context {
   // options
   int k_max = 64, solver = 0, restart = 100, max_iter = 10000;
   int record_pivots = -1;      // -1 auto (N <= 25000), 0 off, 1 on
-  double aca_chunk_mb = 32768, aca_kws = 12;
+  double aca_chunk_mb = 32768, aca_kws = 16;
 
   // tree state
   bool have_tree = false, have_setup = false;

@@ -12,6 +12,8 @@ H = HMatrix(device=0)
 H.build_tree(V, T, 32, 1.0)
 if os.environ.get("HM_KT"):
     H.set_option("kernel_timing", 1)
+if os.environ.get("HM_KWS"):
+    H.set_option("aca_kws", int(os.environ["HM_KWS"]))
 if os.environ.get("HM_OVERLAP"):
     H.set_option("setup_overlap", int(os.environ["HM_OVERLAP"]))
 for _ in range(int(os.environ.get("HM_SETUPS", "1"))):
