@@ -24,6 +24,17 @@ def test_library_loads_and_exports_all_symbols():
         assert hasattr(L, n), f"libhm.so does not export {n}"
 
 
+def test_mesh_struct_matches_header():
+    # the ctypes hm_mesh of the binding has the header's fields, in order, with its C layout
+    from paper_1806_11558_b200 import hm
+    src = open(os.path.join(ROOT, "include", "hm.h")).read()
+    body = re.search(r"typedef struct \{([^}]*)\} hm_mesh;", src).group(1)
+    fields = re.findall(r"\b(\w+)\s*;", body)
+    assert fields == [f[0] for f in hm._Mesh._fields_]
+    assert fields[-1] == "panel_vertices"
+    assert ctypes.sizeof(hm._Mesh) == 40 and hm._Mesh.panel_vertices.offset == 36   # x86-64 C layout
+
+
 def test_library_is_sm100a_only():
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
@@ -90,6 +101,14 @@ def test_error_codes_and_state_machine():
     assert st["N"] == 320 and st["adm_leaves"] == 0 and st["dense_leaves"] == 256
     with pytest.raises(HMError):
         H.solve(torch.ones(320, dtype=torch.float64, device="cuda"), tol=0.0)
+    # quadrilateral meshes: panel_vertices 4 accepted, others rejected
+    from inputs.meshes import cube
+    Vq, Qq = cube(2)
+    H3 = HMatrix(device=0)
+    H3.build_tree(Vq, Qq)
+    assert H3.stats()["N"] == 96
+    with pytest.raises(HMError):
+        H3.build_tree(Vq, np.ascontiguousarray(np.concatenate([Qq, Qq[:, :1]], axis=1)))   # 5 vertices
     # device-resident mesh input gives the same tree
     H2 = HMatrix(device=0)
     H2.build_tree(torch.from_numpy(V).cuda(), torch.from_numpy(T).cuda())
