@@ -112,6 +112,9 @@ const char* hm_last_error(hm_ctx ctx);
  *                  matvec (hm_get_stats "mv_prof_cycles"); diagnostic
  *   "mv_scramble"  1: DIAGNOSTIC ONLY, wrong products: spread the row bases of the CTA-ring
  *                  matvec's y atomics over y (measures same-address atomic contention)
+ *   "mv_concurrent" 1 (default): the large low-rank matvec kernels run on a library side
+ *                  stream beside the small-leaf pipeline (joined before hm_matvec returns its
+ *                  stream order); 0: one stream
  *   "setup_overlap" 1: hm_setup evaluates the near field on a least-priority stream from a
  *                  second host thread while ACA runs on a greatest-priority stream (results
  *                  bit-identical; ~5% shorter setup at N = 1.57M); 0 (default) serial.  With

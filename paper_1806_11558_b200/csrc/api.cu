@@ -327,7 +327,8 @@ hm_status hm_destroy(hm_ctx ctx) {
     hm::Context& C = ctx->C;
     if (C.s_hi) { cudaStreamSynchronize(C.s_hi); cudaStreamDestroy(C.s_hi); }
     if (C.s_lo) { cudaStreamSynchronize(C.s_lo); cudaStreamDestroy(C.s_lo); }
-    for (cudaEvent_t e : {C.ev_fork, C.ev_join[0], C.ev_join[1]}) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {C.ev_fork, C.ev_join[0], C.ev_join[1], C.mv_ev[0], C.mv_ev[1]}) if (e) cudaEventDestroy(e);
+    if (C.mv_side) { cudaStreamSynchronize(C.mv_side); cudaStreamDestroy(C.mv_side); }
   }
   delete ctx;
   if (own && st) cudaStreamDestroy(st);
@@ -357,6 +358,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "mv_small_max") { if (v < 0 || v > 49152) bad(); C.mv_small_max = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_scramble") { if (v != 0 && v != 1) bad(); C.mv_scramble = (int)v; }
     else if (k == "setup_overlap") { if (v != 0 && v != 1) bad(); C.setup_overlap = (int)v; }
+    else if (k == "mv_concurrent") { if (v != 0 && v != 1) bad(); C.mv_concurrent = (int)v; }
     else if (k == "kernel_timing") {
       if (v != 0 && v != 1) bad();
       HM_CUDA(cudaStreamSynchronize(C.stream));
@@ -382,6 +384,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "kernel_timing") *v = C.kt.on ? 1 : 0;
     else if (k == "mv_kernel") *v = C.mv_kind;
     else if (k == "setup_overlap") *v = C.setup_overlap;
+    else if (k == "mv_concurrent") *v = C.mv_concurrent;
     else hm::fail(HM_ERR_ARG, "hm_get_option: unknown key '" + k + "'");
   });
 }

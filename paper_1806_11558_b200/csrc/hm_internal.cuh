@@ -283,6 +283,9 @@ struct Context {
   DBuf<unsigned long long> mv_prof;   // option "mv_profile": [producer empty-wait, consumer full-wait, consumer work] cycles
   int mv_small_max = 16384;    // option "mv_small_max": low-rank leaves up to this many bytes go through the pipeline
   int mv_scramble = 0;         // diagnostic option "mv_scramble" (wrong results): see k_mv_batched
+  int mv_concurrent = 1;       // option "mv_concurrent": large low-rank kernels on a side stream
+  cudaStream_t mv_side = nullptr;
+  cudaEvent_t mv_ev[2] = {nullptr, nullptr};
   int mv_kind = 0;             // option "mv_kernel": 0 two CTA rings per SM, 2 x 48 KiB each (default); 1 one ring of 4
   int64_t mv_nbatches = 0, mv_tlen = 0, mv_nsegs = 0;
   int64_t n_lr_small = 0, n_lr_large = 0;

@@ -781,6 +781,26 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
   HM_CUDA(cudaMemsetAsync(y_int, 0, C.N * sizeof(double), st));
   if (C.mv_tlen) HM_CUDA(cudaMemsetAsync(C.mv_tbuf.get(), 0, C.mv_tlen * sizeof(double), st));
   const double* pool = (const double*)C.fpool.base;
+  // option mv_concurrent (default on): the large low-rank blocks (V^T x, then U z) stream on
+  // a side stream while the CTA rings stream the small blocks, so one kernel family's tail
+  // overlaps the other's streaming (C4: 27.9 -> 27.6 ms)
+  const bool conc = C.mv_concurrent && C.mv_n_tiles_v && C.mv_nbatches;
+  if (conc) {
+    if (!C.mv_side) {
+      HM_CUDA(cudaStreamCreateWithFlags(&C.mv_side, cudaStreamNonBlocking));
+      HM_CUDA(cudaEventCreateWithFlags(&C.mv_ev[0], cudaEventDisableTiming));
+      HM_CUDA(cudaEventCreateWithFlags(&C.mv_ev[1], cudaEventDisableTiming));
+    }
+    HM_CUDA(cudaEventRecord(C.mv_ev[0], st));
+    HM_CUDA(cudaStreamWaitEvent(C.mv_side, C.mv_ev[0], 0));
+    k_mv_large_v<<<148 * 8, 256, 0, C.mv_side>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
+                                                 C.mv_tbuf.get());
+    HM_CHECK_LAUNCH();
+    k_mv_large_u<<<148 * 8, 256, 0, C.mv_side>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
+                                                 C.mv_tbuf.get(), y_int);
+    HM_CHECK_LAUNCH();
+    HM_CUDA(cudaEventRecord(C.mv_ev[1], C.mv_side));
+  }
   if (C.mv_nbatches) {
     unsigned long long* prof = C.mv_prof.n ? C.mv_prof.get() : nullptr;
     const int64_t scramble = C.mv_scramble ? C.N - 4096 : 0;
@@ -799,7 +819,9 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
                                                x_int, y_int);
     HM_CHECK_LAUNCH();
   }
-  if (C.mv_n_tiles_v) {
+  if (conc) {
+    HM_CUDA(cudaStreamWaitEvent(st, C.mv_ev[1], 0));
+  } else if (C.mv_n_tiles_v) {
     k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
                                           C.mv_tbuf.get());
     HM_CHECK_LAUNCH();

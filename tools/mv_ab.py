@@ -41,12 +41,13 @@ def timed(reps=20):
 
 
 ref = None
-for kind, sm in ((0, 16384), (1, 16384), (0, 8192), (0, 32768), (0, 16384)):
+for kind, sm, conc in ((0, 16384, 0), (0, 16384, 1), (1, 16384, 1), (0, 8192, 1), (0, 32768, 1), (0, 16384, 1)):
     H.set_option("mv_kernel", kind)
     H.set_option("mv_small_max", sm)
+    H.set_option("mv_concurrent", conc)
     ms, y = timed()
     ref = y if ref is None else ref
-    print(json.dumps({"config": cfg, "mv_kernel": kind, "mv_small_max": sm, "ms": round(ms, 4),
+    print(json.dumps({"config": cfg, "mv_kernel": kind, "mv_small_max": sm, "concurrent": conc, "ms": round(ms, 4),
                       "GBps": round((st["stored_bytes"] + 40 * N) / (ms * 1e-3) / 1e9, 1),
                       "mv_batches": H.stats()["mv_batches"], "mv_segs": H.stats()["mv_segs"],
                       "rel_diff": (torch.linalg.norm(y - ref) / torch.linalg.norm(ref)).item()}), flush=True)
