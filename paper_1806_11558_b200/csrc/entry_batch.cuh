@@ -65,8 +65,10 @@ __device__ __forceinline__ double map_entry(const M& m, int s, int t, unsigned l
   }
 }
 
+// pass 1 also records every entry's class (one byte) for pass 2
 template <class M>
-__global__ void k_class_count(M m, int64_t total, unsigned long long* __restrict__ cnt) {
+__global__ void k_class_count(M m, int64_t total, unsigned long long* __restrict__ cnt,
+                              unsigned char* __restrict__ ecls) {
   __shared__ unsigned int sc[kNumClass];
   if (threadIdx.x < kNumClass) sc[threadIdx.x] = 0;
   __syncthreads();
@@ -75,15 +77,17 @@ __global__ void k_class_count(M m, int64_t total, unsigned long long* __restrict
   if (m.locate(e, e < total, r)) {
     int s, t, xs, ys;
     m.pair(r, s, t);
-    atomicAdd(&sc[map_class(m, s, t, xs, ys)], 1u);
+    const int cls = map_class(m, s, t, xs, ys);
+    ecls[e] = (unsigned char)cls;
+    atomicAdd(&sc[cls], 1u);
   }
   __syncthreads();
   if (threadIdx.x < kNumClass && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
 }
 
 template <class M>
-__global__ void k_class_scatter(M m, int64_t total, unsigned long long* __restrict__ cursor,
-                                EntryRef* __restrict__ lists) {
+__global__ void k_class_scatter(M m, int64_t total, const unsigned char* __restrict__ ecls,
+                                unsigned long long* __restrict__ cursor, EntryRef* __restrict__ lists) {
   __shared__ unsigned int sc[kNumClass];
   __shared__ unsigned long long base[kNumClass];
   if (threadIdx.x < kNumClass) sc[threadIdx.x] = 0;
@@ -93,9 +97,7 @@ __global__ void k_class_scatter(M m, int64_t total, unsigned long long* __restri
   int cls = -1;
   unsigned int pos = 0;
   if (m.locate(e, e < total, r)) {
-    int s, t, xs, ys;
-    m.pair(r, s, t);
-    cls = map_class(m, s, t, xs, ys);
+    cls = ecls[e];
     pos = atomicAdd(&sc[cls], 1u);
   }
   __syncthreads();
@@ -247,6 +249,7 @@ __global__ void k_quad_sig(M m, const EntryRef* __restrict__ list, int64_t cnt, 
 
 struct EntryBatchWork {
   DBuf<unsigned long long> cnt, cursor, qev;   // qev: evaluations of touching quads (device)
+  DBuf<unsigned char> ecls;                    // class of every entry of the batch (pass 1)
   DBuf<uint16_t> qkey[2];                      // touching quads: signature sort
   DBuf<unsigned long long> qref[2];
   DBuf<char> qtmp;
@@ -262,8 +265,9 @@ double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t s
   W.cnt.alloc(kNumClass);
   W.cursor.alloc(kNumClass);
   W.qev.alloc(1);
+  W.ecls.alloc(total);
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, kNumClass * sizeof(unsigned long long), st));
-  k_class_count<M><<<grid_for(total, 256), 256, 0, st>>>(m, total, W.cnt.get());
+  k_class_count<M><<<grid_for(total, 256), 256, 0, st>>>(m, total, W.cnt.get(), W.ecls.get());
   HM_CHECK_LAUNCH();
   HM_CUDA(cudaMemcpyAsync(W.hcnt, W.cnt.get(), sizeof(W.hcnt), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
@@ -271,7 +275,7 @@ double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t s
   for (int c = 0; c < kNumClass; ++c) { base[c] = acc; acc += W.hcnt[c]; }
   W.list.alloc(acc);
   HM_CUDA(cudaMemcpyAsync(W.cursor.get(), base, sizeof(base), cudaMemcpyHostToDevice, st));
-  k_class_scatter<M><<<grid_for(total, 256), 256, 0, st>>>(m, total, W.cursor.get(), W.list.get());
+  k_class_scatter<M><<<grid_for(total, 256), 256, 0, st>>>(m, total, W.ecls.get(), W.cursor.get(), W.list.get());
   HM_CHECK_LAUNCH();
   const EntryRef* L = W.list.get();
   double evals = 0;

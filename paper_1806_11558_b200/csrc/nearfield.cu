@@ -103,6 +103,7 @@ void near_prepare(Context& C) {
   W.cursor.alloc(kNumClass);
   W.qev.alloc(1);
   W.list.alloc(maxc);
+  W.ecls.alloc(maxc);
   C.near_tab.alloc(maxc / 32 + 2);
 }
 
