@@ -256,6 +256,20 @@ def test_setup_overlap_bit_identical(c2):
     H.close()
 
 
+def test_matvec_options_agree(c2, torch_cuda):
+    # the small/large split, the two CTA-ring pipelines and the side-stream large kernels all
+    # compute the same product (up to the order of the FP64 atomics)
+    V, T, H, R = c2
+    x = torch_cuda.from_numpy(seeded_vector(T.shape[0], 3)).cuda()
+    ref = H.matvec(x).cpu().numpy()
+    for key, vals in (("mv_concurrent", (0, 1)), ("mv_kernel", (1, 0)), ("mv_small_max", (4096, 16384))):
+        for v in vals:
+            H.set_option(key, v)
+            y = H.matvec(x).cpu().numpy()
+            assert np.linalg.norm(y - ref) <= 1e-14 * np.linalg.norm(ref), (key, v)
+    assert H.get_option("mv_concurrent") == 1 and H.get_option("mv_kernel") == 0
+
+
 def test_c3_full_size_sampled_rows(O, torch_cuda):
     # configs[2] at full size, in the launch configuration bench.py times
     import torch
