@@ -45,6 +45,7 @@
 #include "oracle.h"
 
 #include <float.h>
+#include <quadmath.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -416,13 +417,14 @@ static tri_t make_tri(const double* v0, const double* v1, const double* v2) {
 }
 
 /* collapsed-Gauss reference table of order n: s = xi, t = xi*zeta, w = (w_xi*w_zeta)*xi */
-typedef struct { int n; double s[64], t[64], w[64]; } reftab_t;
+typedef struct { int n, np; double s[64], t[64], w[64]; } reftab_t;   /* np points */
 
 static reftab_t make_reftab(int n) {
   reftab_t R;
   double g[32], gw[32];
   or_gauss_legendre01(n, g, gw);
   R.n = n;
+  R.np = n * n;
   for (int a = 0; a < n; ++a)
     for (int b = 0; b < n; ++b) {
       int q = a * n + b;
@@ -433,13 +435,54 @@ static reftab_t make_reftab(int n) {
   return R;
 }
 
+/* Radon's 7-point rule, exact to degree 5 (Radon 1948; Stroud T2:5-1), the A14 rule of the
+ * rho >= 8 band: barycentric (1/3,1/3,1/3) weight 9/40; the three permutations of
+ * (a, a, 1-2a), a = (6 - sqrt15)/21, weight (155 - sqrt15)/1200; of (b, b, 1-2b),
+ * b = (6 + sqrt15)/21, weight (155 + sqrt15)/1200.  In the (s, t) form of chi with
+ * lambda = (1 - s, s - t, t): s = 1 - lambda0, t = lambda2; weights halved (reference area
+ * 1/2, like the collapsed rule).  Order: centre, (a,a,c), (a,c,a), (c,a,a), then b.
+ * Values in binary128 (libquadmath), rounded once to binary64. */
+static reftab_t make_reftab_radon(void) {
+  reftab_t R;
+  R.n = 3;
+  R.np = 7;
+  const __float128 r15 = sqrtq((__float128)15);
+  const __float128 abc[2] = {(6 - r15) / 21, (6 + r15) / 21};
+  const __float128 wab[2] = {(155 - r15) / 2400, (155 + r15) / 2400};
+  const __float128 third = (__float128)1 / 3;
+  R.s[0] = (double)(1 - third); R.t[0] = (double)third; R.w[0] = (double)((__float128)9 / 80);
+  for (int g = 0; g < 2; ++g) {
+    const __float128 a = abc[g], c = 1 - 2 * a;
+    const __float128 lam[3][3] = {{a, a, c}, {a, c, a}, {c, a, a}};
+    for (int k = 0; k < 3; ++k) {
+      const int q = 1 + 3 * g + k;
+      R.s[q] = (double)(1 - lam[k][0]);
+      R.t[q] = (double)lam[k][2];
+      R.w[q] = (double)wab[g];
+    }
+  }
+  return R;
+}
+
+/* number of points of the A14 rule of regular order n on one triangle */
+static int rule_points(const reftab_t* R) { return R->np; }
+
+/* the A14 rule table of regular order n: Radon for n = 3, collapsed Gauss n x n otherwise */
+static reftab_t rule_table(int n) { return n == 3 ? make_reftab_radon() : make_reftab(n); }
+
+int or_rule_table(int n, double* s, double* t, double* w) {
+  reftab_t R = rule_table(n);
+  for (int q = 0; q < R.np; ++q) { s[q] = R.s[q]; t[q] = R.t[q]; w[q] = R.w[q]; }
+  return R.np;
+}
+
 static void tri_point(const tri_t* T, double s, double t, double* x) {
   for (int a = 0; a < 3; ++a) x[a] = fma(t, T->e2[a], fma(s, T->e1[a], T->v0[a]));
 }
 
 /* regular rule: I = sum_p w_p sum_q w_q / |x_p - y_q|  (unscaled by Jacobians) */
 static double regular_sum(const tri_t* X, const tri_t* Y, const reftab_t* R) {
-  int nq = R->n * R->n;
+  int nq = rule_points(R);
   double I = 0.0;
   for (int p = 0; p < nq; ++p) {
     double xp[3];
@@ -459,7 +502,7 @@ static double regular_sum(const tri_t* X, const tri_t* Y, const reftab_t* R) {
 
 double or_regular_rule(const double* tx, const double* ty, int n) {
   tri_t X = make_tri(tx, tx + 3, tx + 6), Y = make_tri(ty, ty + 3, ty + 6);
-  reftab_t R = make_reftab(n);
+  reftab_t R = rule_table(n);
   double c[3], ax, ay, h;
   panel_geometry(tx, tx + 3, tx + 6, c, &ax, &h);
   panel_geometry(ty, ty + 3, ty + 6, c, &ay, &h);
@@ -582,6 +625,7 @@ static reftab_t make_reftab_square(int n) {
   double g[32], gw[32];
   or_gauss_legendre01(n, g, gw);
   R.n = n;
+  R.np = n * n;
   for (int a = 0; a < n; ++a)
     for (int b = 0; b < n; ++b) {
       int q = a * n + b;
@@ -596,7 +640,7 @@ static reftab_t g_tab[7], g_qtab[7];
 static int g_tab_init = 0;
 static void init_tables(void) {
   if (g_tab_init) return;
-  for (int n = 3; n <= 6; ++n) { g_tab[n] = make_reftab(n); g_qtab[n] = make_reftab_square(n); }
+  for (int n = 3; n <= 6; ++n) { g_tab[n] = rule_table(n); g_qtab[n] = make_reftab_square(n); }
   g_tab_init = 1;
 }
 
@@ -692,7 +736,7 @@ static double entry_app(const or_problem* P, int64_t i, int64_t j, double* evals
   tri_t X = make_tri(vtx(P, x, 0), vtx(P, x, 1), vtx(P, x, 2));
   tri_t Y = make_tri(vtx(P, y, 0), vtx(P, y, 1), vtx(P, y, 2));
   const reftab_t* R = &g_tab[cls];
-  if (evals) *evals += (double)(cls * cls * cls * cls);
+  if (evals) *evals += (double)(R->np * R->np);
   double I = regular_sum(&X, &Y, R);
   return (I * ((2.0 * P->area[x]) * (2.0 * P->area[y]))) * INV4PI;
 }
@@ -1106,17 +1150,17 @@ void or_partition(const int64_t* cost, int64_t n, int p, int64_t* out) {
 
 /* ---- single-layer potential at evaluation points (reading A23) ------
  * u(x) = (1/4pi) sum_j alpha_j int_{T_j} 1/|x - y| dy, alpha in application order.  Panel
- * integral: collapsed Gauss n x n on T_j (the regular rule's panel factor), n by the ratio
+ * integral: the A14 rule of order n on T_j (the regular rule's panel factor), n by the ratio
  * rho^2 = |x - c_j|^2 / h_j^2 in the bands of A14 (< 4: 6, < 16: 5, < 64: 4, else 3):
  *   I_j(x) = (2 |T_j|) * sum_q w_q / sqrt(d2_q),  d2 = fma(dz,dz, fma(dy,dy, dx*dx)).
  * Points must lie off the surface (the rule is not singular-aware). */
 double or_panel_potential(const double* x, const double* tri, int n) {
   tri_t T = make_tri(tri, tri + 3, tri + 6);
-  reftab_t R = make_reftab(n);
+  reftab_t R = rule_table(n);
   double c[3], area, h;
   panel_geometry(tri, tri + 3, tri + 6, c, &area, &h);
   double inner = 0.0;
-  for (int q = 0; q < n * n; ++q) {
+  for (int q = 0; q < R.np; ++q) {
     double y[3];
     tri_point(&T, R.s[q], R.t[q], y);
     double dx = x[0] - y[0], dy = x[1] - y[1], dz = x[2] - y[2];
@@ -1135,7 +1179,7 @@ void or_potential(const or_problem* P, const double* alpha, int64_t M, const dou
     return;
   }
   reftab_t R[4];
-  for (int n = 3; n <= 6; ++n) R[n - 3] = make_reftab(n);
+  for (int n = 3; n <= 6; ++n) R[n - 3] = rule_table(n);
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t p = 0; p < M; ++p) {
     const double* x = X + 3 * p;
@@ -1150,7 +1194,7 @@ void or_potential(const or_problem* P, const double* alpha, int64_t M, const dou
       tri_t T = make_tri(P->V + 3 * t[0], P->V + 3 * t[1], P->V + 3 * t[2]);
       const reftab_t* Rn = &R[n - 3];
       double inner = 0.0;
-      for (int q = 0; q < n * n; ++q) {
+      for (int q = 0; q < Rn->np; ++q) {
         double y[3];
         tri_point(&T, Rn->s[q], Rn->t[q], y);
         double ex = x[0] - y[0], ey = x[1] - y[1], ez = x[2] - y[2];

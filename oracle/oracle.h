@@ -69,8 +69,12 @@ double or_sauter_schwab(int kind, const double* tx, const double* ty, int nq);
 /* Sauter-Schwab on the reference pair with a user integrand g(x1,x2,y1,y2) = polynomial
  * prod  x1^a x2^b y1^c y2^d  (tests the measure preservation of the maps). */
 double or_ss_reference_monomial(int kind, int nq, int a, int b, int c, int d);
-/* Regular collapsed-Gauss rule of order n for 1/|x-y| over two triangles (9 doubles each). */
+/* Regular rule of order n of A14 (Radon's 7-point rule for n = 3, collapsed Gauss n x n
+ * otherwise) for 1/|x-y| over two triangles (9 doubles each). */
 double or_regular_rule(const double* tx, const double* ty, int n);
+/* The per-triangle table of that rule in the (s, t) form of chi (reference area 1/2):
+ * writes np <= 36 points and returns np. */
+int or_rule_table(int n, double* s, double* t, double* w);
 
 /* Dense rows of A (application indices) -> out[nrows*N]. */
 void or_dense_rows(const or_problem* P, int64_t nrows, const int64_t* rows, double* out);

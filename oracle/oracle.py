@@ -57,6 +57,7 @@ def lib():
         L.or_ss_reference_monomial.restype = d
         L.or_ss_reference_monomial.argtypes = [i32, i32, i32, i32, i32, i32]
         L.or_regular_rule.restype = d; L.or_regular_rule.argtypes = [ptr, ptr, i32]
+        L.or_rule_table.restype = i32; L.or_rule_table.argtypes = [i32, ptr, ptr, ptr]
         L.or_dense_rows.argtypes = [P, i64, ptr, ptr]
         L.or_aca_block.restype = i32
         L.or_aca_block.argtypes = [P, i32, i32, i32, i32, d, i32, ptr, ptr, ptr]
@@ -116,6 +117,12 @@ def regular_rule(tx, ty, n):
     a = np.ascontiguousarray(tx, dtype=np.float64).reshape(9)
     b = np.ascontiguousarray(ty, dtype=np.float64).reshape(9)
     return lib().or_regular_rule(_p(a), _p(b), n)
+
+
+def rule_table(n):
+    s = np.zeros(64); t = np.zeros(64); w = np.zeros(64)
+    k = lib().or_rule_table(n, _p(s), _p(t), _p(w))
+    return s[:k].copy(), t[:k].copy(), w[:k].copy()
 
 
 def panel_potential(x, tri, n):

@@ -119,7 +119,35 @@ def test_singular_entries_on_sphere_mesh(O):
         assert abs(a - ref) <= 2e-7 * ref
 
 
-@pytest.mark.parametrize("rho,n,tol", [(1.5, 6, 1e-8), (3.0, 5, 1e-8), (6.0, 4, 1e-8), (10.0, 3, 2e-8)])
+def test_radon_rule_table(O):
+    # A14's rho >= 8 rule: Radon's 7-point degree-5 formula (Stroud T2:5-1).  Pins: the table is
+    # the correctly rounded exact one (60-digit decimal here), it integrates every monomial
+    # s^i t^j of degree <= 5 over {0 <= t <= s <= 1} exactly, and not degree 6.
+    from decimal import Decimal, getcontext
+    from fractions import Fraction
+    getcontext().prec = 60
+    s, t, w = O.rule_table(3)
+    assert len(s) == 7
+    r15 = Decimal(15).sqrt()
+    exp = [(Decimal(2) / 3, Decimal(1) / 3, Decimal(9) / 80)]
+    for a, wt in (((6 - r15) / 21, (155 - r15) / 2400), ((6 + r15) / 21, (155 + r15) / 2400)):
+        c = 1 - 2 * a
+        for lam in ((a, a, c), (a, c, a), (c, a, a)):
+            exp.append((1 - lam[0], lam[2], wt))
+    for q in range(7):
+        assert (s[q], t[q], w[q]) == tuple(float(v) for v in exp[q]), q
+    for deg in range(7):
+        for i in range(deg + 1):
+            j = deg - i
+            exact = Fraction(1, (j + 1) * (i + j + 2))          # int_0^1 int_0^s s^i t^j dt ds
+            got = sum(w[q] * s[q] ** i * t[q] ** j for q in range(7))
+            if deg <= 5:
+                assert abs(got - float(exact)) <= 4e-16, (i, j)
+            elif (i, j) == (0, 6):
+                assert abs(got - float(exact)) > 1e-6
+
+
+@pytest.mark.parametrize("rho,n,tol", [(1.5, 6, 1e-8), (3.0, 5, 1e-8), (6.0, 4, 1e-8), (10.0, 3, 2e-9)])
 def test_regular_rule_vs_semianalytic(O, rho, n, tol):
     T = TRIS["tilted"]
     h = max(np.linalg.norm(T[1] - T[0]), np.linalg.norm(T[2] - T[1]), np.linalg.norm(T[0] - T[2]))
