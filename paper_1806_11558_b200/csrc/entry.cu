@@ -34,12 +34,16 @@ void upload_quadrature_tables() {
     for (int a = 0; a < n; ++a)
       for (int b = 0; b < n; ++b) {
         int q = a * n + b;
-        rs[n - 3][q] = g[a];
-        volatile double t = g[a] * g[b];
-        rt[n - 3][q] = t;
-        volatile double ww = w[a] * w[b];
-        volatile double w3 = ww * g[a];
-        rw[n - 3][q] = w3;
+        if (n == 3) {            // triangles, order 3: Radon's 7-point rule (A14)
+          if (q < 7) { rs[0][q] = kRadon7S[q]; rt[0][q] = kRadon7T[q]; rw[0][q] = kRadon7W[q]; }
+        } else {
+          rs[n - 3][q] = g[a];
+          volatile double t = g[a] * g[b];
+          rt[n - 3][q] = t;
+          volatile double ww = w[a] * w[b];
+          volatile double w3 = ww * g[a];
+          rw[n - 3][q] = w3;
+        }
         qs[n - 3][q] = g[a];              // unit square, tensor (A25)
         qt[n - 3][q] = g[b];
         volatile double wq = w[a] * w[b];

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, int64_t total, Entr
   unsigned long long ev = 0;
   if (cls == 3) {
     m.put(r, map_regular<3>(m, xs, ys));
-    ev = 81;
+    ev = M::kQuad ? 81 : tri_rule_points(3) * tri_rule_points(3);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(mask, ev, o);
@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(128) k_eval_list(M m, const EntryRef* __restri
     map_class(m, s, t, xs, ys);
     m.put(r, map_regular<n>(m, xs, ys));
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(evals, (unsigned long long)(n * n * n * n) * (unsigned long long)c);
+  constexpr int np = M::kQuad ? n * n : tri_rule_points(n);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(evals, (unsigned long long)(np * np) * (unsigned long long)c);
 }
 
 // the rare rest (orders 5, 6 and touching pairs), read from the back of `lists`
@@ -306,7 +307,7 @@ double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t s
   if (W.hcnt[3]) { k_eval_regular<3, M><<<grid_for(W.hcnt[3], 128), 128, 0, st>>>(m, L + base[3], W.hcnt[3]); HM_CHECK_LAUNCH(); }
   if (W.hcnt[0] && !M::kQuad) { k_eval_touching<0, M><<<grid_for(W.hcnt[0], 64), 64, 0, st>>>(m, L + base[0], W.hcnt[0], W.qev.get()); HM_CHECK_LAUNCH(); }
   // (quads: class 0 = touching quads, counted on the device into W.qev, read by the caller)
-  const double per[kNumClass] = {0, 6480, 2592, 81, 256, 625, 1296};
+  const double per[kNumClass] = {0, 6480, 2592, M::kQuad ? 81.0 : 49.0, 256, 625, 1296};
   for (int c = 0; c < kNumClass; ++c) evals += per[c] * (double)W.hcnt[c];
   return evals;
 }

@@ -2,7 +2,7 @@
 // (u~(x) = int_Gamma G(x, y) u_h(y) dsigma_y; the paper's accuracy metric
 // evaluates it inside the domain).  With u_h = sum_j alpha_j phi_j (A2):
 //   u~(x) = (1/4pi) sum_j alpha_j int_{T_j} 1/|x - y| dy,
-// each panel integral by the collapsed Gauss rule of the regular entries (A14) on T_j alone,
+// each panel integral by the triangle rule of the regular entries (A14) on T_j alone,
 // order n from rho^2 = |x - c_j|^2 / h_j^2 in the same bands (reading A23).  Direct sum
 // over all panels (M points x N panels; a few hundred points cost milliseconds), every rank
 // computes all points (collective-free; alpha is replicated).
@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(256) k_potential(const Panel* __restrict__ P, 
       const double* T = c_rt[n - 3];
       const double* W = c_rw[n - 3];
       double inner = 0.0;
-      for (int k = 0; k < n * n; ++k) {
+      const int np = tri_rule_points(n);
+      for (int k = 0; k < np; ++k) {
         const double px = dfma(T[k], e2x, dfma(S[k], e1x, V[0]));
         const double py = dfma(T[k], e2y, dfma(S[k], e1y, V[1]));
         const double pz = dfma(T[k], e2z, dfma(S[k], e1z, V[2]));
