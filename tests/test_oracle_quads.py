@@ -7,6 +7,8 @@ rectangle potential and a graded outer rule (tests/_analytic.py, no triangle spl
 integrals of the paper's quadratic f over squares; the exact interior solution U = f of
 the Dirichlet problem (f harmonic) with the paper's measured convergence rate.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -14,6 +16,9 @@ from inputs.meshes import cube
 from _analytic import square_pair_integral
 
 UNIT_SQUARE = 4.0 * np.log(1.0 + np.sqrt(2.0)) - 4.0 / 3.0 * (np.sqrt(2.0) - 1.0)   # 2.97320959824...
+# the paper's observed interior-error rate on the cube (tests/golden/paper_cube_convergence_rate.txt)
+with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "paper_cube_convergence_rate.txt")) as _f:
+    PAPER_RATE = float(dict(ln.split() for ln in _f if ln.strip() and not ln.startswith("#"))["rate"])
 
 
 def _square(V, q):
@@ -111,4 +116,4 @@ def test_cube_interior_solution_converges_at_the_papers_rate(O):
         err.append(np.abs(P.potential(x, X) - fx).max())
     assert err[2] < 1e-3
     rate = np.log(err[1] / err[2]) / np.log(4.0)                              # per N (N = 6 * 4^L)
-    assert 1.1 <= rate <= 1.6, err
+    assert PAPER_RATE - 0.2 <= rate <= PAPER_RATE + 0.3, err
