@@ -141,7 +141,10 @@ hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double e
  * every block runs to k = min(m, n, option k_max) unless its residual is exactly zero.
  * No communication.  Synchronous.
  * Errors: HM_ERR_STATE (no tree), HM_ERR_ARG (eps_aca < 0 or not finite), HM_ERR_OOM,
- * HM_ERR_NUMERIC (a non-finite entry; message names the block), HM_ERR_CUDA. */
+ * HM_ERR_NUMERIC (a non-finite stored value: the message names the first offending dense
+ * leaf with the entry's internal row and column, or the first admissible leaf with a
+ * non-finite ACA factor entry; every stored near-field entry and factor entry is checked),
+ * HM_ERR_CUDA. */
 hm_status hm_setup(hm_ctx ctx, double eps_aca);
 
 /* y = H x, x and y of length N in application order (host or device pointers).
@@ -153,8 +156,13 @@ hm_status hm_setup(hm_ctx ctx, double eps_aca);
 hm_status hm_matvec(hm_ctx ctx, const double* x, double* y);
 
 /* Solve H sol = rhs with x0 = 0, stopping at ||r||_2 <= tol ||rhs||_2 or after
- * "max_iter" matvecs.  Solver chosen by option "solver".  Vectors replicated on all ranks,
- * one all-reduce per matvec.  COLLECTIVE.  Synchronous.
+ * "max_iter" matvecs.  Solver chosen by option "solver".  With world_size > 1 the Krylov
+ * vectors are sharded by internal row range (rank r owns rows [r S, r S + n), S = ceil(N/p));
+ * each matvec all-gathers x (ncclAllGather) and reduce-scatters the partial products
+ * (ncclReduceScatter) — the volume of the paper's replicated vector + global sum, P:578-587 —
+ * and dot products are all-reduced (ncclAllReduce), so all ranks take identical decisions;
+ * rhs and sol are full-length on every rank (sol is all-gathered at the end).  COLLECTIVE.
+ * Synchronous.
  * iters_out: matvecs performed (may be NULL); rel_residual_out: true relative residual
  * ||rhs - H sol|| / ||rhs|| after the last iteration (may be NULL).
  * Non-convergence within max_iter is NOT an error: HM_OK with *rel_residual_out > tol.
@@ -172,9 +180,10 @@ hm_status hm_assemble_rhs(hm_ctx ctx, int kind, double* f);
 /* Single-layer potential of the density sol at m evaluation points (the paper's
  * accuracy metric evaluates it inside the domain):
  *   out[p] = (1/4pi) sum_j sol_j int_{T_j} 1/|x_p - y| dy,
- * each panel integral by the collapsed Gauss rule of the regular entries on T_j with its
- * order from rho = |x_p - c_j| / h_j in the bands of A14 (reading A23); points must lie off
- * the surface.  Direct sum over all N panels on every rank (collective-free).
+ * each panel integral by the triangle rule of the regular entries on T_j alone (A14: Radon's
+ * 7-point degree-5 rule for order 3, collapsed Gauss n x n for orders 4..6) with its order
+ * from rho = |x_p - c_j| / h_j in the bands of A14 (reading A23); points must lie off the
+ * surface.  Any m >= 0 (point tiles are launched in slices of at most 65535 x 8 points).  Direct sum over all N panels on every rank (collective-free).
  * sol: length N, application order; points: m*3 xyz row-major; out: length m; each host or
  * device.  Synchronous.  Errors: HM_ERR_STATE (no tree), HM_ERR_ARG. */
 hm_status hm_potential(hm_ctx ctx, const double* sol, int64_t m, const double* points, double* out);

@@ -338,6 +338,10 @@ static void free_assembly(or_problem* P) {
   }
 }
 
+/* Release the stored blocks of the last or_assemble (bookkeeping only, no arithmetic):
+ * lets a caller that times or_assemble keep the frees of a previous assembly out of it. */
+void or_release(or_problem* P) { free_assembly(P); }
+
 void or_destroy(or_problem* P) {
   if (!P) return;
   free_assembly(P);

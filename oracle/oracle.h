@@ -93,6 +93,8 @@ int or_aca_matrix(const double* A, int m, int n, double eps, int kcap,
  * Returns 0 on success. */
 int or_assemble(or_problem* P, double eps, int kcap, int64_t d0, int64_t d1,
                 int64_t a0, int64_t a1);
+/* Free the blocks of the last or_assemble (or_assemble itself frees them first). */
+void or_release(or_problem* P);
 int64_t or_stored_doubles(const or_problem* P);                /* dense + factor doubles */
 int or_get_rank(const or_problem* P, int64_t adm_leaf);         /* -1 if not assembled */
 void or_get_factors(const or_problem* P, int64_t adm_leaf, double* U, double* V);

@@ -66,6 +66,7 @@ def lib():
         L.or_assemble.restype = i32
         L.or_assemble.argtypes = [P, d, i32, i64, i64, i64, i64]
         L.or_stored_doubles.restype = i64; L.or_stored_doubles.argtypes = [P]
+        L.or_release.argtypes = [P]
         L.or_get_rank.restype = i32; L.or_get_rank.argtypes = [P, i64]
         L.or_get_factors.argtypes = [P, i64, ptr, ptr]
         L.or_get_pivots.argtypes = [P, i64, ptr]
@@ -221,6 +222,10 @@ class Problem:
         d0, d1 = dense_range if dense_range is not None else (0, nd)
         a0, a1 = adm_range if adm_range is not None else (0, na)
         return lib().or_assemble(self._h, eps, kcap, d0, d1, a0, a1)
+
+    def release(self):
+        """Free the stored blocks (outside any timed region)."""
+        lib().or_release(self._h)
 
     def stored_doubles(self):
         return lib().or_stored_doubles(self._h)

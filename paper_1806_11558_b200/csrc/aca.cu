@@ -45,6 +45,7 @@ struct AcaWork {
   DBuf<int64_t> tot;
   DBuf<int32_t> ovf;
   DBuf<unsigned long long> novf;
+  DBuf<int32_t> bad;    // smallest owned block index with a non-finite factor entry (INT_MAX: none)
   PinnedVec<int64_t> h_tot;
   PinnedVec<AcaBlk> h_blk;
   PinnedVec<int32_t> h_idsp;
@@ -455,13 +456,14 @@ __global__ void k_final_sizes(const AcaBlk* __restrict__ B, const AcaState* __re
   if (st.status == 2) ovf[atomicAdd(novf, 1ull)] = owned[c];
 }
 // pack finished blocks: [U (m x k) | V (n x k)] column-major, straight copies of the
-// first k workspace columns; one CTA per block
+// first k workspace columns; one CTA per block.  The copy also checks every factor entry for
+// finiteness (hm.h: HM_ERR_NUMERIC names the first offending block): bad = min owned index.
 __global__ void __launch_bounds__(256) k_aca_store(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S,
                                                    int64_t nb, const int32_t* __restrict__ owned,
                                                    const int64_t* __restrict__ fpre, int64_t base,
                                                    const double* __restrict__ Uw, const double* __restrict__ Vw,
                                                    double* __restrict__ pool, int64_t* __restrict__ foff,
-                                                   int32_t* __restrict__ frank) {
+                                                   int32_t* __restrict__ frank, int32_t* __restrict__ bad) {
   const int64_t c = blockIdx.x;
   if (c >= nb) return;
   const AcaState st = S[c];
@@ -469,8 +471,10 @@ __global__ void __launch_bounds__(256) k_aca_store(const AcaBlk* __restrict__ B,
   const AcaBlk b = B[c];
   const int64_t o = base + fpre[c];
   const int64_t mu = (int64_t)st.k * b.m, nv = (int64_t)st.k * b.n;
-  for (int64_t x = threadIdx.x; x < mu; x += blockDim.x) pool[o + x] = Uw[b.uoff + x];
-  for (int64_t x = threadIdx.x; x < nv; x += blockDim.x) pool[o + mu + x] = Vw[b.voff + x];
+  bool fin = true;
+  for (int64_t x = threadIdx.x; x < mu; x += blockDim.x) { const double a = Uw[b.uoff + x]; fin &= isfinite(a); pool[o + x] = a; }
+  for (int64_t x = threadIdx.x; x < nv; x += blockDim.x) { const double a = Vw[b.voff + x]; fin &= isfinite(a); pool[o + mu + x] = a; }
+  if (!fin) atomicMin(bad, owned[c]);
   if (threadIdx.x == 0) {
     foff[owned[c]] = o;
     frank[owned[c]] = st.k;
@@ -639,7 +643,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   C.fpool.ensure((base + add) * sizeof(double) + 64);
   C.fpool.used = (base + add) * sizeof(double);
   k_aca_store<<<(unsigned)nb, 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(), base,
-                                           Uw, Vw, (double*)C.fpool.base, C.foff.get(), C.frank.get());
+                                           Uw, Vw, (double*)C.fpool.base, C.foff.get(), C.frank.get(), W.bad.get());
   HM_CHECK_LAUNCH();
   if (nov) {
     const size_t o0 = overflow.size();
@@ -702,6 +706,11 @@ void setup_aca(Context& C) {
   AcaWork& W = *C.aca_ws;
   W.ev.alloc(1);
   HM_CUDA(cudaMemsetAsync(W.ev.get(), 0, sizeof(unsigned long long), st));
+  W.bad.alloc(1);
+  {
+    const int32_t none = INT_MAX;
+    HM_CUDA(cudaMemcpyAsync(W.bad.get(), &none, sizeof(none), cudaMemcpyHostToDevice, st));
+  }
   const bool rec = C.record_pivots == 1 || (C.record_pivots < 0 && C.N <= 25000);
   auto& pivots = C.h_piv;
   pivots.clear();
@@ -814,8 +823,17 @@ void setup_aca(Context& C) {
   HM_CUDA(cudaMemcpyAsync(C.h_foff.data(), C.foff.get(), nb * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
   unsigned long long hev = 0;
+  int32_t hbad = INT_MAX;
   HM_CUDA(cudaMemcpyAsync(&hev, W.ev.get(), sizeof(hev), cudaMemcpyDeviceToHost, st));
+  HM_CUDA(cudaMemcpyAsync(&hbad, W.bad.get(), sizeof(hbad), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
+  if (hbad != INT_MAX) {
+    const Quad& q = C.h_adm[C.adm_begin + hbad];
+    fail(HM_ERR_NUMERIC, "hm_setup: non-finite ACA factor entry in admissible leaf " +
+                             std::to_string(C.adm_begin + hbad) + " (rows [" + std::to_string(q.rlo) + "," +
+                             std::to_string(q.rhi) + ") x cols [" + std::to_string(q.clo) + "," +
+                             std::to_string(q.chi) + "), internal order)");
+  }
   C.evals_aca = (double)hev;
   C.factor_doubles = (int64_t)(C.fpool.used / sizeof(double));
   C.aca_prev_valid = true;

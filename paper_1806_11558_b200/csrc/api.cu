@@ -470,6 +470,11 @@ hm_status hm_setup(hm_ctx ctx, double eps_aca) {
     C.have_setup = false;
     C.eps_aca = eps_aca;
     Timer all(C);
+    struct JoinPlanner {   // on any failure below: no planner thread outlives this call
+      Context& c;
+      bool armed = true;
+      ~JoinPlanner() { if (armed) hm::plan_dense_abort(c); }
+    } join_planner{C};
     hm::near_prepare(C);
     hm::plan_dense_begin(C);
     if (C.setup_overlap && C.dense_doubles > 0) {
@@ -490,6 +495,7 @@ hm_status hm_setup(hm_ctx ctx, double eps_aca) {
       hm::plan_matvec(C);
       C.times.plan_ms = t.ms();
     }
+    join_planner.armed = false;
     C.times.setup_ms = all.ms();
     C.kt.resolve();
     C.have_setup = true;

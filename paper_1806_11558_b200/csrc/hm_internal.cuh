@@ -347,6 +347,7 @@ void near_check(Context& C);                                   // non-finite che
 // aca.cu
 void setup_aca(Context& C);
 // matvec.cu
+void plan_dense_abort(Context& C);   // join a still-running dense planner (error path / tree rebuild)
 void plan_dense_begin(Context& C);   // dense half of the plan on host threads (overlaps ACA)
 void plan_matvec(Context& C);
 void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce = true);   // y = H x (local

@@ -622,6 +622,17 @@ void plan_dense_begin(Context& C) {
   });
 }
 
+// Join a dense planner thread that is still running (hm_setup failed between
+// plan_dense_begin and plan_matvec, or the tree is being rebuilt): it reads h_dense,
+// dense_begin and the offsets, which hm_build_tree is about to rewrite.
+void plan_dense_abort(Context& C) {
+  if (!C.plan_ws) return;
+  PlanWs& W = *C.plan_ws;
+  if (W.dense_thread.joinable()) W.dense_thread.join();
+  W.dense_started = false;
+  W.dense_err = nullptr;
+}
+
 // The matvec plan, built on the host by threads over contiguous slices of the item sequence
 // (owned dense leaves in list order — planned during ACA by plan_dense_begin — then owned
 // low-rank leaves in block order); batches never straddle two slices.

@@ -49,9 +49,10 @@ struct NearMap {
   __device__ void put(EntryRef r, double a) const { store[off[r.seg] + r.idx] = a; }
 };
 
+// bad[0] = number of non-finite entries, bad[1] = smallest offset of one (if any)
 __global__ void k_check_finite(const double* __restrict__ a, int64_t n, unsigned long long* bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    if (!isfinite(a[i])) atomicAdd(bad, 1ull);
+    if (!isfinite(a[i])) { atomicAdd(bad, 1ull); atomicMin(bad + 1, (unsigned long long)i); }
 }
 
 }  // namespace
@@ -141,14 +142,24 @@ void near_check(Context& C) {
   const int64_t total = C.dense_doubles;
   if (total == 0) return;
   DBuf<unsigned long long> bad;
-  bad.alloc(1);
-  HM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), st));
+  bad.alloc(2);
+  unsigned long long hb[2] = {0ull, ~0ull};
+  HM_CUDA(cudaMemcpyAsync(bad.get(), hb, sizeof(hb), cudaMemcpyHostToDevice, st));
   k_check_finite<<<148 * 4, 256, 0, st>>>(C.dstore.get(), total, bad.get());
   HM_CHECK_LAUNCH();
-  unsigned long long hb = 0;
-  HM_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, st));
+  HM_CUDA(cudaMemcpyAsync(hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
-  if (hb) fail(HM_ERR_NUMERIC, "hm_setup: " + std::to_string(hb) + " non-finite near-field entries");
+  if (hb[0]) {
+    // name the first offending entry: owned dense leaf (offsets near_hoff), local row and column
+    const std::vector<int64_t>& hoff = C.near_hoff;
+    const int64_t e = (int64_t)hb[1];
+    const int64_t b = std::upper_bound(hoff.begin(), hoff.end(), e) - hoff.begin() - 1;
+    const Quad& q = C.h_dense[C.dense_begin + b];
+    const int64_t n = q.chi - q.clo, r = (e - hoff[b]) / n, c = (e - hoff[b]) % n;
+    fail(HM_ERR_NUMERIC, "hm_setup: " + std::to_string(hb[0]) + " non-finite near-field entries; first in dense leaf " +
+                             std::to_string(C.dense_begin + b) + " at internal (row, col) = (" +
+                             std::to_string(q.rlo + r) + ", " + std::to_string(q.clo + c) + ")");
+  }
 }
 
 }  // namespace hm

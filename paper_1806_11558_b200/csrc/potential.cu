@@ -10,6 +10,8 @@
 // Grid: (panel tiles of 256) x (point tiles of kPts).  A thread owns one panel and keeps the
 // kPts points' sums in registers; the CTA reduces them through shared memory and adds one
 // FP64 atomic per point.
+#include <algorithm>
+
 #include "entry.cuh"
 
 namespace hm {
@@ -94,9 +96,15 @@ void potential(Context& C, const double* alpha_app, int64_t M, const double* X_d
   gather_perm(C, alpha_app, C.xin.get());
   HM_CUDA(cudaMemsetAsync(out_dev, 0, M * sizeof(double), st));
   if (M == 0) return;
-  const dim3 grid(grid_for(C.npanel, 256), (unsigned)((M + kPts - 1) / kPts));
-  k_potential<<<grid, 256, 0, st>>>(C.panel.get(), C.xin.get(), C.npanel, C.quad ? 1 : 0, X_dev, M, out_dev);
-  HM_CHECK_LAUNCH();
+  // point tiles on grid.y, at most 65535 per launch (gridDim.y limit): launches over point slices
+  constexpr int64_t kMaxTilesY = 65535;
+  for (int64_t p0 = 0; p0 < M; p0 += kMaxTilesY * kPts) {
+    const int64_t m = std::min<int64_t>(M - p0, kMaxTilesY * kPts);
+    const dim3 grid(grid_for(C.npanel, 256), (unsigned)((m + kPts - 1) / kPts));
+    k_potential<<<grid, 256, 0, st>>>(C.panel.get(), C.xin.get(), C.npanel, C.quad ? 1 : 0, X_dev + 3 * p0, m,
+                                      out_dev + p0);
+    HM_CHECK_LAUNCH();
+  }
   k_scale_inplace<<<grid_for(M, 256), 256, 0, st>>>(out_dev, M, kInv4Pi);
   HM_CHECK_LAUNCH();
 }

@@ -1,9 +1,12 @@
 // solver.cu — Krylov solvers driving the batched H-matvec (A17):
 //   CG (the paper's solver) and GMRES(m) with classical Gram-Schmidt + one
 //   re-orthogonalisation (CGS2) and Givens rotations (BASELINE.json's solver).
-// Vectors live in internal (Morton) order on the device and are replicated on every rank
-// (P:578-582); the only collective per iteration is the all-reduce inside the matvec.
-// Reductions use a fixed grid and a fixed tree, so every rank computes bit-identical
+// Vectors live in internal (Morton) order on the device.  One rank: full vectors.  p ranks:
+// every Krylov vector is sharded by internal row range (rank r owns [r S, r S + n), S =
+// ceil(N / p)); each matvec all-gathers x (ncclAllGather), applies the rank's leaves and
+// reduce-scatters the partial y into the slices (ncclReduceScatter) — the volume of the
+// paper's replicated vector + global sum; dot products are local fixed-grid tree
+// reductions followed by an ncclAllReduce of the partials, so every rank sees bit-identical
 // scalars and takes identical convergence decisions.  x0 = 0; stop at ||r|| <= tol ||b||.
 #include <cub/cub.cuh>
 

@@ -400,6 +400,7 @@ void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_
 }  // namespace
 
 void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
+  plan_dense_abort(C);   // a planner thread of a failed hm_setup must not see the new tree
   cudaStream_t st = C.stream;
   cudaEvent_t ev[7];
   for (auto& e : ev) HM_CUDA(cudaEventCreate(&e));

@@ -1,0 +1,141 @@
+"""GPU-vs-oracle parity at the sizes and in the launch configuration the bench runs.
+
+The small-mesh parity tests (test_gpu_parity.py) only reach blocks with m + n <= 640; the
+benchmarked configs run other code paths: CTA-per-block pivot / Frobenius-update kernels for
+blocks with m + n >= 2048 (C3 has 20,606 of them), overflow re-runs with a doubled
+workspace, the large-block matvec kernels, and solves whose conditioning grows like 1/h.
+Bars:
+  - ACA: identical rank and pivot sequence on >= 99.9% of blocks (A12/A15 make the residuals
+    bit-identical); factors of those blocks equal to 1e-12 relative;
+  - H-matvec: ||Hx - Ax|| <= 10 eps_aca ||Ax|| on sampled exact Galerkin rows (A21);
+  - solution: ||a_gpu - a_oracle|| <= 1e-5 ||a_oracle||, both GMRES(100) at tol 1e-10 (A17).
+"""
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from inputs.meshes import geodesic, icosphere, seeded_vector
+
+pytestmark = pytest.mark.gpu
+
+EPS = 1e-6
+THREADS = max(1, len(os.sched_getaffinity(0)))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return torch
+
+
+def _gpu(V, T, **opts):
+    from paper_1806_11558_b200 import HMatrix
+    H = HMatrix(device=0)
+    for k, v in opts.items():
+        H.set_option(k, v)
+    H.build_tree(V, T)
+    return H
+
+
+def test_c3_big_block_aca_pivots(O, torch_cuda):
+    """configs[2] (icosphere L=7, N = 327,680): every admissible block with m + n >= 2048 —
+    the blocks that k_aca_pivot_big / k_aca_update_big process — against the oracle's
+    one-block-at-a-time ACA (or_aca_block, P:318-321 with A11/A12): rank and pivots
+    identical on >= 99.9% of blocks, factors equal to 1e-12 where they are."""
+    V, T = icosphere(7)
+    H = _gpu(V, T, record_pivots=1)
+    H.setup(EPS)
+    R = O.Problem(V, T)
+    adm, _ = H.leaves(0)
+    assert np.array_equal(adm, R.leaves(0))
+    m = adm[:, 1] - adm[:, 0]
+    n = adm[:, 3] - adm[:, 2]
+    big = np.nonzero(m + n >= 2048)[0]
+    assert big.size > 20000                      # 20,606 at C3 with C_leaf = 32, eta = 1
+    R.aca_block(adm[big[0]], EPS, 64)             # initialises the oracle's rule tables once
+    same = 0
+    worst = 0.0
+    window = 4 * THREADS
+    with ThreadPoolExecutor(THREADS) as ex:       # ctypes releases the GIL during or_aca_block
+        fut = {}
+        for i, b in enumerate(big[:window]):
+            fut[i] = ex.submit(R.aca_block, adm[b], EPS, 64)
+        for i, b in enumerate(big):
+            if i + window < big.size:
+                fut[i + window] = ex.submit(R.aca_block, adm[big[i + window]], EPS, 64)
+            Uo, Wo, pvo = fut.pop(i).result()
+            Ug, Wg, pvg = H.lowrank(int(b), int(m[b]), int(n[b]), pivots=True)
+            if Ug.shape[1] == Uo.shape[1] and np.array_equal(pvg, pvo):
+                same += 1
+                su = max(np.abs(Uo).max(), 1e-300)
+                sv = max(np.abs(Wo).max(), 1e-300)
+                worst = max(worst, np.abs(Ug - Uo).max() / su, np.abs(Wg - Wo).max() / sv)
+    H.close()
+    assert same >= 0.999 * big.size, f"identical rank and pivots on {same}/{big.size} big blocks"
+    assert worst <= 1e-12, f"factor difference {worst:.3e} on blocks with identical pivots"
+
+
+def test_c2_overflow_rerun_bit_identical(O, torch_cuda):
+    """Overflow path: with a 4-column first workspace nearly every block of
+    configs[1] fills it and is re-run from scratch with 8, 16 ... columns.  ACA is
+    deterministic, so every factor must be bit-identical to the default 16-column run."""
+    V, T = icosphere(5)
+    H0 = _gpu(V, T)
+    H0.setup(EPS)
+    H1 = _gpu(V, T, aca_kws=4)
+    H1.setup(EPS)
+    assert H1.stats()["aca_overflow"] > 1000
+    adm, _ = H0.leaves(0)
+    ranks = []
+    for b, q in enumerate(adm):
+        mm, nn = q[1] - q[0], q[3] - q[2]
+        U0, W0 = H0.lowrank(b, mm, nn)
+        U1, W1 = H1.lowrank(b, mm, nn)
+        assert np.array_equal(U0, U1) and np.array_equal(W0, W1), f"block {b}"
+        ranks.append(U0.shape[1])
+    assert max(ranks) > 8          # re-runs reached the third workspace size (4 -> 8 -> 16)
+    H0.close(); H1.close()
+
+
+def test_c4_matvec_sampled_exact_rows(O, torch_cuda):
+    """configs[3] (geodesic nu = 280, N = 1,568,000 — the bench workload, default options):
+    ||(Hx)_R - (Ax)_R|| <= 10 eps_aca ||(Ax)_R|| on 128 seeded exact Galerkin rows R
+    (or_dense_rows) for x = 1, the paper's f and a seeded N(0,1) vector."""
+    import torch
+    V, T = geodesic(280)
+    N = T.shape[0]
+    H = _gpu(V, T)
+    H.setup(EPS)
+    R = O.Problem(V, T)
+    rows = np.random.default_rng(7).permutation(N)[:128]
+    Arows = R.dense_rows(rows)
+    fbar = H.assemble_rhs(1)
+    for x in (np.ones(N), fbar, seeded_vector(N, 0)):
+        yg = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        ye = Arows @ x
+        err = np.linalg.norm(yg[rows] - ye) / np.linalg.norm(ye)
+        assert err <= 10 * EPS, err
+    H.close()
+
+
+def test_nu64_solution_vs_oracle(O, torch_cuda):
+    """Geodesic sphere nu = 64 (N = 81,920, 4x configs[1]): the GPU GMRES(100) solution of the
+    paper's right-hand side against the oracle's full H path (assembly + GMRES(100)),
+    both at tol 1e-10: ||a_gpu - a_oracle|| <= 1e-5 ||a_oracle|| (BASELINE.json)."""
+    import torch
+    V, T = geodesic(64)
+    H = _gpu(V, T)
+    H.setup(EPS)
+    R = O.Problem(V, T)
+    R.assemble(EPS)
+    f = R.rhs(1)
+    assert np.abs(H.assemble_rhs(1) - f).max() <= 1e-15 * np.abs(f).max()
+    sol, it, rr = H.solve(torch.from_numpy(f).cuda(), tol=1e-10)
+    xo, ito, rro, st = R.gmres(f, tol=1e-10, restart=100)
+    assert st == 0 and rro <= 1e-9 and rr <= 1e-9
+    d = np.linalg.norm(sol.cpu().numpy() - xo) / np.linalg.norm(xo)
+    assert d <= 1e-5, d
+    H.close()

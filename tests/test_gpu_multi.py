@@ -29,7 +29,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C1odd"])   # C1odd: N = 1279, N mod p != 0
 def test_two_rank_matvec_and_solve(cfg):
     if _ngpus() < 2:
         pytest.skip("needs >= 2 GPUs")

@@ -124,7 +124,9 @@ def test_cube_interior_error_rate_on_gpu(torch_cuda):
         err.append(np.abs(u - fx).max())
         H.close()
     rates = [np.log(err[k] / err[k + 1]) / np.log(4.0) for k in range(3)]
-    assert all(1.0 <= r <= 1.7 for r in rates), (err, rates)
+    # the oracle pin's band around the paper's 1.3 (tests/golden/paper_cube_convergence_rate.txt)
+    from test_oracle_quads import PAPER_RATE
+    assert all(PAPER_RATE - 0.2 <= r <= PAPER_RATE + 0.3 for r in rates), (err, rates)
 
 
 def test_cube_full_size_sampled_rows(O, torch_cuda):
@@ -134,7 +136,7 @@ def test_cube_full_size_sampled_rows(O, torch_cuda):
     H = _gpu(V, Q)
     H.setup(EPS)
     R = O.Problem(V, Q)
-    rows = np.random.default_rng(7).permutation(N)[:6]
+    rows = np.random.default_rng(7).permutation(N)[:128]
     Arows = R.dense_rows(rows)
     for x in [np.ones(N), seeded_vector(N, 0)]:
         yg = H.matvec(torch_cuda.from_numpy(x).cuda()).cpu().numpy()

@@ -36,6 +36,22 @@ def test_morton_axis_order(O):
     assert int(c[2]) == 1 << 61 and int(c[3]) == 1 << 60 and int(c[4]) == 1 << 59
 
 
+def test_morton_per_axis_normalisation(O):
+    # A6: every axis is normalised to its OWN extent of the centroid box, here
+    # [0,2] x [0,1] x [0,4]; codes computed by hand from q_a = floor(((c-lo)/(hi-lo)) 2^21) and
+    # bit b of q_x, q_y, q_z at 3b+2, 3b+1, 3b.  An isotropic normalisation (by the largest
+    # extent 4) would give (1,0,0) -> 1<<59 and (0,0.5,0) -> 1<<55 instead.
+    V, T = _point_mesh([[0, 0, 0], [2, 1, 4], [1, 0, 0], [0, 0.5, 0], [0, 0, 1],
+                        [0.5, 0.25, 3], [1.5, 0.75, 0.5]])
+    c = [int(v) for v in O.Problem(V, T).codes()]
+    assert c[0] == 0 and c[1] == (1 << 63) - 1
+    assert c[2] == 1 << 62                                   # x: 1/2 -> q = 2^20
+    assert c[3] == 1 << 61                                   # y: 1/2 -> q = 2^20
+    assert c[4] == 1 << 57                                   # z: 1/4 -> q = 2^19
+    assert c[5] == (1 << 59) | (1 << 58) | (1 << 60) | (1 << 57)     # x 1/4, y 1/4, z 3/4
+    assert c[6] == (1 << 62) | (1 << 59) | (1 << 61) | (1 << 58) | (1 << 54)   # x 3/4, y 3/4, z 1/8
+
+
 def test_cbc_spec_examples(O):
     # 5 identical points, C_leaf = 32 -> single leaf
     V, T = _point_mesh([[0.25, 0.25, 0.25]] * 5)

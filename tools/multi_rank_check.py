@@ -32,7 +32,13 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     obj = [hm.hm_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    V, T = config_mesh(cfg)
+    if cfg.endswith("odd"):
+        # an open surface with an odd panel count (the closed meshes all have even N): the
+        # last rank's Krylov slice is shorter than the others (n < S = ceil(N / p))
+        V, T = config_mesh(cfg[:-3])
+        T = T[:-1].copy()
+    else:
+        V, T = config_mesh(cfg)
     N = T.shape[0]
     H = HMatrix(device=local, rank=rank, world_size=world, nccl_unique_id=obj[0])
     H.build_tree(V, T)
