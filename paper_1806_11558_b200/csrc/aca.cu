@@ -52,6 +52,9 @@ struct AcaWork {
   std::vector<AcaState> h_state;
   std::vector<int32_t> h_ids, h_big;
   DBuf<EntryRef> lists;
+  PinnedVec<int64_t> h_ring;          // per-step totals read back kLag steps late
+  cudaEvent_t ring_ev[3] = {nullptr, nullptr, nullptr};
+  ~AcaWork() { for (auto& e : ring_ev) if (e) cudaEventDestroy(e); }
 };
 
 namespace {
@@ -175,12 +178,8 @@ __device__ int first_unused(const uint32_t* bm, int m, int lane) {
 // blocks with m + n >= kBigMN get a CTA (not a warp) in the pivot and update kernels
 constexpr int kBigMN = 2048;
 
-__global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, const int32_t* __restrict__ act,
-                            int64_t nact, double* __restrict__ Vw, uint32_t* __restrict__ bmap) {
-  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (a >= nact) return;
-  const int64_t c = act[a];
+__device__ __forceinline__ void aca_pivot_block(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, int64_t c,
+                                                double* __restrict__ Vw, uint32_t* __restrict__ bmap, int lane) {
   AcaState st = S[c];
   if (st.status != 0) return;
   const AcaBlk b = B[c];
@@ -220,6 +219,17 @@ __global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__
     st.skip = 0;
     S[c] = st;
   }
+}
+
+
+// one warp per active block, persistent over the step's active count *dnact (device)
+__global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, const int32_t* __restrict__ act,
+                            const int64_t* __restrict__ dnact, double* __restrict__ Vw, uint32_t* __restrict__ bmap) {
+  const int64_t nact = *dnact;
+  const int lane = threadIdx.x & 31;
+  for (int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; a < nact;
+       a += ((int64_t)gridDim.x * blockDim.x) >> 5)
+    aca_pivot_block(B, S, act[a], Vw, bmap, lane);
 }
 
 // k_aca_pivot for the big blocks of the chunk (m + n >= kBigMN): one CTA per block
@@ -403,22 +413,25 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
   }
 }
 
-// G = 1: one warp per active block (small blocks; big ones are skipped), act[] = compact list
+// G = 1: one warp per active block (small blocks; big ones are skipped), act[] = compact list;
+// persistent over the step's active count *dnact (device)
 __global__ void __launch_bounds__(64, 16) k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
-                                                    const int32_t* __restrict__ act, int64_t nact,
+                                                    const int32_t* __restrict__ act, const int64_t* __restrict__ dnact,
                                                     const double* __restrict__ Uw, const double* __restrict__ Vw,
                                                     const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv,
                                                     int kws, double eps) {
-  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nact = *dnact;
   const int lane = threadIdx.x & 31;
-  if (a >= nact) return;
-  const int64_t c = act[a];
-  AcaState st = S[c];
-  const AcaBlk b = B[c];
-  if (st.status != 0 || st.skip) return;
-  if (b.m + b.n >= kBigMN) return;
-  aca_update_block<1>(b, st, Uw, Vw, bmap, piv, c, kws, eps, 0, lane, nullptr);
-  if (lane == 0) S[c] = st;
+  for (int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; a < nact;
+       a += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t c = act[a];
+    AcaState st = S[c];
+    const AcaBlk b = B[c];
+    if (st.status != 0 || st.skip) continue;
+    if (b.m + b.n >= kBigMN) continue;
+    aca_update_block<1>(b, st, Uw, Vw, bmap, piv, c, kws, eps, 0, lane, nullptr);
+    if (lane == 0) S[c] = st;
+  }
 }
 
 // G = 8: one CTA per big block of the chunk (list fixed per chunk; finished blocks return)
@@ -491,20 +504,21 @@ void cub_call(DBuf<char>& tmp, F&& f) {
 
 
 
-// one batch of residual entries: order-3 in place, then the order-4 list, then the rest
+// one batch of residual entries (row or column step): order-3 in place, then the order-4
+// list, then the rest; the batch size *dtot lives on the device, `upper` bounds it (grid size)
 template <class M>
-void aca_eval(Context& C, const M& m, int64_t total, AcaWork& W) {
-  if (total <= 0) return;
+void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWork& W) {
+  if (upper <= 0) return;
   cudaStream_t st = C.stream;
-  W.cnt.alloc(2);
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 2 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
-  k_eval_class3<M><<<grid_for(total, 128), 128, 0, st>>>(m, total, W.lists.get(), W.cnt.get(), W.ev.get());
+  const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4 * 2);
+  k_eval_class3<M><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
-  const unsigned g = (unsigned)std::min<int64_t>(grid_for(total, 128), 148 * 16);
-  k_eval_list<4, M><<<g, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
+  const unsigned g4 = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 16);
+  k_eval_list<4, M><<<g4, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
-  k_eval_rest<M><<<std::min<unsigned>(g, 148 * 4), 128, 0, st>>>(m, W.lists.get(), total, W.cnt.get(), W.ev.get());
+  k_eval_rest<M><<<std::min<unsigned>(g4, 148 * 4), 128, 0, st>>>(m, W.lists.get(), dtot, W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
 }
 
@@ -521,7 +535,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   hb.resize(nb);
   std::vector<int32_t>& hbig = W.h_big;
   hbig.clear();
-  int64_t uo = 0, vo = 0, bo = 0;
+  int64_t uo = 0, vo = 0, bo = 0, rmax = 0, cmax = 0;   // rmax / cmax: entries of the first row / column step
   for (int64_t c = 0; c < nb; ++c) {
     const Quad& q = C.h_adm[C.adm_begin + ids[c]];
     AcaBlk& b = hb[c];
@@ -534,6 +548,8 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     uo += (int64_t)b.m * kws;
     vo += (int64_t)b.n * kws;
     bo += (b.m + 31) / 32;
+    rmax += b.n;
+    cmax += b.m;
     if (b.m + b.n >= kBigMN) hbig.push_back((int32_t)c);
   }
   const int64_t nbig = (int64_t)hbig.size();
@@ -557,6 +573,24 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   const int4* QV = C.qv.get();
   C.times.aca_phase_ms[0] += ms_since(t0);
   const auto t1 = clk::now();
+  // Host-sync-free step loop: every kernel of a step reads the step's sizes (active blocks,
+  // row / column entry totals) from device memory, so the host enqueues step after step and
+  // only reads each step's totals back kLag steps later (pinned ring + events) to learn when
+  // the chunk is done; the at most kLag steps enqueued past the last active one find no active
+  // block and return at once.
+  constexpr int kLag = 2;
+  W.lists.alloc(std::max(rmax, cmax));
+  W.rtab.alloc(rmax / 32 + 2);
+  W.ctab.alloc(cmax / 32 + 2);
+  W.cnt.alloc(2);
+  W.h_ring.resize(3 * (kLag + 1));
+  for (auto& e : W.ring_ev)
+    if (!e) HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const int64_t* drow = W.tot.get();          // tot[0]: row entries, tot[1]: column entries, tot[2]: active blocks
+  const int64_t* dcol = W.tot.get() + 1;
+  const int64_t* dnact = W.tot.get() + 2;
+  const unsigned gpiv = (unsigned)std::min<int64_t>(grid_for(nb * 32, 256), 148 * 8);
+  const unsigned gupd = (unsigned)std::min<int64_t>(grid_for(nb * 32, 64), 148 * 16);
   for (int step = 0;; ++step) {
     std::unique_ptr<KScope> ks(new KScope(C, KF_ACA_OTHER));
     k_step_flags<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.state.get(), nb, W.flag.get());
@@ -575,32 +609,23 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     });
     k_step_totals<<<1, 1, 0, st>>>(W.rpre.get(), W.cpre.get(), W.pos.get(), nb, W.tot.get());
     HM_CHECK_LAUNCH();
-    int64_t tot[3];
-    HM_CUDA(cudaMemcpyAsync(tot, W.tot.get(), sizeof(tot), cudaMemcpyDeviceToHost, st));
+    const int slot = step % (kLag + 1);
+    HM_CUDA(cudaMemcpyAsync(W.h_ring.data() + 3 * slot, W.tot.get(), 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HM_CUDA(cudaEventRecord(W.ring_ev[slot], st));
+    // segment tables over all nb slots: slots past the active count have empty ranges
+    k_seg_table<<<grid_for(nb, 256), 256, 0, st>>>(W.rpre.get(), nb, 0, W.rtab.get());
+    HM_CHECK_LAUNCH();
+    k_seg_table<<<grid_for(nb, 256), 256, 0, st>>>(W.cpre.get(), nb, 0, W.ctab.get());
+    HM_CHECK_LAUNCH();
     ks.reset();
-    const auto ts = clk::now();
-    HM_CUDA(cudaStreamSynchronize(st));
-    C.times.aca_phase_ms[2] += ms_since(ts);
-    if (tot[0] == 0) break;
-    const int64_t nact = tot[2];
-    C.aca_steps++;
-    C.entries_aca += (double)(tot[0] + tot[1]);
-    W.lists.alloc(std::max(tot[0], tot[1]));
-    W.rtab.alloc(tot[0] / 32 + 2);
-    W.ctab.alloc(tot[1] / 32 + 2);
-    k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.rpre.get(), nact, 0, W.rtab.get());
-    HM_CHECK_LAUNCH();
-    k_seg_table<<<grid_for(nact, 256), 256, 0, st>>>(W.cpre.get(), nact, 0, W.ctab.get());
-    HM_CHECK_LAUNCH();
     if (C.quad)
       aca_eval(C, AcaMap<true, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(),
-                                     nb, Uw, Vw}, tot[0], W);
+                                     nb, Uw, Vw}, drow, rmax, W);
     else
       aca_eval(C, AcaMap<true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
-                               W.rtab.get(), nb, Uw, Vw}, tot[0], W);
+                               W.rtab.get(), nb, Uw, Vw}, drow, rmax, W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_pivot<<<grid_for(nact * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, Vw,
-                                                          W.bmap.get());
+    k_aca_pivot<<<gpiv, 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Vw, W.bmap.get());
     HM_CHECK_LAUNCH();
     if (nbig) {
       k_aca_pivot_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Vw, W.bmap.get());
@@ -609,18 +634,30 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     ks.reset();
     if (C.quad)
       aca_eval(C, AcaMap<false, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(),
-                                      nb, Uw, Vw}, tot[1], W);
+                                      nb, Uw, Vw}, dcol, cmax, W);
     else
       aca_eval(C, AcaMap<false>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(),
-                                W.ctab.get(), nb, Uw, Vw}, tot[1], W);
+                                W.ctab.get(), nb, Uw, Vw}, dcol, cmax, W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_update<<<grid_for(nact * 32, 64), 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), nact, Uw,
-                                                           Vw, W.bmap.get(), W.piv.get(), kws, C.eps_aca);
+    k_aca_update<<<gupd, 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Uw, Vw, W.bmap.get(),
+                                      W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();
     if (nbig) {
       k_aca_update_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Uw, Vw,
                                                        W.bmap.get(), W.piv.get(), kws, C.eps_aca);
       HM_CHECK_LAUNCH();
+    }
+    ks.reset();
+    // read back the totals of step - kLag (all earlier ones were read already)
+    if (step >= kLag) {
+      const int rs = (step - kLag) % (kLag + 1);
+      const auto ts = clk::now();
+      HM_CUDA(cudaEventSynchronize(W.ring_ev[rs]));
+      C.times.aca_phase_ms[2] += ms_since(ts);
+      const int64_t* t = W.h_ring.data() + 3 * rs;
+      if (t[0] == 0) break;        // no active block since step - kLag: the later steps were no-ops
+      C.aca_steps++;
+      C.entries_aca += (double)(t[0] + t[1]);
     }
   }
   C.times.aca_phase_ms[1] += ms_since(t1);

@@ -157,44 +157,49 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
 }
 
 // Three-kernel, host-sync-free variant for ACA rows / columns (nearly all entries are order 3,
-// most of the rest order 4):
-//   k_eval_class3   evaluates the order-3 entries in place (others exit at once) and appends
-//                   order-4 references to the front of `lists`, all other classes to the back;
+// most of the rest order 4).  The batch size is read on the device (*dtot: the step's row or
+// column total, written by the step's scans), so the host never waits for it:
+//   k_eval_class3   persistent grid-stride pass over the batch: evaluates the order-3 entries
+//                   in place and appends order-4 references to the front of `lists`, all other
+//                   classes to the back (warp-aggregated atomics);
 //   k_eval_list<4>  persistent grid-stride over the order-4 list (count read on the device);
-//   k_eval_rest     persistent, in-CTA class sort of the remaining few.
+//   k_eval_rest     persistent, the remaining few (orders 5, 6, touching pairs).
 template <class M>
-__global__ void __launch_bounds__(128, 4) k_eval_class3(M m, int64_t total, EntryRef* __restrict__ lists,
+__global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __restrict__ dtot,
+                                                     EntryRef* __restrict__ lists,
                                                      unsigned long long* __restrict__ cnt /* [n4, nrest] */,
                                                      unsigned long long* __restrict__ evals) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  EntryRef r;
-  int cls = -1, xs = 0, ys = 0;
-  if (m.locate(e, e < total, r)) {
-    int s, t;
-    m.pair(r, s, t);
-    cls = map_class(m, s, t, xs, ys);
-  }
-  const unsigned mask = __activemask();
+  const int64_t total = *dtot;
   const int lane = threadIdx.x & 31;
-  // warp-aggregated appends: order 4 at the front, everything else (not 3) at the back
-  const unsigned b4 = __ballot_sync(mask, cls == 4), br = __ballot_sync(mask, cls >= 0 && cls != 3 && cls != 4);
-  unsigned long long base4 = 0, baser = 0;
-  if (lane == 0) {
-    if (b4) base4 = atomicAdd(&cnt[0], (unsigned long long)__popc(b4));
-    if (br) baser = atomicAdd(&cnt[1], (unsigned long long)__popc(br));
-  }
-  base4 = __shfl_sync(mask, base4, 0);
-  baser = __shfl_sync(mask, baser, 0);
   const unsigned below = (1u << lane) - 1u;
-  if (cls == 4) lists[base4 + __popc(b4 & below)] = r;
-  else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
   unsigned long long ev = 0;
-  if (cls == 3) {
-    m.put(r, map_regular<3>(m, xs, ys));
-    ev = M::kQuad ? 81 : tri_rule_points(3) * tri_rule_points(3);
+  // the loop bound is uniform per CTA, so every warp runs whole iterations (full-mask ballots)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = base + threadIdx.x;
+    EntryRef r;
+    int cls = -1, xs = 0, ys = 0;
+    if (m.locate(e, e < total, r)) {
+      int s, t;
+      m.pair(r, s, t);
+      cls = map_class(m, s, t, xs, ys);
+    }
+    const unsigned b4 = __ballot_sync(0xffffffffu, cls == 4), br = __ballot_sync(0xffffffffu, cls >= 0 && cls != 3 && cls != 4);
+    unsigned long long base4 = 0, baser = 0;
+    if (lane == 0) {
+      if (b4) base4 = atomicAdd(&cnt[0], (unsigned long long)__popc(b4));
+      if (br) baser = atomicAdd(&cnt[1], (unsigned long long)__popc(br));
+    }
+    base4 = __shfl_sync(0xffffffffu, base4, 0);
+    baser = __shfl_sync(0xffffffffu, baser, 0);
+    if (cls == 4) lists[base4 + __popc(b4 & below)] = r;
+    else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
+    if (cls == 3) {
+      m.put(r, map_regular<3>(m, xs, ys));
+      ev += M::kQuad ? 81 : tri_rule_points(3) * tri_rule_points(3);
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(mask, ev, o);
+  for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
   if (lane == 0 && ev) atomicAdd(evals, ev);
 }
 
@@ -216,9 +221,11 @@ __global__ void __launch_bounds__(128) k_eval_list(M m, const EntryRef* __restri
 
 // the rare rest (orders 5, 6 and touching pairs), read from the back of `lists`
 template <class M>
-__global__ void __launch_bounds__(128) k_eval_rest(M m, const EntryRef* __restrict__ lists, int64_t total,
+__global__ void __launch_bounds__(128) k_eval_rest(M m, const EntryRef* __restrict__ lists,
+                                                   const int64_t* __restrict__ dtot,
                                                    const unsigned long long* __restrict__ cnt,
                                                    unsigned long long* __restrict__ evals) {
+  const int64_t total = *dtot;
   const int64_t c = (int64_t)cnt[1];
   unsigned long long ev = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < c; k += (int64_t)gridDim.x * blockDim.x) {
