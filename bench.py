@@ -415,23 +415,26 @@ def host_cores():
     return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
 
 
-def oracle_step_estimate(cfg, V, T, budget_s=20.0, gmres_iters=None, mv_gb=1.0, seed=0):
+def oracle_step_estimate(cfg, V, T, gmres_iters=None, mv_gb=1.0, seed=0):
     """Time the oracle (as it stands, OpenMP over all host cores) on a bounded sample of the
     workload and scale to one full step (tree + near field + ACA + GMRES):
-      tree       built in full and timed;
-      near / ACA random windows of 64 x cores consecutive leaves of each canonical list, one
-                 or_assemble call per window (the previous window's blocks are released
-                 outside the timed call); time per entry (near) and per sum(m+n) (ACA) scaled
-                 to the full lists;
-      matvec     or_matvec timed on a contiguous dense sample and a contiguous low-rank sample
-                 of mv_gb/2 GB of stored H each (larger than the host's L3, so streamed from
-                 DRAM like the full product), minus the time of the same call with nothing
-                 stored (or_matvec's per-call work: the permutation, the nth x N partial sums
-                 and their reduction, at the full N); full product = that per-call time +
-                 dense bytes / dense rate + low-rank bytes / low-rank rate;
-      solve      gmres_iters x the full product (GMRES's BLAS-1 work is left out: < 2% of
-                 an oracle iteration at C3, see tools/oracle_full_step.py).
-    Validated against a fully measured oracle step at C3 (profiles/r02_oracle_full_c3.json)."""
+      tree      built in full and timed;
+      samples   a uniformly random subset of the dense leaves holding ~mv_gb/2 GB of entries,
+                and one of the admissible leaves holding ~mv_gb/2 GB of factors, each assembled
+                by one or_assemble_list call (the same per-leaf code and OpenMP schedule as
+                or_assemble; spread over the whole lists, so or_matvec's static split keeps
+                every thread busy, as in the full product);
+      near/ACA  time per entry (dense) and per sum(m+n) (admissible) of those calls, scaled to
+                the full lists;
+      matvec    or_matvec on each sample minus the same call with nothing stored (its per-call
+                work at the full N: permutation, nth x N partial sums and their reduction);
+                full product = that per-call time + dense bytes / dense rate + low-rank bytes /
+                low-rank rate (low-rank bytes from the sample's mean rank);
+      solve     (gmres_iters + 1) full products (the last one: or_gmres's true residual) + the
+                orthogonalisation, measured as or_gmres on the low-rank sample for G0 iterations
+                minus their products, scaled by sum of the Krylov index j (CGS2 costs ~ j N).
+    Validated against a fully measured oracle step at C3 (tools/oracle_full_step.py,
+    profiles/r02_oracle_full_c3.json)."""
     from oracle import oracle as O
     t0 = time.perf_counter()
     P = O.Problem(V, T, LEAF, ETA)
@@ -441,84 +444,67 @@ def oracle_step_estimate(cfg, V, T, budget_s=20.0, gmres_iters=None, mv_gb=1.0, 
     am = ((adm[:, 1] - adm[:, 0]) + (adm[:, 3] - adm[:, 2])).astype(np.int64)
     rng = np.random.default_rng(seed)
     cores = host_cores()
-    win = 64 * cores
-
-    def windows(n, share_s, assemble, work, want_k):
-        t_used, w_done, k_tot, k_cnt, nwin = 0.0, 0, 0.0, 0, 0
-        for st in rng.permutation(max(1, n - win + 1)):
-            lo, hi = int(st), int(min(n, st + win))
-            P.release()
-            ta = time.perf_counter()
-            assemble(lo, hi)
-            t_used += time.perf_counter() - ta
-            w_done += int(work[lo:hi].sum())
-            nwin += 1
-            if want_k:
-                ks = np.array([P.rank(b) for b in range(lo, hi)], dtype=np.float64)
-                k_tot += float(ks @ am[lo:hi]); k_cnt += int(am[lo:hi].sum())
-            if t_used > share_s or w_done >= work.sum():
-                break
-        return t_used, w_done, (k_tot / k_cnt if k_cnt else 0.0), nwin
-
-    tn, wn, _, nwn = windows(len(dense), 0.25 * budget_s, lambda lo, hi: P.assemble(EPS, 64, (lo, hi), (0, 0)), dm, False)
-    if len(adm):
-        ta, wa, kbar, nwa = windows(len(adm), 0.35 * budget_s, lambda lo, hi: P.assemble(EPS, 64, (0, 0), (lo, hi)),
-                                    am, True)
-    else:
-        ta, wa, kbar, nwa = 0.0, 1, 0.0, 0
-    near_full = tn * dm.sum() / max(1, wn)
-    aca_full = ta * am.sum() / max(1, wa) if len(adm) else 0.0
-
     x = np.random.default_rng(1).standard_normal(P.N)
 
-    def time_matvec(reps=3):
+    def time_matvec(reps=5, warm=2):
+        # the first products after an assembly run slower (thread wake-up, first touch of the
+        # per-thread partial vectors): warm-up calls, then the median
         ts = []
-        for _ in range(reps):
-            tm = time.perf_counter(); P.matvec(x); ts.append(time.perf_counter() - tm)
+        for r in range(warm + reps):
+            tm = time.perf_counter(); P.matvec(x); dt = time.perf_counter() - tm
+            if r >= warm:
+                ts.append(dt)
         return statistics.median(ts)
 
     P.release()
     t_empty = time_matvec()
-
-    def contiguous(work_bytes, nleaves, target):
-        lo = int(rng.integers(0, max(1, nleaves)))
-        c = np.cumsum(work_bytes[lo:])
-        hi = lo + int(np.searchsorted(c, target)) + 1
-        if hi > nleaves:                       # wrap: take the range ending at the list's end
-            c = np.cumsum(work_bytes[::-1])
-            lo = nleaves - (int(np.searchsorted(c, target)) + 1)
-            hi = nleaves
-        return max(0, lo), min(nleaves, hi)
-
-    rates, sampled = {}, {}
     half = 0.5 * mv_gb * 1e9
-    d0, d1 = contiguous(8 * dm, len(dense), half)
-    P.release(); P.assemble(EPS, 64, (d0, d1), (0, 0))
+    none = np.zeros(0, dtype=np.int64)
+    # dense sample
+    fd = min(1.0, half / max(1.0, 8.0 * dm.sum()))
+    dl = np.nonzero(rng.random(len(dense)) < fd)[0]
+    ta = time.perf_counter(); P.assemble_list(EPS, dl, none); near_t = time.perf_counter() - ta
     bd = 8.0 * P.stored_doubles()
-    rates["dense"] = bd / max(1e-9, time_matvec() - t_empty)
-    sampled["dense"] = (d1 - d0, bd)
+    rate_d = bd / max(1e-9, time_matvec() - t_empty)
+    near_full = near_t * dm.sum() / max(1, dm[dl].sum())
+    # admissible sample (size from a first guess of the mean rank, 9)
+    aca_full, rate_a, kbar, al, ba, blas_j = 0.0, 1.0, 0.0, none, 0.0, 0.0
+    g0 = 0
     if len(adm):
-        a0, a1 = contiguous(8 * am * max(kbar, 1.0), len(adm), half)
-        P.release(); P.assemble(EPS, 64, (0, 0), (a0, a1))
+        fa = min(1.0, half / max(1.0, 8.0 * 9.0 * am.sum()))
+        al = np.nonzero(rng.random(len(adm)) < fa)[0]
+        if al.size == 0:
+            al = np.array([int(rng.integers(0, len(adm)))], dtype=np.int64)
+        P.release()
+        ta = time.perf_counter(); P.assemble_list(EPS, none, al); aca_t = time.perf_counter() - ta
+        ks = np.array([P.rank(b) for b in al], dtype=np.float64)
+        kbar = float(ks @ am[al]) / max(1, am[al].sum())
         ba = 8.0 * P.stored_doubles()
-        rates["lowrank"] = ba / max(1e-9, time_matvec() - t_empty)
-        sampled["lowrank"] = (a1 - a0, ba)
+        t_mv_a = time_matvec()
+        rate_a = ba / max(1e-9, t_mv_a - t_empty)
+        aca_full = aca_t * am.sum() / max(1, am[al].sum())
+        # orthogonalisation cost of or_gmres (CGS2 + Givens), per unit of Krylov index j
+        g0 = int(min(20, max(1, gmres_iters or 1)))
+        b = np.random.default_rng(2).standard_normal(P.N)
+        tg = time.perf_counter(); P.gmres(b, tol=1e-300, restart=100, maxit=g0); tg = time.perf_counter() - tg
+        blas_j = max(0.0, tg - (g0 + 1) * t_mv_a) / (g0 * (g0 + 1) / 2)
     P.release()
     dense_bytes = 8.0 * dm.sum()
     lr_bytes = 8.0 * kbar * am.sum()
-    matvec_s = t_empty + dense_bytes / rates["dense"] + (lr_bytes / rates["lowrank"] if len(adm) else 0.0)
-    solve_s = (gmres_iters or 0) * matvec_s
+    matvec_s = t_empty + dense_bytes / rate_d + (lr_bytes / rate_a if len(adm) else 0.0)
+    it = int(gmres_iters or 0)
+    jsum = sum(((j % 100) + 1) for j in range(it))          # Krylov index j of every iteration (restart 100)
+    solve_s = (it + 1) * matvec_s + blas_j * jsum
     return {"tree_s": tree_s, "near_s": near_full, "aca_s": aca_full, "solve_s": solve_s, "matvec_s": matvec_s,
-            "matvec_empty_call_s": t_empty, "matvec_rate_GBps": {k: v / 1e9 for k, v in rates.items()},
-            "k_mean_sampled": kbar,
-            "sample": f"tree full; near field: {nwn} random windows of {win} consecutive dense leaves ({wn} of "
-                      f"{int(dm.sum())} entries); ACA: {nwa} windows of {win} admissible leaves ({wa} of "
-                      f"{int(am.sum())} sum(m+n)); rates scaled to the full lists; matvec: contiguous samples of "
-                      f"{sampled['dense'][0]} dense leaves ({sampled['dense'][1]/1e9:.2f} GB)"
-                      + (f" and {sampled['lowrank'][0]} admissible leaves ({sampled['lowrank'][1]/1e9:.2f} GB)"
-                         if len(adm) else "")
-                      + f" minus the empty-call time {t_empty:.3f} s, scaled to {(dense_bytes + lr_bytes)/1e9:.2f} GB; "
-                      f"solve = {gmres_iters} GMRES iterations x the full product",
+            "matvec_empty_call_s": t_empty, "matvec_rate_GBps": {"dense": rate_d / 1e9, "lowrank": rate_a / 1e9},
+            "gmres_orth_s_per_j": blas_j, "k_mean_sampled": kbar,
+            "sample": f"tree full; {dl.size} random dense leaves ({int(dm[dl].sum())} of {int(dm.sum())} entries, "
+                      f"{bd/1e9:.2f} GB) and {al.size} random admissible leaves ({int(am[al].sum()) if al.size else 0} of "
+                      f"{int(am.sum())} sum(m+n), {ba/1e9:.2f} GB of factors), each set assembled by one "
+                      f"or_assemble_list call and multiplied by or_matvec (minus its {t_empty:.3f} s empty-call time); "
+                      f"rates scaled to the full lists ({(dense_bytes + lr_bytes)/1e9:.2f} GB of H); solve = "
+                      f"{it} GMRES iterations + 1 true-residual product + CGS2 orthogonalisation measured on "
+                      f"{g0} or_gmres iterations",
             "cores": cores}
 
 
@@ -531,7 +517,7 @@ def oracle_gmres_iters(cfg):
     return None
 
 
-def cpu_baseline(cfg, V, T, gmres_iters, budget_s=20.0):
+def cpu_baseline(cfg, V, T, gmres_iters):
     """The oracle timed on the host (bounded sample, see oracle_step_estimate).  The GMRES
     iteration count is the oracle's own where a full oracle solve was run and committed (C1-C3,
     profiles/r02_oracle_gmres_iters.json); at C4-C6 the oracle's H (158 GB at C4) does not fit
@@ -540,7 +526,7 @@ def cpu_baseline(cfg, V, T, gmres_iters, budget_s=20.0):
     it_or = oracle_gmres_iters(cfg)
     it = it_or if it_or is not None else gmres_iters
     try:
-        e = oracle_step_estimate(cfg, V, T, budget_s, it)
+        e = oracle_step_estimate(cfg, V, T, it)
     except Exception as ex:  # the baseline must not take the bench down
         return {"error": str(ex)}
     step = e["tree_s"] + e["near_s"] + e["aca_s"] + e["solve_s"]
@@ -566,11 +552,8 @@ def run_reference(args):
     vals = []
     it_or = oracle_gmres_iters(args.config)
     iters = it_or if it_or is not None else GPU_GMRES_ITERS.get(args.config, 100)
-    nst = max(1, args.steps + args.warmup)
-    budget = max(4.0, 150.0 / nst)
     for s in range(args.warmup + args.steps):
-        e = oracle_step_estimate(args.config, V, T, budget_s=budget, gmres_iters=iters, mv_gb=max(0.2, budget / 25.0),
-                                 seed=s)
+        e = oracle_step_estimate(args.config, V, T, gmres_iters=iters, mv_gb=0.5, seed=s)
         if s >= args.warmup:
             vals.append(e["tree_s"] + e["near_s"] + e["aca_s"] + e["solve_s"])
     v = statistics.median(vals)
@@ -579,7 +562,7 @@ def run_reference(args):
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "N": N},
            "cpu_baseline": {"value": round(v, 3), "kind": "oracle", "cores": e["cores"],
-                            "sample": "each step: " + e["sample"], "gmres_iters": iters,
+                            "sample": "each step (fresh tree, fresh random leaf samples): " + e["sample"], "gmres_iters": iters,
                             "gmres_iters_source": "oracle GMRES (committed)" if it_or is not None else "GPU GMRES",
                             "steps_are": "bounded-sample estimates of one full oracle step (median reported)"},
            "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -93,6 +93,10 @@ int or_aca_matrix(const double* A, int m, int n, double eps, int kcap,
  * Returns 0 on success. */
 int or_assemble(or_problem* P, double eps, int kcap, int64_t d0, int64_t d1,
                 int64_t a0, int64_t a1);
+/* The same for explicit ascending lists of dense / admissible leaf indices (timing samples
+ * spread over the whole lists). */
+int or_assemble_list(or_problem* P, double eps, int kcap, int64_t nd, const int64_t* dense_leaves,
+                     int64_t na, const int64_t* adm_leaves);
 /* Free the blocks of the last or_assemble (or_assemble itself frees them first). */
 void or_release(or_problem* P);
 int64_t or_stored_doubles(const or_problem* P);                /* dense + factor doubles */

@@ -67,6 +67,8 @@ def lib():
         L.or_assemble.argtypes = [P, d, i32, i64, i64, i64, i64]
         L.or_stored_doubles.restype = i64; L.or_stored_doubles.argtypes = [P]
         L.or_release.argtypes = [P]
+        L.or_assemble_list.restype = i32
+        L.or_assemble_list.argtypes = [P, d, i32, i64, ptr, i64, ptr]
         L.or_get_rank.restype = i32; L.or_get_rank.argtypes = [P, i64]
         L.or_get_factors.argtypes = [P, i64, ptr, ptr]
         L.or_get_pivots.argtypes = [P, i64, ptr]
@@ -222,6 +224,12 @@ class Problem:
         d0, d1 = dense_range if dense_range is not None else (0, nd)
         a0, a1 = adm_range if adm_range is not None else (0, na)
         return lib().or_assemble(self._h, eps, kcap, d0, d1, a0, a1)
+
+    def assemble_list(self, eps, dense_leaves, adm_leaves, kcap=64):
+        """Assemble only the listed leaves (ascending indices into the canonical lists)."""
+        dl = np.ascontiguousarray(dense_leaves, dtype=np.int64)
+        al = np.ascontiguousarray(adm_leaves, dtype=np.int64)
+        return lib().or_assemble_list(self._h, eps, kcap, dl.size, _p(dl), al.size, _p(al))
 
     def release(self):
         """Free the stored blocks (outside any timed region)."""

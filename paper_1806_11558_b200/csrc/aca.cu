@@ -510,10 +510,24 @@ template <class M>
 void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWork& W) {
   if (upper <= 0) return;
   cudaStream_t st = C.stream;
-  HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 2 * sizeof(unsigned long long), st));
+  HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 3 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
-  const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4 * 2);
-  k_eval_class3<M><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
+  // option "eval_variant" (A/B of the order-3 kernel): 0 / 1 / 2 = grid-stride with 4 / 5 / 6
+  // CTAs of 128 per SM (register caps 128 / 102 / 85), 3 / 4 = dynamic groups with 4 / 5;
+  // grid = option "aca_waves" waves of resident CTAs
+  const int v = C.eval_variant;
+  const int minb = (v == 1 || v == 4) ? 5 : v == 2 ? 6 : 4;
+  const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), (int64_t)148 * minb * C.aca_waves);
+  unsigned long long* cnt = W.cnt.get();
+  auto* L = W.lists.get();
+  auto* E = W.ev.get();
+  switch (v) {
+    case 1: k_eval_class3<M, 5, false><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
+    case 2: k_eval_class3<M, 6, false><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
+    case 3: k_eval_class3<M, 4, true><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
+    case 4: k_eval_class3<M, 5, true><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
+    default: k_eval_class3<M, 4, false><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
+  }
   HM_CHECK_LAUNCH();
   const unsigned g4 = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 16);
   k_eval_list<4, M><<<g4, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
@@ -582,15 +596,15 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   W.lists.alloc(std::max(rmax, cmax));
   W.rtab.alloc(rmax / 32 + 2);
   W.ctab.alloc(cmax / 32 + 2);
-  W.cnt.alloc(2);
+  W.cnt.alloc(3);
   W.h_ring.resize(3 * (kLag + 1));
   for (auto& e : W.ring_ev)
     if (!e) HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const int64_t* drow = W.tot.get();          // tot[0]: row entries, tot[1]: column entries, tot[2]: active blocks
   const int64_t* dcol = W.tot.get() + 1;
   const int64_t* dnact = W.tot.get() + 2;
-  const unsigned gpiv = (unsigned)std::min<int64_t>(grid_for(nb * 32, 256), 148 * 8);
-  const unsigned gupd = (unsigned)std::min<int64_t>(grid_for(nb * 32, 64), 148 * 16);
+  const unsigned gpiv = (unsigned)std::min<int64_t>(grid_for(nb * 32, 256), (int64_t)148 * 8 * C.aca_waves);
+  const unsigned gupd = (unsigned)std::min<int64_t>(grid_for(nb * 32, 64), (int64_t)148 * 16 * C.aca_waves);
   for (int step = 0;; ++step) {
     std::unique_ptr<KScope> ks(new KScope(C, KF_ACA_OTHER));
     k_step_flags<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.state.get(), nb, W.flag.get());

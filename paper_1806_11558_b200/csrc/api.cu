@@ -348,6 +348,8 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "max_iter") { if (v < 1) bad(); C.max_iter = (int)v; }
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
     else if (k == "aca_kws") { if (v < 1 || v > 256) bad(); C.aca_kws = v; }
+    else if (k == "eval_variant") { if (v < 0 || v > 4) bad(); C.eval_variant = (int)v; }
+    else if (k == "aca_waves") { if (v < 1 || v > 1024) bad(); C.aca_waves = (int)v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
     else if (k == "mv_kernel") { if (v != 0 && v != 1) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_profile") {
@@ -380,6 +382,8 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "max_iter") *v = C.max_iter;
     else if (k == "aca_chunk_mb") *v = C.aca_chunk_mb;
     else if (k == "aca_kws") *v = C.aca_kws;
+    else if (k == "eval_variant") *v = C.eval_variant;
+    else if (k == "aca_waves") *v = C.aca_waves;
     else if (k == "record_pivots") *v = C.record_pivots;
     else if (k == "kernel_timing") *v = C.kt.on ? 1 : 0;
     else if (k == "mv_kernel") *v = C.mv_kind;

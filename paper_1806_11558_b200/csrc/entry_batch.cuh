@@ -164,39 +164,59 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
 //                   classes to the back (warp-aggregated atomics);
 //   k_eval_list<4>  persistent grid-stride over the order-4 list (count read on the device);
 //   k_eval_rest     persistent, the remaining few (orders 5, 6, touching pairs).
+// one 32-entry group of a warp (lanes e = e0 + lane): classify, append non-order-3 entries,
+// evaluate order 3 in place
 template <class M>
-__global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __restrict__ dtot,
-                                                     EntryRef* __restrict__ lists,
-                                                     unsigned long long* __restrict__ cnt /* [n4, nrest] */,
-                                                     unsigned long long* __restrict__ evals) {
+__device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t total, int lane, EntryRef* __restrict__ lists,
+                                             unsigned long long* __restrict__ cnt, unsigned long long& ev) {
+  EntryRef r;
+  int cls = -1, xs = 0, ys = 0;
+  if (m.locate(e, e < total, r)) {
+    int s, t;
+    m.pair(r, s, t);
+    cls = map_class(m, s, t, xs, ys);
+  }
+  const unsigned below = (1u << lane) - 1u;
+  const unsigned b4 = __ballot_sync(0xffffffffu, cls == 4), br = __ballot_sync(0xffffffffu, cls >= 0 && cls != 3 && cls != 4);
+  unsigned long long base4 = 0, baser = 0;
+  if (lane == 0) {
+    if (b4) base4 = atomicAdd(&cnt[0], (unsigned long long)__popc(b4));
+    if (br) baser = atomicAdd(&cnt[1], (unsigned long long)__popc(br));
+  }
+  base4 = __shfl_sync(0xffffffffu, base4, 0);
+  baser = __shfl_sync(0xffffffffu, baser, 0);
+  if (cls == 4) lists[base4 + __popc(b4 & below)] = r;
+  else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
+  if (cls == 3) {
+    m.put(r, map_regular<3>(m, xs, ys));
+    ev += M::kQuad ? 81 : tri_rule_points(3) * tri_rule_points(3);
+  }
+}
+
+// DYN = false: grid-stride (static) over the batch; DYN = true: every warp takes groups of
+// kDynGroups x 32 entries from the counter cnt[2] (dynamic balance across SMs)
+constexpr int kDynGroups = 4;
+template <class M, int MINB = 4, bool DYN = false>
+__global__ void __launch_bounds__(128, MINB) k_eval_class3(M m, const int64_t* __restrict__ dtot,
+                                                        EntryRef* __restrict__ lists,
+                                                        unsigned long long* __restrict__ cnt /* [n4, nrest, next] */,
+                                                        unsigned long long* __restrict__ evals) {
   const int64_t total = *dtot;
   const int lane = threadIdx.x & 31;
-  const unsigned below = (1u << lane) - 1u;
   unsigned long long ev = 0;
-  // the loop bound is uniform per CTA, so every warp runs whole iterations (full-mask ballots)
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = base + threadIdx.x;
-    EntryRef r;
-    int cls = -1, xs = 0, ys = 0;
-    if (m.locate(e, e < total, r)) {
-      int s, t;
-      m.pair(r, s, t);
-      cls = map_class(m, s, t, xs, ys);
+  if (DYN) {
+    for (;;) {
+      unsigned long long b0 = 0;
+      if (lane == 0) b0 = atomicAdd(&cnt[2], (unsigned long long)(32 * kDynGroups));
+      b0 = __shfl_sync(0xffffffffu, b0, 0);
+      if ((int64_t)b0 >= total) break;
+#pragma unroll 1
+      for (int g = 0; g < kDynGroups; ++g) class3_group(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
     }
-    const unsigned b4 = __ballot_sync(0xffffffffu, cls == 4), br = __ballot_sync(0xffffffffu, cls >= 0 && cls != 3 && cls != 4);
-    unsigned long long base4 = 0, baser = 0;
-    if (lane == 0) {
-      if (b4) base4 = atomicAdd(&cnt[0], (unsigned long long)__popc(b4));
-      if (br) baser = atomicAdd(&cnt[1], (unsigned long long)__popc(br));
-    }
-    base4 = __shfl_sync(0xffffffffu, base4, 0);
-    baser = __shfl_sync(0xffffffffu, baser, 0);
-    if (cls == 4) lists[base4 + __popc(b4 & below)] = r;
-    else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
-    if (cls == 3) {
-      m.put(r, map_regular<3>(m, xs, ys));
-      ev += M::kQuad ? 81 : tri_rule_points(3) * tri_rule_points(3);
-    }
+  } else {
+    // the loop bound is uniform per CTA, so every warp runs whole iterations (full-mask ballots)
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x)
+      class3_group(m, base + threadIdx.x, total, lane, lists, cnt, ev);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);

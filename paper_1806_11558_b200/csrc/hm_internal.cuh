@@ -226,6 +226,8 @@ struct Context {
   int k_max = 64, solver = 0, restart = 100, max_iter = 10000;
   int record_pivots = -1;      // -1 auto (N <= 25000), 0 off, 1 on
   double aca_chunk_mb = 32768, aca_kws = 16;
+  int eval_variant = 0;        // diagnostic option "eval_variant": variant of the ACA order-3 kernel
+  int aca_waves = 2;           // diagnostic option "aca_waves": grid of the persistent ACA kernels, in waves
 
   // tree state
   bool have_tree = false, have_setup = false;

@@ -15,7 +15,16 @@ METRICS = {
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_cyc_pct",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_pct",
     "launch__grid_size": "grid",
+    "launch__block_size": "block",
+    "sm__sass_thread_inst_executed_op_dadd_pred_on.sum": "dadd",
+    "sm__sass_thread_inst_executed_op_dmul_pred_on.sum": "dmul",
+    "sm__sass_thread_inst_executed_op_dfma_pred_on.sum": "dfma",
+    "smsp__inst_executed_pipe_fp64.sum": "fp64_warp_inst",
+    "smsp__inst_executed.sum": "warp_inst",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
 }
+STALL = re.compile(r"smsp__average_warp_latency_issue_stalled_(\w+)\.ratio$|smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio$")
 FULLNAME = True
 
 
@@ -45,6 +54,16 @@ def rows(path):
                 except ValueError:
                     pass
                 rec[k] = v
+        stalls = {}
+        for h, i in idx.items():
+            m = STALL.match(h)
+            if m:
+                try:
+                    stalls[m.group(1) or m.group(2)] = float(d[i].replace(",", ""))
+                except ValueError:
+                    pass
+        if stalls:
+            rec["stalls_top"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:6])
         yield rec
 
 

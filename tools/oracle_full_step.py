@@ -32,7 +32,6 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--out", default=None)
     ap.add_argument("--tol", type=float, default=1e-8)
-    ap.add_argument("--budget", type=float, default=20.0)
     ap.add_argument("--gpu-solution", default=None)
     ap.add_argument("--parity-tol", type=float, default=1e-10)
     args = ap.parse_args()
@@ -64,7 +63,7 @@ def main():
         res["parity_tol"] = args.parity_tol
     P = None
     t0 = time.perf_counter()
-    e = bench.oracle_step_estimate(args.config, V, T, budget_s=args.budget, gmres_iters=it)
+    e = bench.oracle_step_estimate(args.config, V, T, gmres_iters=it)
     res["estimator_wall_s"] = time.perf_counter() - t0
     est = e["tree_s"] + e["near_s"] + e["aca_s"] + e["solve_s"]
     res["estimate"] = {k: (float(v) if isinstance(v, (int, float, np.floating)) else v) for k, v in e.items()}
