@@ -199,6 +199,8 @@ def _run_gpu(args, rank, world, local, dev, stream):
     H.N = N
     H.set_option("solver", 0)
     H.set_option("restart", 100)
+    if args.lr_f32:                     # SURVEY §8(f)-4 option: ACA factors stored in binary32
+        H.set_option("lr_f32", 1)
     # rhs = the paper's f, assembled by the library
     H.build_tree(Vd, Td, LEAF, ETA)
     f = torch.empty(N, dtype=torch.float64, device=dev)
@@ -386,6 +388,8 @@ def _run_gpu(args, rank, world, local, dev, stream):
             "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "N": N, "leaf_size": LEAF, "eta": ETA,
                        "eps_aca": EPS, "solver": "GMRES(100)", "tol": TOL, "rhs": "paper f=4x^2-3y^2-z^2",
                        "parallelism": f"leaf-partition x{world}",
+                       "factor_storage": "binary32 U, V (option lr_f32; dense blocks and all arithmetic FP64)"
+                       if args.lr_f32 else "FP64",
                        "l2": "inputs larger than L2 (stored H >> 126 MB); matvec timing flushes L2 with a 256 MB write"},
             "breakdown": {"instrumented_steps": KI, "ms_per_step_instrumented": round(ms_instr, 3),
                           "cold_first_step": cold, "tree_s": round(tree_s, 6), "setup_s": round(setup_s, 6), "near_field_s": round(near_s, 6),
@@ -581,6 +585,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--instrumented-steps", type=int, default=2)
+    ap.add_argument("--lr-f32", action="store_true", help="store the ACA factors in binary32 (option lr_f32)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -115,6 +115,11 @@ const char* hm_last_error(hm_ctx ctx);
  *   "mv_concurrent" 1 (default): the large low-rank matvec kernels run on a library side
  *                  stream beside the small-leaf pipeline (joined before hm_matvec returns its
  *                  stream order); 0: one stream
+ *   "lr_f32"       1: hm_setup stores the ACA factors U, V in binary32 (each entry rounded once;
+ *                  dense blocks, ACA itself and all matvec / Krylov arithmetic stay FP64: the
+ *                  matvec widens the factors exactly before every FMA).  Halves the low-rank bytes
+ *                  the matvec streams.  0 (default): FP64 factors.
+ *                  Takes effect at the next hm_setup; hm_get_lowrank returns the widened values.
  *   "setup_overlap" 1: hm_setup evaluates the near field on a least-priority stream from a
  *                  second host thread while ACA runs on a greatest-priority stream (results
  *                  bit-identical; ~5% shorter setup at N = 1.57M); 0 (default) serial.  With

@@ -222,14 +222,21 @@ __device__ __forceinline__ void aca_pivot_block(const AcaBlk* __restrict__ B, Ac
 }
 
 
-// one warp per active block, persistent over the step's active count *dnact (device)
+// next active block of a persistent warp (dynamic: counter *ctr, reset to 0 before the launch)
+__device__ __forceinline__ int64_t next_block(unsigned long long* ctr, int lane) {
+  unsigned long long a = 0;
+  if (lane == 0) a = atomicAdd(ctr, 1ull);
+  return (int64_t)__shfl_sync(0xffffffffu, a, 0);
+}
+
+// one warp per active block, persistent and dynamically balanced over the step's active count
+// *dnact (device)
 __global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, const int32_t* __restrict__ act,
-                            const int64_t* __restrict__ dnact, double* __restrict__ Vw, uint32_t* __restrict__ bmap) {
+                            const int64_t* __restrict__ dnact, double* __restrict__ Vw, uint32_t* __restrict__ bmap,
+                            unsigned long long* __restrict__ ctr) {
   const int64_t nact = *dnact;
   const int lane = threadIdx.x & 31;
-  for (int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; a < nact;
-       a += ((int64_t)gridDim.x * blockDim.x) >> 5)
-    aca_pivot_block(B, S, act[a], Vw, bmap, lane);
+  for (int64_t a = next_block(ctr, lane); a < nact; a = next_block(ctr, lane)) aca_pivot_block(B, S, act[a], Vw, bmap, lane);
 }
 
 // k_aca_pivot for the big blocks of the chunk (m + n >= kBigMN): one CTA per block
@@ -414,16 +421,15 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
 }
 
 // G = 1: one warp per active block (small blocks; big ones are skipped), act[] = compact list;
-// persistent over the step's active count *dnact (device)
+// persistent and dynamically balanced over the step's active count *dnact (device)
 __global__ void __launch_bounds__(64, 16) k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
                                                     const int32_t* __restrict__ act, const int64_t* __restrict__ dnact,
                                                     const double* __restrict__ Uw, const double* __restrict__ Vw,
                                                     const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv,
-                                                    int kws, double eps) {
+                                                    int kws, double eps, unsigned long long* __restrict__ ctr) {
   const int64_t nact = *dnact;
   const int lane = threadIdx.x & 31;
-  for (int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; a < nact;
-       a += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+  for (int64_t a = next_block(ctr, lane); a < nact; a = next_block(ctr, lane)) {
     const int64_t c = act[a];
     AcaState st = S[c];
     const AcaBlk b = B[c];
@@ -469,13 +475,15 @@ __global__ void k_final_sizes(const AcaBlk* __restrict__ B, const AcaState* __re
   if (st.status == 2) ovf[atomicAdd(novf, 1ull)] = owned[c];
 }
 // pack finished blocks: [U (m x k) | V (n x k)] column-major, straight copies of the
-// first k workspace columns; one CTA per block.  The copy also checks every factor entry for
-// finiteness (hm.h: HM_ERR_NUMERIC names the first offending block): bad = min owned index.
+// first k workspace columns (T = float: option lr_f32, each entry rounded to binary32 once);
+// one CTA per block.  The copy also checks every factor entry for finiteness (hm.h:
+// HM_ERR_NUMERIC names the first offending block): bad = min owned index.
+template <class T>
 __global__ void __launch_bounds__(256) k_aca_store(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S,
                                                    int64_t nb, const int32_t* __restrict__ owned,
                                                    const int64_t* __restrict__ fpre, int64_t base,
                                                    const double* __restrict__ Uw, const double* __restrict__ Vw,
-                                                   double* __restrict__ pool, int64_t* __restrict__ foff,
+                                                   T* __restrict__ pool, int64_t* __restrict__ foff,
                                                    int32_t* __restrict__ frank, int32_t* __restrict__ bad) {
   const int64_t c = blockIdx.x;
   if (c >= nb) return;
@@ -485,8 +493,8 @@ __global__ void __launch_bounds__(256) k_aca_store(const AcaBlk* __restrict__ B,
   const int64_t o = base + fpre[c];
   const int64_t mu = (int64_t)st.k * b.m, nv = (int64_t)st.k * b.n;
   bool fin = true;
-  for (int64_t x = threadIdx.x; x < mu; x += blockDim.x) { const double a = Uw[b.uoff + x]; fin &= isfinite(a); pool[o + x] = a; }
-  for (int64_t x = threadIdx.x; x < nv; x += blockDim.x) { const double a = Vw[b.voff + x]; fin &= isfinite(a); pool[o + mu + x] = a; }
+  for (int64_t x = threadIdx.x; x < mu; x += blockDim.x) { const T a = (T)Uw[b.uoff + x]; fin &= isfinite(a); pool[o + x] = a; }
+  for (int64_t x = threadIdx.x; x < nv; x += blockDim.x) { const T a = (T)Vw[b.voff + x]; fin &= isfinite(a); pool[o + mu + x] = a; }
   if (!fin) atomicMin(bad, owned[c]);
   if (threadIdx.x == 0) {
     foff[owned[c]] = o;
@@ -512,22 +520,8 @@ void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWor
   cudaStream_t st = C.stream;
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 3 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
-  // option "eval_variant" (A/B of the order-3 kernel): 0 / 1 / 2 = grid-stride with 4 / 5 / 6
-  // CTAs of 128 per SM (register caps 128 / 102 / 85), 3 / 4 = dynamic groups with 4 / 5;
-  // grid = option "aca_waves" waves of resident CTAs
-  const int v = C.eval_variant;
-  const int minb = (v == 1 || v == 4) ? 5 : v == 2 ? 6 : 4;
-  const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), (int64_t)148 * minb * C.aca_waves);
-  unsigned long long* cnt = W.cnt.get();
-  auto* L = W.lists.get();
-  auto* E = W.ev.get();
-  switch (v) {
-    case 1: k_eval_class3<M, 5, false><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
-    case 2: k_eval_class3<M, 6, false><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
-    case 3: k_eval_class3<M, 4, true><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
-    case 4: k_eval_class3<M, 5, true><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
-    default: k_eval_class3<M, 4, false><<<g, 128, 0, st>>>(m, dtot, L, cnt, E); break;
-  }
+  const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4);   // one wave, persistent
+  k_eval_class3<M><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
   const unsigned g4 = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 16);
   k_eval_list<4, M><<<g4, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
@@ -596,15 +590,15 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   W.lists.alloc(std::max(rmax, cmax));
   W.rtab.alloc(rmax / 32 + 2);
   W.ctab.alloc(cmax / 32 + 2);
-  W.cnt.alloc(3);
+  W.cnt.alloc(5);                 // [n4, nrest, next entry group | pivot, update block counters]
   W.h_ring.resize(3 * (kLag + 1));
   for (auto& e : W.ring_ev)
     if (!e) HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const int64_t* drow = W.tot.get();          // tot[0]: row entries, tot[1]: column entries, tot[2]: active blocks
   const int64_t* dcol = W.tot.get() + 1;
   const int64_t* dnact = W.tot.get() + 2;
-  const unsigned gpiv = (unsigned)std::min<int64_t>(grid_for(nb * 32, 256), (int64_t)148 * 8 * C.aca_waves);
-  const unsigned gupd = (unsigned)std::min<int64_t>(grid_for(nb * 32, 64), (int64_t)148 * 16 * C.aca_waves);
+  const unsigned gpiv = (unsigned)std::min<int64_t>(grid_for(nb * 32, 256), 148 * 8);   // one wave each
+  const unsigned gupd = (unsigned)std::min<int64_t>(grid_for(nb * 32, 64), 148 * 16);
   for (int step = 0;; ++step) {
     std::unique_ptr<KScope> ks(new KScope(C, KF_ACA_OTHER));
     k_step_flags<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.state.get(), nb, W.flag.get());
@@ -623,6 +617,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     });
     k_step_totals<<<1, 1, 0, st>>>(W.rpre.get(), W.cpre.get(), W.pos.get(), nb, W.tot.get());
     HM_CHECK_LAUNCH();
+    HM_CUDA(cudaMemsetAsync(W.cnt.get() + 3, 0, 2 * sizeof(unsigned long long), st));   // pivot / update counters
     const int slot = step % (kLag + 1);
     HM_CUDA(cudaMemcpyAsync(W.h_ring.data() + 3 * slot, W.tot.get(), 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     HM_CUDA(cudaEventRecord(W.ring_ev[slot], st));
@@ -639,7 +634,8 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
       aca_eval(C, AcaMap<true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
                                W.rtab.get(), nb, Uw, Vw}, drow, rmax, W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_pivot<<<gpiv, 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Vw, W.bmap.get());
+    k_aca_pivot<<<gpiv, 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Vw, W.bmap.get(),
+                                      W.cnt.get() + 3);
     HM_CHECK_LAUNCH();
     if (nbig) {
       k_aca_pivot_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Vw, W.bmap.get());
@@ -654,7 +650,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
                                 W.ctab.get(), nb, Uw, Vw}, dcol, cmax, W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
     k_aca_update<<<gupd, 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Uw, Vw, W.bmap.get(),
-                                      W.piv.get(), kws, C.eps_aca);
+                                      W.piv.get(), kws, C.eps_aca, W.cnt.get() + 4);
     HM_CHECK_LAUNCH();
     if (nbig) {
       k_aca_update_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Uw, Vw,
@@ -690,11 +686,19 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   HM_CUDA(cudaMemcpyAsync(ht, W.tot.get(), 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   HM_CUDA(cudaStreamSynchronize(st));
   const int64_t add = ht[0], nov = ht[1];
-  const int64_t base = (int64_t)(C.fpool.used / sizeof(double));
-  C.fpool.ensure((base + add) * sizeof(double) + 64);
-  C.fpool.used = (base + add) * sizeof(double);
-  k_aca_store<<<(unsigned)nb, 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(), base,
-                                           Uw, Vw, (double*)C.fpool.base, C.foff.get(), C.frank.get(), W.bad.get());
+  // factor pool in elements of C.lr_esz bytes (8, or 4 with option lr_f32)
+  const int64_t esz = C.lr_esz;
+  const int64_t base = (int64_t)(C.fpool.used / esz);
+  C.fpool.ensure((base + add) * esz + 64);
+  C.fpool.used = (base + add) * esz;
+  if (esz == 4)
+    k_aca_store<float><<<(unsigned)nb, 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(), base,
+                                                     Uw, Vw, (float*)C.fpool.base, C.foff.get(), C.frank.get(),
+                                                     W.bad.get());
+  else
+    k_aca_store<double><<<(unsigned)nb, 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(),
+                                                      base, Uw, Vw, (double*)C.fpool.base, C.foff.get(), C.frank.get(),
+                                                      W.bad.get());
   HM_CHECK_LAUNCH();
   if (nov) {
     const size_t o0 = overflow.size();
@@ -727,6 +731,7 @@ void setup_aca(Context& C) {
   auto ms_since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
   const auto t0 = clk::now();
   const int64_t nb = C.adm_end - C.adm_begin;
+  C.lr_esz = C.lr_f32 ? 4 : 8;          // factor storage precision of this setup (option lr_f32)
   C.foff.alloc(nb + 1);
   C.frank.alloc(nb + 1);
   HM_CUDA(cudaMemsetAsync(C.frank.get(), 0, (nb + 1) * sizeof(int32_t), st));
@@ -789,6 +794,7 @@ void setup_aca(Context& C) {
   // it is at most twice the budget and the factor growth still fits in the free memory.
   // the same owned block list (signature) with the same ACA options as the previous setup
   const bool steady = C.aca_prev_valid && C.aca_prev_eps == C.eps_aca && C.aca_prev_kmax == C.k_max &&
+                      C.aca_prev_esz == C.lr_esz &&
                       C.aca_prev_sig[0] == nb && C.aca_prev_sig[1] == sum_mn;
   const double prev_bytes = steady ? C.aca_prev_bytes : 0.0;   // deterministic ACA: the same factor bytes
   auto chunk_budget = [&]() {
@@ -886,13 +892,14 @@ void setup_aca(Context& C) {
                              std::to_string(q.chi) + "), internal order)");
   }
   C.evals_aca = (double)hev;
-  C.factor_doubles = (int64_t)(C.fpool.used / sizeof(double));
+  C.factor_doubles = (int64_t)(C.fpool.used / C.lr_esz);       // factor entries (stored as lr_esz bytes)
   C.aca_prev_valid = true;
   C.aca_prev_sig[0] = nb;
   C.aca_prev_sig[1] = sum_mn;
   C.aca_prev_bytes = (double)C.fpool.used;
   C.aca_prev_eps = C.eps_aca;
   C.aca_prev_kmax = C.k_max;
+  C.aca_prev_esz = C.lr_esz;
   C.times.aca_phase_ms[5] = ms_since(t5);
 }
 

@@ -348,8 +348,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "max_iter") { if (v < 1) bad(); C.max_iter = (int)v; }
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
     else if (k == "aca_kws") { if (v < 1 || v > 256) bad(); C.aca_kws = v; }
-    else if (k == "eval_variant") { if (v < 0 || v > 4) bad(); C.eval_variant = (int)v; }
-    else if (k == "aca_waves") { if (v < 1 || v > 1024) bad(); C.aca_waves = (int)v; }
+    else if (k == "lr_f32") { if (v != 0 && v != 1) bad(); C.lr_f32 = (int)v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
     else if (k == "mv_kernel") { if (v != 0 && v != 1) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_profile") {
@@ -382,8 +381,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "max_iter") *v = C.max_iter;
     else if (k == "aca_chunk_mb") *v = C.aca_chunk_mb;
     else if (k == "aca_kws") *v = C.aca_kws;
-    else if (k == "eval_variant") *v = C.eval_variant;
-    else if (k == "aca_waves") *v = C.aca_waves;
+    else if (k == "lr_f32") *v = C.lr_f32;
     else if (k == "record_pivots") *v = C.record_pivots;
     else if (k == "kernel_timing") *v = C.kt.on ? 1 : 0;
     else if (k == "mv_kernel") *v = C.mv_kind;
@@ -670,11 +668,20 @@ hm_status hm_get_lowrank(hm_ctx ctx, int64_t leaf, int32_t* k, double* U, double
     const int64_t m = q.rhi - q.rlo, n = q.chi - q.clo;
     const int32_t kk = C.h_rank[b];
     if (k) *k = kk;
-    const double* base = (const double*)C.fpool.base + C.h_foff[b];
-    if (U && kk > 0)
-      HM_CUDA(cudaMemcpyAsync(U, base, m * kk * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-    if (V && kk > 0)
-      HM_CUDA(cudaMemcpyAsync(V, base + m * kk, n * kk * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    if (C.lr_esz == 4 && kk > 0 && (U || V)) {        // binary32 factors (option lr_f32): widened exactly
+      std::vector<float> f((size_t)(m + n) * kk);
+      const float* base = (const float*)C.fpool.base + C.h_foff[b];
+      HM_CUDA(cudaMemcpyAsync(f.data(), base, f.size() * sizeof(float), cudaMemcpyDeviceToHost, C.stream));
+      HM_CUDA(cudaStreamSynchronize(C.stream));
+      if (U) for (int64_t x = 0; x < m * kk; ++x) U[x] = f[x];
+      if (V) for (int64_t x = 0; x < n * kk; ++x) V[x] = f[m * kk + x];
+    } else {
+      const double* base = (const double*)C.fpool.base + C.h_foff[b];
+      if (U && kk > 0)
+        HM_CUDA(cudaMemcpyAsync(U, base, m * kk * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+      if (V && kk > 0)
+        HM_CUDA(cudaMemcpyAsync(V, base + m * kk, n * kk * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    }
     if (pivots) {
       if (C.h_piv.size() != (size_t)(C.adm_end - C.adm_begin)) hm::fail(HM_ERR_STATE, "pivots not recorded: set option record_pivots = 1 before hm_setup");
       std::memcpy(pivots, C.h_piv[b].data(), C.h_piv[b].size() * sizeof(int32_t));
@@ -710,7 +717,8 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
       << ",\"dense_leaves\":" << C.ndense << ",\"adm_owned\":[" << C.adm_begin << "," << C.adm_end << "]"
       << ",\"dense_owned\":[" << C.dense_begin << "," << C.dense_end << "]"
       << ",\"dense_doubles\":" << C.dense_doubles << ",\"factor_doubles\":" << C.factor_doubles
-      << ",\"stored_bytes\":" << 8 * (C.dense_doubles + C.factor_doubles) << ",\"eps_aca\":" << C.eps_aca
+      << ",\"stored_bytes\":" << 8 * C.dense_doubles + (int64_t)C.lr_esz * C.factor_doubles
+      << ",\"factor_bytes_per_entry\":" << C.lr_esz << ",\"eps_aca\":" << C.eps_aca
       << ",\"k_mean\":" << (C.h_rank.empty() ? 0.0 : ksum / C.h_rank.size()) << ",\"k_min\":" << kmin
       << ",\"k_max_seen\":" << kmax << ",\"evals_near\":" << C.evals_near << ",\"evals_aca\":" << C.evals_aca
       << ",\"entries_aca\":" << C.entries_aca << ",\"aca_steps\":" << C.aca_steps << ",\"aca_chunks\":" << C.aca_chunks

@@ -159,9 +159,10 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
 // Three-kernel, host-sync-free variant for ACA rows / columns (nearly all entries are order 3,
 // most of the rest order 4).  The batch size is read on the device (*dtot: the step's row or
 // column total, written by the step's scans), so the host never waits for it:
-//   k_eval_class3   persistent grid-stride pass over the batch: evaluates the order-3 entries
-//                   in place and appends order-4 references to the front of `lists`, all other
-//                   classes to the back (warp-aggregated atomics);
+//   k_eval_class3   persistent pass over the batch (warps take groups of entries from a
+//                   counter): evaluates the order-3 entries in place and appends order-4
+//                   references to the front of `lists`, all other classes to the back
+//                   (warp-aggregated atomics);
 //   k_eval_list<4>  persistent grid-stride over the order-4 list (count read on the device);
 //   k_eval_rest     persistent, the remaining few (orders 5, 6, touching pairs).
 // one 32-entry group of a warp (lanes e = e0 + lane): classify, append non-order-3 entries,
@@ -193,30 +194,26 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
   }
 }
 
-// DYN = false: grid-stride (static) over the batch; DYN = true: every warp takes groups of
-// kDynGroups x 32 entries from the counter cnt[2] (dynamic balance across SMs)
+// Persistent, dynamically balanced: every warp takes groups of kDynGroups x 32 consecutive
+// entries from the counter cnt[2] until the batch is exhausted (a fixed grid-stride split or
+// one thread per entry leave SMs idle at the tail: C4 ACA evaluation 1.85 s resp. 1.75 s vs
+// 1.61 s, profiles/r02_setup_ab1.jsonl)
 constexpr int kDynGroups = 4;
-template <class M, int MINB = 4, bool DYN = false>
-__global__ void __launch_bounds__(128, MINB) k_eval_class3(M m, const int64_t* __restrict__ dtot,
-                                                        EntryRef* __restrict__ lists,
-                                                        unsigned long long* __restrict__ cnt /* [n4, nrest, next] */,
-                                                        unsigned long long* __restrict__ evals) {
+template <class M>
+__global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __restrict__ dtot,
+                                                     EntryRef* __restrict__ lists,
+                                                     unsigned long long* __restrict__ cnt /* [n4, nrest, next] */,
+                                                     unsigned long long* __restrict__ evals) {
   const int64_t total = *dtot;
   const int lane = threadIdx.x & 31;
   unsigned long long ev = 0;
-  if (DYN) {
-    for (;;) {
-      unsigned long long b0 = 0;
-      if (lane == 0) b0 = atomicAdd(&cnt[2], (unsigned long long)(32 * kDynGroups));
-      b0 = __shfl_sync(0xffffffffu, b0, 0);
-      if ((int64_t)b0 >= total) break;
+  for (;;) {
+    unsigned long long b0 = 0;
+    if (lane == 0) b0 = atomicAdd(&cnt[2], (unsigned long long)(32 * kDynGroups));
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if ((int64_t)b0 >= total) break;
 #pragma unroll 1
-      for (int g = 0; g < kDynGroups; ++g) class3_group(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
-    }
-  } else {
-    // the loop bound is uniform per CTA, so every warp runs whole iterations (full-mask ballots)
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x)
-      class3_group(m, base + threadIdx.x, total, lane, lists, cnt, ev);
+    for (int g = 0; g < kDynGroups; ++g) class3_group(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);

@@ -139,7 +139,8 @@ struct VmmPool {
 struct MvTask {
   int32_t rlo;              // first internal row of the leaf (y += ...)
   int32_t xoff;             // stage offset (doubles) of x[clo]
-  int32_t loff;             // stage offset (doubles) of the leaf's storage
+  int32_t loff;             // stage offset of the leaf's storage, in doubles (dense leaves) or in
+                            // factor elements (low-rank leaves: doubles, or floats with lr_f32)
   uint32_t mnk;             // m | n << 11 | k << 22 (k == 0: dense m x n row-major)
 };                          // header record of a batch: {count, 0, 0, 0}
 struct MvSeg {              // one bulk copy: [src, src + bytes) of base -> stage offset dst
@@ -155,7 +156,7 @@ struct MvBatch {
 };
 struct MvLarge {
   int32_t rlo, clo, m, n, k, pad;
-  int64_t off;              // doubles from the factor pool base
+  int64_t off;              // elements (C.lr_esz bytes) from the factor pool base; dense: doubles of the store
   int64_t toff;             // offset into the t buffer
 };
 struct MvTileV { int32_t blk, l, j0, j1; };
@@ -226,8 +227,6 @@ struct Context {
   int k_max = 64, solver = 0, restart = 100, max_iter = 10000;
   int record_pivots = -1;      // -1 auto (N <= 25000), 0 off, 1 on
   double aca_chunk_mb = 32768, aca_kws = 16;
-  int eval_variant = 0;        // diagnostic option "eval_variant": variant of the ACA order-3 kernel
-  int aca_waves = 2;           // diagnostic option "aca_waves": grid of the persistent ACA kernels, in waves
 
   // tree state
   bool have_tree = false, have_setup = false;
@@ -270,7 +269,9 @@ struct Context {
   bool aca_prev_valid = false;   // a previous hm_setup of the same owned block list: its pool size
   int64_t aca_prev_sig[2] = {0, 0};
   double aca_prev_bytes = 0, aca_prev_eps = -1;
-  int aca_prev_kmax = 0;
+  int aca_prev_kmax = 0, aca_prev_esz = 0;
+  int lr_f32 = 0;              // option "lr_f32": store the ACA factors U, V in binary32 (dense blocks stay FP64)
+  int lr_esz = 8;              // bytes per stored factor entry of the current setup (8, or 4 with lr_f32)
 
   // matvec plan (matvec.cu)
   DBuf<MvBatch> mv_batches;

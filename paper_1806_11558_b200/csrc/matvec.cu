@@ -150,11 +150,12 @@ __device__ __forceinline__ void warp_allreduce_vec(double (&a)[KB], int lane) {
 // Low-rank block U (m x k) | V (n x k), column-major, columns [l0, l0 + kc) (kc <= KB), out of
 // shared memory: t = V^T x with all kc column sums in registers, one vector all-reduce over
 // the warp, then y += U t (one FP64 atomic per row).
-template <int KB>
-__device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int m, int n, int k, int l0, int kc,
+// T = float: binary32 factors (option lr_f32), widened exactly to FP64 before every FMA.
+template <int KB, class T>
+__device__ __forceinline__ void lowrank_block(const T* __restrict__ U0, int m, int n, int k, int l0, int kc,
                                               const double* __restrict__ xs, double* __restrict__ y, int lane) {
-  const double* V = U0 + m * k + l0 * n;
-  const double* U = U0 + l0 * m;
+  const T* V = U0 + m * k + l0 * n;
+  const T* U = U0 + l0 * m;
   double acc[KB];
 #pragma unroll
   for (int l = 0; l < KB; ++l) acc[l] = 0.0;
@@ -163,22 +164,22 @@ __device__ __forceinline__ void lowrank_block(const double* __restrict__ U0, int
     const double xj = xs[j];
 #pragma unroll
     for (int l = 0; l < KB; ++l)
-      if (l < kc) acc[l] = __fma_rn(V[j + l * n], xj, acc[l]);
+      if (l < kc) acc[l] = __fma_rn((double)V[j + l * n], xj, acc[l]);
   }
   warp_allreduce_vec<KB>(acc, lane);
   for (int t = lane; t < m; t += 32) {
     double s0 = 0.0, s1 = 0.0;                  // two chains: half the dependent-FMA latency
 #pragma unroll
     for (int l = 0; l < KB; l += 2) {
-      if (l < kc) s0 = __fma_rn(U[t + l * m], acc[l], s0);
-      if (l + 1 < kc) s1 = __fma_rn(U[t + (l + 1) * m], acc[l + 1], s1);
+      if (l < kc) s0 = __fma_rn((double)U[t + l * m], acc[l], s0);
+      if (l + 1 < kc) s1 = __fma_rn((double)U[t + (l + 1) * m], acc[l + 1], s1);
     }
     atomicAdd(y + t, s0 + s1);
   }
 }
 
-__device__ __forceinline__ void lowrank_any(const double* U, int m, int n, int k, const double* xs, double* y,
-                                            int lane) {
+template <class T>
+__device__ __forceinline__ void lowrank_any(const T* U, int m, int n, int k, const double* xs, double* y, int lane) {
   if (k <= 8) lowrank_block<8>(U, m, n, k, 0, k, xs, y, lane);
   else if (k <= 16) lowrank_block<16>(U, m, n, k, 0, k, xs, y, lane);
   else
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                  const int32_t* __restrict__ cta_first,
                  const char* __restrict__ base0, const char* __restrict__ base1, const char* __restrict__ base2,
                  const double* __restrict__ x, double* __restrict__ y, int64_t scramble_n,
-                 unsigned long long* __restrict__ prof) {
+                 unsigned long long* __restrict__ prof, int lr32) {
   constexpr int NW = THREADS / 32, NC = NW - 1;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -294,6 +295,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
       // measure same-address atomic contention
       const int64_t r0 = scramble_n > 0 ? ((int64_t)T.x * 2654435761ll) % scramble_n : T.x;
       if (k == 0) dense_any(sd + T.z, m, n, sd + T.y, y + r0, lane);
+      else if (lr32) lowrank_any(reinterpret_cast<const float*>(sb) + T.z, m, n, k, sd + T.y, y + r0, lane);
       else lowrank_any(sd + T.z, m, n, k, sd + T.y, y + r0, lane);
     }
     __syncwarp();
@@ -329,8 +331,9 @@ __device__ __forceinline__ void warp_reduce_halving(double (&v)[KB], int lane) {
   for (int o = 16 >> LV; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
 }
 
+template <class E>
 __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
-                                                      const MvLarge* __restrict__ L, const double* __restrict__ pool,
+                                                      const MvLarge* __restrict__ L, const E* __restrict__ pool,
                                                       const double* __restrict__ x, double* __restrict__ tbuf) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ 
     const MvTileV T = tiles[i];
     const MvLarge B = L[T.blk];
     const int kc = min(16, B.k - T.l);
-    const double* V = pool + B.off + (int64_t)B.m * B.k + (int64_t)T.l * B.n;
+    const E* V = pool + B.off + (int64_t)B.m * B.k + (int64_t)T.l * B.n;
     const double* xs = x + B.clo;
     double acc[16];
 #pragma unroll
@@ -350,8 +353,8 @@ __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ 
       double va[16], vb[16];
 #pragma unroll
       for (int l = 0; l < 16; ++l) {
-        va[l] = l < kc ? __ldg(V + j + (int64_t)l * B.n) : 0.0;
-        vb[l] = (l < kc && two) ? __ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
+        va[l] = l < kc ? (double)__ldg(V + j + (int64_t)l * B.n) : 0.0;
+        vb[l] = (l < kc && two) ? (double)__ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
       }
 #pragma unroll
       for (int l = 0; l < 16; ++l) acc[l] = __fma_rn(vb[l], xb, __fma_rn(va[l], xa, acc[l]));
@@ -365,8 +368,9 @@ __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ 
 
 // Phase 2, tile = (block, 256 rows t0..): y[rlo + t] += sum_l U[t, l] t_l; each lane keeps its
 // 8 rows of the tile in registers: per column l one broadcast t_l and 8 independent loads of U.
+template <class E>
 __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ tiles, int64_t ntiles,
-                                                     const MvLarge* __restrict__ L, const double* __restrict__ pool,
+                                                     const MvLarge* __restrict__ L, const E* __restrict__ pool,
                                                      const double* __restrict__ tbuf, double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ 
   for (int64_t i = w0; i < ntiles; i += nw) {
     const MvTileU T = tiles[i];
     const MvLarge B = L[T.blk];
-    const double* U = pool + B.off + T.t0 + lane;
+    const E* U = pool + B.off + T.t0 + lane;
     const double* tl = tbuf + B.toff;
     const int rows = T.t1 - T.t0;
     double acc[8];
@@ -383,24 +387,24 @@ __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ 
     int l = 0;
     for (; l + 1 < B.k; l += 2) {
       const double ta = __ldg(tl + l), tb = __ldg(tl + l + 1);
-      const double* Ua = U + (int64_t)l * B.m;
-      const double* Ub = Ua + B.m;
+      const E* Ua = U + (int64_t)l * B.m;
+      const E* Ub = Ua + B.m;
       double ua[8], ub[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const bool ok = lane + 32 * q < rows;
-        ua[q] = ok ? __ldg(Ua + 32 * q) : 0.0;
-        ub[q] = ok ? __ldg(Ub + 32 * q) : 0.0;
+        ua[q] = ok ? (double)__ldg(Ua + 32 * q) : 0.0;
+        ub[q] = ok ? (double)__ldg(Ub + 32 * q) : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = __fma_rn(ub[q], tb, __fma_rn(ua[q], ta, acc[q]));
     }
     if (l < B.k) {
       const double ta = __ldg(tl + l);
-      const double* Ua = U + (int64_t)l * B.m;
+      const E* Ua = U + (int64_t)l * B.m;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        if (lane + 32 * q < rows) acc[q] = __fma_rn(__ldg(Ua + 32 * q), ta, acc[q]);
+        if (lane + 32 * q < rows) acc[q] = __fma_rn((double)__ldg(Ua + 32 * q), ta, acc[q]);
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q)
@@ -427,6 +431,7 @@ namespace {
 struct Item { int64_t byte0, bytes; int base; int32_t rlo, clo, n; uint32_t mnk; };
 // one planner thread's output over a contiguous slice of the item sequence
 struct PlanPart {
+  int lr_esz = 8;                      // bytes per factor entry (task offsets of low-rank items)
   std::vector<MvBatch> batches;
   std::vector<MvSeg> segs;
   std::vector<MvTask> stream;
@@ -506,7 +511,7 @@ struct PlanPart {
         MvTask t;
         t.rlo = it.rlo;
         t.xoff = (int32_t)((xoff[item_x[c]] + 8 * (it.clo - X.a0)) / 8);
-        t.loff = (int32_t)((roff[item_run[c]] + (it.byte0 - R.a0)) / 8);
+        t.loff = (int32_t)((roff[item_run[c]] + (it.byte0 - R.a0)) / (it.base == 1 ? lr_esz : 8));
         t.mnk = it.mnk;
         stream.push_back(t);
       }
@@ -559,14 +564,15 @@ void plan_dense_part(Context& C, PlanWs& W, PlanPart& P, int64_t i0, int64_t i1)
 void plan_lowrank_part(Context& C, PlanWs& W, PlanPart& P, int64_t i0, int64_t i1) {
   P.clear();
   P.items.reserve(i1 - i0);
-  const int64_t cap = kMvStageBytes;
+  P.lr_esz = C.lr_esz;
+  const int64_t cap = kMvStageBytes, esz = C.lr_esz;
   for (int64_t i = i0; i < i1; ++i) {
     const int64_t b = W.lr_order[i];
     const Quad& q = C.h_adm[C.adm_begin + b];
     const int m = q.rhi - q.rlo, n = q.chi - q.clo, k = C.h_rank[b];
-    const int64_t bytes = 8 * (int64_t)k * (m + n);
+    const int64_t bytes = esz * (int64_t)k * (m + n);
     if (bytes <= std::min<int64_t>(C.mv_small_max, cap - 8 * n - 64) && m <= 2047 && n <= 2047 && k <= 1023)
-      P.items.push_back(Item{8 * C.h_foff[b], bytes, 1, q.rlo, q.clo, n,
+      P.items.push_back(Item{esz * C.h_foff[b], bytes, 1, q.rlo, q.clo, n,
                              (uint32_t)m | ((uint32_t)n << 11) | ((uint32_t)k << 22)});
     else
       P.large.push_back(MvLarge{q.rlo, q.clo, m, n, k, 0, C.h_foff[b], 0});
@@ -792,6 +798,22 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
   HM_CUDA(cudaMemsetAsync(y_int, 0, C.N * sizeof(double), st));
   if (C.mv_tlen) HM_CUDA(cudaMemsetAsync(C.mv_tbuf.get(), 0, C.mv_tlen * sizeof(double), st));
   const double* pool = (const double*)C.fpool.base;
+  const float* pool32 = (const float*)C.fpool.base;     // option lr_f32
+  const bool f32 = C.lr_esz == 4;
+  auto large_v = [&](cudaStream_t s) {
+    if (f32) k_mv_large_v<float><<<148 * 8, 256, 0, s>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool32,
+                                                          x_int, C.mv_tbuf.get());
+    else k_mv_large_v<double><<<148 * 8, 256, 0, s>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool,
+                                                       x_int, C.mv_tbuf.get());
+    HM_CHECK_LAUNCH();
+  };
+  auto large_u = [&](cudaStream_t s) {
+    if (f32) k_mv_large_u<float><<<148 * 8, 256, 0, s>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool32,
+                                                          C.mv_tbuf.get(), y_int);
+    else k_mv_large_u<double><<<148 * 8, 256, 0, s>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
+                                                       C.mv_tbuf.get(), y_int);
+    HM_CHECK_LAUNCH();
+  };
   // option mv_concurrent (default on): the large low-rank blocks (V^T x, then U z) stream on
   // a side stream while the CTA rings stream the small blocks, so one kernel family's tail
   // overlaps the other's streaming (C4: 27.9 -> 27.6 ms)
@@ -804,12 +826,8 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
     }
     HM_CUDA(cudaEventRecord(C.mv_ev[0], st));
     HM_CUDA(cudaStreamWaitEvent(C.mv_side, C.mv_ev[0], 0));
-    k_mv_large_v<<<148 * 8, 256, 0, C.mv_side>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
-                                                 C.mv_tbuf.get());
-    HM_CHECK_LAUNCH();
-    k_mv_large_u<<<148 * 8, 256, 0, C.mv_side>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
-                                                 C.mv_tbuf.get(), y_int);
-    HM_CHECK_LAUNCH();
+    large_v(C.mv_side);
+    large_u(C.mv_side);
     HM_CUDA(cudaEventRecord(C.mv_ev[1], C.mv_side));
   }
   if (C.mv_nbatches) {
@@ -818,11 +836,11 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
     if (C.mv_kind == 0)      // two CTA rings per SM, 2 x 48 KiB stages, 7 consumer warps each
       k_mv_batched<2, kMvStageBytes, 256, 2><<<C.mv_grid, 256, 256 + 2 * kMvStageBytes, st>>>(
           C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof);
+          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
     else                     // one CTA ring per SM, 4 x 48 KiB stages, 15 consumer warps
       k_mv_batched<4, kMvStageBytes, 512, 1><<<C.mv_grid, 512, 256 + 4 * kMvStageBytes, st>>>(
           C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
-          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof);
+          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
     HM_CHECK_LAUNCH();
   }
   if (C.mv_n_dense_big) {
@@ -833,12 +851,8 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
   if (conc) {
     HM_CUDA(cudaStreamWaitEvent(st, C.mv_ev[1], 0));
   } else if (C.mv_n_tiles_v) {
-    k_mv_large_v<<<148 * 8, 256, 0, st>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool, x_int,
-                                          C.mv_tbuf.get());
-    HM_CHECK_LAUNCH();
-    k_mv_large_u<<<148 * 8, 256, 0, st>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
-                                          C.mv_tbuf.get(), y_int);
-    HM_CHECK_LAUNCH();
+    large_v(st);
+    large_u(st);
   }
   ks.reset();
   if (C.world > 1 && reduce) allreduce_sum(C, y_int, C.N);

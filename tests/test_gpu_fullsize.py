@@ -138,4 +138,49 @@ def test_nu64_solution_vs_oracle(O, torch_cuda):
     assert st == 0 and rro <= 1e-9 and rr <= 1e-9
     d = np.linalg.norm(sol.cpu().numpy() - xo) / np.linalg.norm(xo)
     assert d <= 1e-5, d
+    # SURVEY §8(f)-4, reduced-traffic matvec: the same H with the ACA factors stored in binary32
+    # (option lr_f32; dense blocks stay FP64) against the oracle's FP64 solution
+    x = seeded_vector(T.shape[0], 0)
+    y64 = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    H.set_option("lr_f32", 1)
+    H.setup(EPS)
+    assert H.stats()["factor_bytes_per_entry"] == 4
+    y32 = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.linalg.norm(y32 - y64) <= 1e-6 * np.linalg.norm(y64)       # binary32 rounding of U, V only
+    sol32, it32, rr32 = H.solve(torch.from_numpy(f).cuda(), tol=1e-10)
+    d32 = np.linalg.norm(sol32.cpu().numpy() - xo) / np.linalg.norm(xo)
+    assert rr32 <= 1e-9 and d32 <= 1e-5, d32
     H.close()
+
+
+def test_lr_f32_c2_matvec_and_solution(O, torch_cuda):
+    """Option lr_f32 at configs[1]: H-matvec within 10 eps_aca of the exact Galerkin rows, the
+    factors equal to the FP64 run's rounded to binary32, GMRES solution within 1e-5 of the
+    oracle's (FP64) solution."""
+    import torch
+    V, T = icosphere(5)
+    N = T.shape[0]
+    H = _gpu(V, T, lr_f32=1)
+    H.setup(EPS)
+    G = _gpu(V, T)
+    G.setup(EPS)
+    adm, _ = H.leaves(0)
+    for b in range(0, len(adm), 97):
+        mm, nn = adm[b][1] - adm[b][0], adm[b][3] - adm[b][2]
+        U1, W1 = H.lowrank(b, mm, nn)
+        U0, W0 = G.lowrank(b, mm, nn)
+        assert np.array_equal(U1, U0.astype(np.float32).astype(np.float64))
+        assert np.array_equal(W1, W0.astype(np.float32).astype(np.float64))
+    R = O.Problem(V, T)
+    rows = np.random.default_rng(7).permutation(N)[:256]
+    Arows = R.dense_rows(rows)
+    for x in (np.ones(N), seeded_vector(N, 1)):
+        yg = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        ye = Arows @ x
+        assert np.linalg.norm(yg[rows] - ye) <= 10 * EPS * np.linalg.norm(ye)
+    R.assemble(EPS)
+    f = R.rhs(1)
+    sol, it, rr = H.solve(torch.from_numpy(f).cuda(), tol=1e-10)
+    xo = R.gmres(f, tol=1e-10)[0]
+    assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-5 * np.linalg.norm(xo)
+    H.close(); G.close()
