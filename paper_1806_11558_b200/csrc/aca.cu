@@ -30,7 +30,7 @@ struct AcaBlk {
 struct AcaState {
   int32_t i, k, js, status;   // status: 0 active, 1 done, 2 workspace overflow
   int32_t skip, pad0;
-  double S2, vv, pv;          // ||S_k||_F^2, ||v_k||^2, pivot value r_js of the current step
+  double S2, vv;
 };
 
 struct AcaWork {
@@ -46,7 +46,6 @@ struct AcaWork {
   DBuf<int32_t> ovf;
   DBuf<unsigned long long> novf;
   DBuf<int32_t> bad;    // smallest owned block index with a non-finite factor entry (INT_MAX: none)
-  DBuf<double> facc;    // per block 2 kws cross sums of the current step: [V_l^T r (row step) | U_l^T u (column step)]
   PinnedVec<int64_t> h_tot;
   PinnedVec<AcaBlk> h_blk;
   PinnedVec<int32_t> h_idsp;
@@ -96,29 +95,6 @@ __global__ void k_step_totals(const int64_t* __restrict__ rpre, const int64_t* _
   tot[2] = pos[nb];
 }
 
-// Sum 16 per-lane values over the warp by recursive halving (16 shuffles instead of 16 x 5):
-// on return a[0] of lane L holds the warp total of value index acc_reduce16_index(L) =
-// 8*bit4(L) + 4*bit3(L) + 2*bit2(L) + bit1(L)  (two lanes per index).
-__device__ __forceinline__ void acc_reduce16(double (&a)[16], int lane) {
-#pragma unroll
-  for (int lvl = 0; lvl < 4; ++lvl) {
-    const int o = 16 >> lvl, half = 8 >> lvl;
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (i < half) {
-        const double send = up ? a[i] : a[i + half];
-        const double keep = up ? a[i + half] : a[i];
-        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
-  }
-  a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
-}
-__device__ __forceinline__ int acc_reduce16_index(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-}
-
 // Residual row (ROW) or column entries of the active blocks of a chunk, as a batch mapping
 // for entry_batch.cuh.  put() applies the rank-one corrections of the previous k steps in
 // ascending l, each product and difference separately rounded (A15), and stores the residual
@@ -153,7 +129,7 @@ struct AcaMap {
     s = ROW ? b.q.rlo + st.i : b.q.rlo + r.idx;
     t = ROW ? b.q.clo + r.idx : b.q.clo + st.js;
   }
-  __device__ double put(EntryRef r, double a) const {
+  __device__ void put(EntryRef r, double a) const {
     const AcaBlk& b = B[r.seg];
     const AcaState st = S[r.seg];
     const double* U = Uw + b.uoff;
@@ -164,52 +140,6 @@ struct AcaMap {
     } else {
       for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[r.idx + (int64_t)l * b.m], V[st.js + (int64_t)l * b.n]));
       Uw[b.uoff + (int64_t)st.k * b.m + r.idx] = a;
-    }
-    return a;
-  }
-  // L1 prefetch of what the entry 32 positions further along the same residual row / column
-  // will load (its panel's cache line and its k correction operands): the next group of a
-  // warp in k_eval_class3, so its loads overlap this group's quadrature
-  __device__ void prefetch_next(EntryRef r) const {
-    const AcaBlk& b = B[r.seg];
-    const int len = ROW ? b.n : b.m;
-    const int nx = r.idx + 32;
-    if (nx >= len) return;
-    const int pidx = ROW ? b.q.clo + nx : b.q.rlo + nx;
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(P + pidx));
-    const int k = S[r.seg].k;
-    const double* w = ROW ? Vw + b.voff + nx : Uw + b.uoff + nx;
-    const int64_t ld = ROW ? b.n : b.m;
-    for (int l = 0; l < k; ++l) asm volatile("prefetch.global.L1 [%0];" ::"l"(w + l * ld));
-  }
-  // Cross sums of the Frobenius update (A11), accumulated while the residual's operands are
-  // still in L1: row step V_l^T r (= r_js V_l^T v), column step U_l^T u, l < k, per block into
-  // facc.  Warp-collective: the lanes holding entries of one block reduce their k products by
-  // recursive halving (16 values per pass), one atomic per value per block and warp.  These
-  // sums feed the stop test only (A15: norms may be reduced in any order).
-  double* facc;
-  int kws;
-  __device__ void cross(EntryRef r, bool valid, double res, int lane) const {
-    unsigned todo = __ballot_sync(0xffffffffu, valid);
-    while (todo) {
-      const int leader = __ffs(todo) - 1;
-      const int c0 = __shfl_sync(0xffffffffu, r.seg, leader);
-      const bool mine = valid && r.seg == c0;
-      todo &= ~__ballot_sync(0xffffffffu, mine);
-      const AcaBlk& b = B[c0];
-      const int k = S[c0].k;
-      const double* src = ROW ? Vw + b.voff : Uw + b.uoff;
-      const int64_t ld = ROW ? b.n : b.m;
-      double* dst = facc + (int64_t)c0 * 2 * kws + (ROW ? 0 : kws);
-      for (int l0 = 0; l0 < k; l0 += 16) {
-        double p[16];
-#pragma unroll
-        for (int l = 0; l < 16; ++l)
-          p[l] = (mine && l0 + l < k) ? dmul(src[r.idx + (int64_t)(l0 + l) * ld], res) : 0.0;
-        acc_reduce16(p, lane);
-        const int idx = acc_reduce16_index(lane);
-        if ((lane & 1) == 0 && l0 + idx < k) atomicAdd(dst + l0 + idx, p[0]);
-      }
     }
   }
 };
@@ -249,8 +179,7 @@ __device__ int first_unused(const uint32_t* bm, int m, int lane) {
 constexpr int kBigMN = 2048;
 
 __device__ __forceinline__ void aca_pivot_block(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, int64_t c,
-                                                double* __restrict__ Vw, uint32_t* __restrict__ bmap, int lane,
-                                                double* __restrict__ facc, int kws) {
+                                                double* __restrict__ Vw, uint32_t* __restrict__ bmap, int lane) {
   AcaState st = S[c];
   if (st.status != 0) return;
   const AcaBlk b = B[c];
@@ -270,7 +199,6 @@ __device__ __forceinline__ void aca_pivot_block(const AcaBlk* __restrict__ B, Ac
   const double piv = r[bj];
   if (piv == 0.0) {                                     // zero residual row: next unused row
     int nx = first_unused(bm, b.m, lane);
-    for (int l = lane; l < st.k; l += 32) facc[c * 2 * kws + l] = 0.0;   // this row's cross sums
     if (lane == 0) {
       if (nx < 0) st.status = 1;
       else { st.i = nx; st.skip = 1; }
@@ -288,35 +216,26 @@ __device__ __forceinline__ void aca_pivot_block(const AcaBlk* __restrict__ B, Ac
   if (lane == 0) {
     st.js = bj;
     st.vv = vv;
-    st.pv = piv;
     st.skip = 0;
     S[c] = st;
   }
 }
 
 
-// next active block of a persistent warp (dynamic: counter *ctr, reset to 0 before the launch)
-__device__ __forceinline__ int64_t next_block(unsigned long long* ctr, int lane) {
-  unsigned long long a = 0;
-  if (lane == 0) a = atomicAdd(ctr, 1ull);
-  return (int64_t)__shfl_sync(0xffffffffu, a, 0);
-}
-
-// one warp per active block, persistent and dynamically balanced over the step's active count
-// *dnact (device)
+// one warp per active block; the step's active count *dnact is read on the device, the grid
+// covers an upper bound of it known to the host (the count read back kLag steps earlier: the
+// active set only shrinks)
 __global__ void k_aca_pivot(const AcaBlk* __restrict__ B, AcaState* __restrict__ S, const int32_t* __restrict__ act,
-                            const int64_t* __restrict__ dnact, double* __restrict__ Vw, uint32_t* __restrict__ bmap,
-                            unsigned long long* __restrict__ ctr, double* __restrict__ facc, int kws) {
-  const int64_t nact = *dnact;
-  const int lane = threadIdx.x & 31;
-  for (int64_t a = next_block(ctr, lane); a < nact; a = next_block(ctr, lane))
-    aca_pivot_block(B, S, act[a], Vw, bmap, lane, facc, kws);
+                            const int64_t* __restrict__ dnact, double* __restrict__ Vw, uint32_t* __restrict__ bmap) {
+  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (a >= *dnact) return;
+  aca_pivot_block(B, S, act[a], Vw, bmap, threadIdx.x & 31);
 }
 
 // k_aca_pivot for the big blocks of the chunk (m + n >= kBigMN): one CTA per block
 __global__ void __launch_bounds__(256) k_aca_pivot_big(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
                                                        const int32_t* __restrict__ big, double* __restrict__ Vw,
-                                                       uint32_t* __restrict__ bmap, double* __restrict__ facc, int kws) {
+                                                       uint32_t* __restrict__ bmap) {
   __shared__ double sbest[8];
   __shared__ int sidx[8];
   const int64_t c = big[blockIdx.x];
@@ -342,7 +261,6 @@ __global__ void __launch_bounds__(256) k_aca_pivot_big(const AcaBlk* __restrict_
   __syncthreads();
   const double piv = r[bj];
   if (piv == 0.0) {                                            // zero residual row: next unused row
-    for (int l = threadIdx.x; l < st.k; l += 256) facc[c * 2 * kws + l] = 0.0;   // this row's cross sums
     if (w == 0) {
       const int nx = first_unused(bm, b.m, lane);
       if (lane == 0) {
@@ -368,46 +286,98 @@ __global__ void __launch_bounds__(256) k_aca_pivot_big(const AcaBlk* __restrict_
     for (int g = 0; g < 8; ++g) vv += sbest[g];
     st.js = bj;
     st.vv = vv;
-    st.pv = piv;
     st.skip = 0;
     S[c] = st;
   }
 }
 
+// Sum 16 per-lane values over the warp by recursive halving (16 shuffles instead of 16 x 5):
+// on return a[0] of lane L holds the warp total of value index
+// 8*bit4(L) + 4*bit3(L) + 2*bit2(L) + bit1(L)  (two lanes per index).
+__device__ __forceinline__ void warp_reduce16(double (&a)[16], int lane) {
+#pragma unroll
+  for (int lvl = 0; lvl < 4; ++lvl) {
+    const int o = 16 >> lvl, half = 8 >> lvl;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < half) {
+        const double send = up ? a[i] : a[i + half];
+        const double keep = up ? a[i + half] : a[i];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+  }
+  a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+}
+__device__ __forceinline__ int reduce16_index(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
 // Frobenius update of step k (A11): S2 += 2 sum_l (u^T U_l)(V_l^T v) + |u|^2 |v|^2, the stop
 // test, and the next row pivot.  A group of G warps works on one block (G = 1 for most
-// blocks, G = 8 for blocks with m + n >= kBigMN).  The cross sums U_l^T u and V_l^T r were
-// accumulated by the evaluation kernels of this step (AcaMap::cross, facc: V_l^T v = V_l^T r /
-// r_js), so only u itself is read here: |u|^2 and the next-row argmax.  Norms feed the stop
-// test only (A15: tree-reduced on the GPU).
+// blocks, G = 8 for blocks with m + n >= kBigMN); the cross products are formed 8 columns per
+// pass with the 8 (u^T U_l) and 8 (V_l^T v) partial sums in registers (u_t / v_j loaded once
+// per pass, 8 independent loads in flight) and reduced together by one recursive-halving
+// butterfly.  Norms feed the stop test only (A15: tree-reduced on the GPU).
+
 template <int G>
 __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, const double* __restrict__ Uw,
-                                                 const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv,
-                                                 double* __restrict__ facc, int64_t c, int kws, double eps, int gw,
-                                                 int lane, double* red /* smem [G][2] + [G] ints (G > 1) */) {
-  const double* u = Uw + b.uoff + (int64_t)st.k * b.m;
+                                                 const double* __restrict__ Vw, const uint32_t* __restrict__ bmap,
+                                                 int32_t* __restrict__ piv, int64_t c, int kws, double eps, int gw,
+                                                 int lane, double* red /* smem [G][17] (G > 1) */) {
+  const double* U = Uw + b.uoff;
+  const double* V = Vw + b.voff;
+  const double* u = U + (int64_t)st.k * b.m;
+  const double* v = V + (int64_t)st.k * b.n;
   const int t0 = gw * 32 + lane, stride = G * 32;
-  double uu = 0.0, cr = 0.0;
-  for (int t = t0; t < b.m; t += stride) {
-    const double ut = u[t];
-    uu = fma(ut, ut, uu);
-  }
-  double* fa = facc + c * 2 * kws;
-  for (int l = t0; l < st.k; l += stride) {
-    cr = fma(fa[kws + l], fa[l], cr);
-    fa[l] = 0.0;                                        // ready for the next step's sums
-    fa[kws + l] = 0.0;
+  double uu = 0.0;   // ||u_k||^2, accumulated in the first pass over u (one pass also when k = 0)
+  double cross = 0.0;
+  for (int l0 = 0; l0 < max(st.k, 1); l0 += 8) {
+    const int kc = min(8, st.k - l0);
+    double acc[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) acc[l] = 0.0;
+    for (int t = t0; t < b.m; t += stride) {
+      const double ut = u[t];
+      if (l0 == 0) uu = fma(ut, ut, uu);
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < kc) acc[l] = fma(ut, U[t + (int64_t)(l0 + l) * b.m], acc[l]);
+    }
+    if (kc <= 0) break;
+    for (int j = t0; j < b.n; j += stride) {
+      const double vj = v[j];
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < kc) acc[8 + l] = fma(V[j + (int64_t)(l0 + l) * b.n], vj, acc[8 + l]);
+    }
+    warp_reduce16(acc, lane);   // lane L: total of index reduce16_index(L); du_l at bit4 = 0, dv_l at L ^ 16
+    if (G > 1) {
+      if ((lane & 1) == 0) red[gw * 17 + reduce16_index(lane)] = acc[0];
+      __syncthreads();
+      double tsum = 0.0;
+      if (lane < 16)
+        for (int g = 0; g < G; ++g) tsum += red[g * 17 + lane];
+      const double other = __shfl_down_sync(0xffffffffu, tsum, 8);
+      const double part = (lane < 8 && lane < kc) ? tsum * other : 0.0;
+      cross += warp_sum(part);
+      __syncthreads();
+    } else {
+      const double other = __shfl_xor_sync(0xffffffffu, acc[0], 16);
+      const int idx = reduce16_index(lane);
+      const double part = ((lane & 17) == 0 && idx < kc) ? acc[0] * other : 0.0;
+      cross += warp_sum(part);
+    }
   }
   uu = warp_sum(uu);
-  cr = warp_sum(cr);
   if (G > 1) {
-    if (lane == 0) { red[2 * gw] = uu; red[2 * gw + 1] = cr; }
+    if (lane == 0) red[gw * 17 + 16] = uu;
     __syncthreads();
-    uu = 0.0; cr = 0.0;
-    for (int g = 0; g < G; ++g) { uu += red[2 * g]; cr += red[2 * g + 1]; }
+    uu = 0.0;
+    for (int g = 0; g < G; ++g) uu += red[g * 17 + 16];
     __syncthreads();
   }
-  const double cross = st.k > 0 ? cr / st.pv : 0.0;
   st.S2 = (st.S2 + 2.0 * cross) + uu * st.vv;
   if (gw == 0 && lane == 0) {
     piv[c * 2 * kws + 2 * st.k] = st.i;
@@ -428,12 +398,12 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
     }
     warp_argmax(best, bt);
     if (G > 1) {
-      int* ri = reinterpret_cast<int*>(red + 2 * G);
-      if (lane == 0) { red[2 * gw] = best; ri[gw] = bt; }
+      int* ri = reinterpret_cast<int*>(red + G * 17);
+      if (lane == 0) { red[gw * 17] = best; ri[gw] = bt; }
       __syncthreads();
       best = red[0]; bt = ri[0];
       for (int g = 1; g < G; ++g) {
-        const double ob = red[2 * g];
+        const double ob = red[g * 17];
         const int oi = ri[g];
         if (ob > best || (ob == best && oi < bt)) { best = ob; bt = oi; }
       }
@@ -444,36 +414,35 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
 }
 
 // G = 1: one warp per active block (small blocks; big ones are skipped), act[] = compact list;
-// persistent and dynamically balanced over the step's active count *dnact (device)
+// the active count *dnact is read on the device (grid: a host-side upper bound, see k_aca_pivot)
 __global__ void __launch_bounds__(64, 16) k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
                                                     const int32_t* __restrict__ act, const int64_t* __restrict__ dnact,
-                                                    const double* __restrict__ Uw, double* __restrict__ facc,
+                                                    const double* __restrict__ Uw, const double* __restrict__ Vw,
                                                     const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv,
-                                                    int kws, double eps, unsigned long long* __restrict__ ctr) {
-  const int64_t nact = *dnact;
+                                                    int kws, double eps) {
+  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  for (int64_t a = next_block(ctr, lane); a < nact; a = next_block(ctr, lane)) {
-    const int64_t c = act[a];
-    AcaState st = S[c];
-    const AcaBlk b = B[c];
-    if (st.status != 0 || st.skip) continue;
-    if (b.m + b.n >= kBigMN) continue;
-    aca_update_block<1>(b, st, Uw, bmap, piv, facc, c, kws, eps, 0, lane, nullptr);
-    if (lane == 0) S[c] = st;
-  }
+  if (a >= *dnact) return;
+  const int64_t c = act[a];
+  AcaState st = S[c];
+  const AcaBlk b = B[c];
+  if (st.status != 0 || st.skip) return;
+  if (b.m + b.n >= kBigMN) return;
+  aca_update_block<1>(b, st, Uw, Vw, bmap, piv, c, kws, eps, 0, lane, nullptr);
+  if (lane == 0) S[c] = st;
 }
 
 // G = 8: one CTA per big block of the chunk (list fixed per chunk; finished blocks return)
 __global__ void __launch_bounds__(256, 4) k_aca_update_big(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
                                                         const int32_t* __restrict__ big, const double* __restrict__ Uw,
-                                                        double* __restrict__ facc, const uint32_t* __restrict__ bmap,
+                                                        const double* __restrict__ Vw, const uint32_t* __restrict__ bmap,
                                                         int32_t* __restrict__ piv, int kws, double eps) {
-  __shared__ double red[2 * 8 + 8];
+  __shared__ double red[8 * 17 + 8];
   const int64_t c = big[blockIdx.x];
   AcaState st = S[c];
   if (st.status != 0 || st.skip) return;
   const AcaBlk b = B[c];
-  aca_update_block<8>(b, st, Uw, bmap, piv, facc, c, kws, eps, threadIdx.x >> 5, threadIdx.x & 31, red);
+  aca_update_block<8>(b, st, Uw, Vw, bmap, piv, c, kws, eps, threadIdx.x >> 5, threadIdx.x & 31, red);
   if (threadIdx.x == 0) S[c] = st;
 }
 
@@ -481,7 +450,7 @@ __global__ void k_init_state(AcaState* __restrict__ S, int64_t nb) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nb) return;
   AcaState s;
-  s.i = 0; s.k = 0; s.js = 0; s.status = 0; s.skip = 0; s.pad0 = 0; s.S2 = 0.0; s.vv = 0.0; s.pv = 0.0;
+  s.i = 0; s.k = 0; s.js = 0; s.status = 0; s.skip = 0; s.pad0 = 0; s.S2 = 0.0; s.vv = 0.0;
   S[c] = s;
 }
 
@@ -544,8 +513,7 @@ void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWor
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 3 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4);   // one wave, persistent
-  if (C.aca_prefetch) k_eval_class3<M, true><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
-  else k_eval_class3<M, false><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
+  k_eval_class3<M><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
   const unsigned g4 = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 16);
   k_eval_list<4, M><<<g4, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
@@ -598,8 +566,6 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   std::memcpy(W.h_idsp.data(), ids.data(), nb * sizeof(int32_t));
   HM_CUDA(cudaMemcpyAsync(W.owned.get(), W.h_idsp.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   HM_CUDA(cudaMemsetAsync(W.bmap.get(), 0, bo * sizeof(uint32_t), st));
-  W.facc.alloc(nb * 2 * kws);
-  HM_CUDA(cudaMemsetAsync(W.facc.get(), 0, nb * 2 * kws * sizeof(double), st));
   k_init_state<<<grid_for(nb, 256), 256, 0, st>>>(W.state.get(), nb);
   HM_CHECK_LAUNCH();
   const Panel* P = C.panel.get();
@@ -616,15 +582,14 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   W.lists.alloc(std::max(rmax, cmax));
   W.rtab.alloc(rmax / 32 + 2);
   W.ctab.alloc(cmax / 32 + 2);
-  W.cnt.alloc(5);                 // [n4, nrest, next entry group | pivot, update block counters]
+  W.cnt.alloc(3);                 // [n4, nrest, next entry group]
   W.h_ring.resize(3 * (kLag + 1));
   for (auto& e : W.ring_ev)
     if (!e) HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const int64_t* drow = W.tot.get();          // tot[0]: row entries, tot[1]: column entries, tot[2]: active blocks
   const int64_t* dcol = W.tot.get() + 1;
   const int64_t* dnact = W.tot.get() + 2;
-  const unsigned gpiv = (unsigned)std::min<int64_t>(grid_for(nb * 32, 256), 148 * 8);   // one wave each
-  const unsigned gupd = (unsigned)std::min<int64_t>(grid_for(nb * 32, 64), 148 * 16);
+  int64_t nact_ub = nb;              // upper bound of the active count of every step still to be enqueued
   for (int step = 0;; ++step) {
     std::unique_ptr<KScope> ks(new KScope(C, KF_ACA_OTHER));
     k_step_flags<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.state.get(), nb, W.flag.get());
@@ -643,7 +608,6 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     });
     k_step_totals<<<1, 1, 0, st>>>(W.rpre.get(), W.cpre.get(), W.pos.get(), nb, W.tot.get());
     HM_CHECK_LAUNCH();
-    HM_CUDA(cudaMemsetAsync(W.cnt.get() + 3, 0, 2 * sizeof(unsigned long long), st));   // pivot / update counters
     const int slot = step % (kLag + 1);
     HM_CUDA(cudaMemcpyAsync(W.h_ring.data() + 3 * slot, W.tot.get(), 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     HM_CUDA(cudaEventRecord(W.ring_ev[slot], st));
@@ -655,32 +619,31 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     ks.reset();
     if (C.quad)
       aca_eval(C, AcaMap<true, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(),
-                                     nb, Uw, Vw, W.facc.get(), kws}, drow, rmax, W);
+                                     nb, Uw, Vw}, drow, rmax, W);
     else
       aca_eval(C, AcaMap<true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
-                               W.rtab.get(), nb, Uw, Vw, W.facc.get(), kws}, drow, rmax, W);
+                               W.rtab.get(), nb, Uw, Vw}, drow, rmax, W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_pivot<<<gpiv, 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Vw, W.bmap.get(),
-                                      W.cnt.get() + 3, W.facc.get(), kws);
+    k_aca_pivot<<<grid_for(nact_ub * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Vw,
+                                                             W.bmap.get());
     HM_CHECK_LAUNCH();
     if (nbig) {
-      k_aca_pivot_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Vw, W.bmap.get(),
-                                                      W.facc.get(), kws);
+      k_aca_pivot_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Vw, W.bmap.get());
       HM_CHECK_LAUNCH();
     }
     ks.reset();
     if (C.quad)
       aca_eval(C, AcaMap<false, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(),
-                                      nb, Uw, Vw, W.facc.get(), kws}, dcol, cmax, W);
+                                      nb, Uw, Vw}, dcol, cmax, W);
     else
       aca_eval(C, AcaMap<false>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(),
-                                W.ctab.get(), nb, Uw, Vw, W.facc.get(), kws}, dcol, cmax, W);
+                                W.ctab.get(), nb, Uw, Vw}, dcol, cmax, W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_update<<<gupd, 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Uw, W.facc.get(), W.bmap.get(),
-                                      W.piv.get(), kws, C.eps_aca, W.cnt.get() + 4);
+    k_aca_update<<<grid_for(nact_ub * 32, 64), 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Uw, Vw,
+                                                            W.bmap.get(), W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();
     if (nbig) {
-      k_aca_update_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Uw, W.facc.get(),
+      k_aca_update_big<<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), Uw, Vw,
                                                        W.bmap.get(), W.piv.get(), kws, C.eps_aca);
       HM_CHECK_LAUNCH();
     }
@@ -693,6 +656,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
       C.times.aca_phase_ms[2] += ms_since(ts);
       const int64_t* t = W.h_ring.data() + 3 * rs;
       if (t[0] == 0) break;        // no active block since step - kLag: the later steps were no-ops
+      nact_ub = t[2];
       C.aca_steps++;
       C.entries_aca += (double)(t[0] + t[1]);
     }

@@ -10,11 +10,7 @@
 // A batch is described by a mapping M (device-side functor, passed by value):
 //   bool locate(int64_t e, bool valid, EntryRef& r)  flattened entry -> reference (warp-collective)
 //   void pair(EntryRef r, int& s, int& t)            internal row / column indices of the entry
-//   double put(EntryRef r, double a)                 consume the value (store / residual update),
-//                                                    return what was stored
-//   void cross(EntryRef r, bool valid, double v, int lane)  warp-collective: after put(), all
-//                                                    32 lanes (ACA: Frobenius cross sums; near
-//                                                    field: nothing)
+//   void put(EntryRef r, double a)                   consume the value (store / residual update)
 //   kQuad, P (node panels), PT, QV                   quadrilateral meshes (A25): class 0 = touching
 //                                                    quads (four triangle pairs over PT), classes
 //                                                    3..6 = separated quads, tensor rule on P
@@ -171,7 +167,7 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
 //   k_eval_rest     persistent, the remaining few (orders 5, 6, touching pairs).
 // one 32-entry group of a warp (lanes e = e0 + lane): classify, append non-order-3 entries,
 // evaluate order 3 in place
-template <bool PF, class M>
+template <class M>
 __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t total, int lane, EntryRef* __restrict__ lists,
                                              unsigned long long* __restrict__ cnt, unsigned long long& ev) {
   EntryRef r;
@@ -180,7 +176,6 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
     int s, t;
     m.pair(r, s, t);
     cls = map_class(m, s, t, xs, ys);
-    if (PF) m.prefetch_next(r);
   }
   const unsigned below = (1u << lane) - 1u;
   const unsigned b4 = __ballot_sync(0xffffffffu, cls == 4), br = __ballot_sync(0xffffffffu, cls >= 0 && cls != 3 && cls != 4);
@@ -193,12 +188,10 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
   baser = __shfl_sync(0xffffffffu, baser, 0);
   if (cls == 4) lists[base4 + __popc(b4 & below)] = r;
   else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
-  double res = 0.0;
   if (cls == 3) {
-    res = m.put(r, map_regular<3>(m, xs, ys));
+    m.put(r, map_regular<3>(m, xs, ys));
     ev += M::kQuad ? 81 : tri_rule_points(3) * tri_rule_points(3);
   }
-  m.cross(r, cls == 3, res, lane);
 }
 
 // Persistent, dynamically balanced: every warp takes groups of kDynGroups x 32 consecutive
@@ -206,7 +199,7 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
 // one thread per entry leave SMs idle at the tail: C4 ACA evaluation 1.85 s resp. 1.75 s vs
 // 1.61 s, profiles/r02_setup_ab1.jsonl)
 constexpr int kDynGroups = 4;
-template <class M, bool PF = true>
+template <class M>
 __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __restrict__ dtot,
                                                      EntryRef* __restrict__ lists,
                                                      unsigned long long* __restrict__ cnt /* [n4, nrest, next] */,
@@ -220,7 +213,7 @@ __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __re
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     if ((int64_t)b0 >= total) break;
 #pragma unroll 1
-    for (int g = 0; g < kDynGroups; ++g) class3_group<PF>(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
+    for (int g = 0; g < kDynGroups; ++g) class3_group(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
@@ -232,20 +225,12 @@ __global__ void __launch_bounds__(128) k_eval_list(M m, const EntryRef* __restri
                                                    const unsigned long long* __restrict__ cnt,
                                                    unsigned long long* __restrict__ evals) {
   const int64_t c = (int64_t)*cnt;
-  const int lane = threadIdx.x & 31;
-  // warp-uniform loop (whole warps per iteration) so that m.cross can be warp-collective
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); b < c; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = b + lane;
-    EntryRef r{0, 0};
-    double res = 0.0;
-    if (k < c) {
-      r = list[k];
-      int s, t, xs, ys;
-      m.pair(r, s, t);
-      map_class(m, s, t, xs, ys);
-      res = m.put(r, map_regular<n>(m, xs, ys));
-    }
-    m.cross(r, k < c, res, lane);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < c; k += (int64_t)gridDim.x * blockDim.x) {
+    const EntryRef r = list[k];
+    int s, t, xs, ys;
+    m.pair(r, s, t);
+    map_class(m, s, t, xs, ys);
+    m.put(r, map_regular<n>(m, xs, ys));
   }
   constexpr int np = M::kQuad ? n * n : tri_rule_points(n);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(evals, (unsigned long long)(np * np) * (unsigned long long)c);
@@ -259,19 +244,12 @@ __global__ void __launch_bounds__(128) k_eval_rest(M m, const EntryRef* __restri
                                                    unsigned long long* __restrict__ evals) {
   const int64_t total = *dtot;
   const int64_t c = (int64_t)cnt[1];
-  const int lane = threadIdx.x & 31;
   unsigned long long ev = 0;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); b < c; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = b + lane;
-    EntryRef r{0, 0};
-    double res = 0.0;
-    if (k < c) {
-      r = lists[total - 1 - k];
-      int s, t;
-      m.pair(r, s, t);
-      res = m.put(r, map_entry(m, s, t, ev));
-    }
-    m.cross(r, k < c, res, lane);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < c; k += (int64_t)gridDim.x * blockDim.x) {
+    const EntryRef r = lists[total - 1 - k];
+    int s, t;
+    m.pair(r, s, t);
+    m.put(r, map_entry(m, s, t, ev));
   }
   if (ev) atomicAdd(evals, ev);
 }

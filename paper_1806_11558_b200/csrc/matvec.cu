@@ -332,7 +332,7 @@ __device__ __forceinline__ void warp_reduce_halving(double (&v)[KB], int lane) {
 }
 
 template <class E>
-__global__ void __launch_bounds__(256, 2) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
+__global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
                                                       const MvLarge* __restrict__ L, const E* __restrict__ pool,
                                                       const double* __restrict__ x, double* __restrict__ tbuf) {
   const int lane = threadIdx.x & 31;
@@ -347,38 +347,17 @@ __global__ void __launch_bounds__(256, 2) k_mv_large_v(const MvTileV* __restrict
     double acc[16];
 #pragma unroll
     for (int l = 0; l < 16; ++l) acc[l] = 0.0;
-    if constexpr (sizeof(E) == 8) {
-      for (int j = T.j0 + lane; j < T.j1; j += 64) {
-        const bool two = j + 32 < T.j1;
-        const double xa = __ldg(xs + j), xb = two ? __ldg(xs + j + 32) : 0.0;
-        double va[16], vb[16];
+    for (int j = T.j0 + lane; j < T.j1; j += 64) {
+      const bool two = j + 32 < T.j1;
+      const double xa = __ldg(xs + j), xb = two ? __ldg(xs + j + 32) : 0.0;
+      double va[16], vb[16];
 #pragma unroll
-        for (int l = 0; l < 16; ++l) {
-          va[l] = l < kc ? (double)__ldg(V + j + (int64_t)l * B.n) : 0.0;
-          vb[l] = (l < kc && two) ? (double)__ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
-        }
-#pragma unroll
-        for (int l = 0; l < 16; ++l) acc[l] = __fma_rn(vb[l], xb, __fma_rn(va[l], xa, acc[l]));
-      }
-    } else {
-    // binary32 factors: 4 rows per lane per pass, 64 loads in flight per lane (the bytes in
-    // flight of the FP64 path)
-    constexpr int R = 4;
-    for (int j = T.j0 + lane; j < T.j1; j += 32 * R) {
-      double xr[R];
-      E v[R][16];
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const bool ok = j + 32 * q < T.j1;
-        xr[q] = ok ? __ldg(xs + j + 32 * q) : 0.0;
-#pragma unroll
-        for (int l = 0; l < 16; ++l) v[q][l] = (l < kc && ok) ? __ldg(V + j + 32 * q + (int64_t)l * B.n) : E(0);
+      for (int l = 0; l < 16; ++l) {
+        va[l] = l < kc ? (double)__ldg(V + j + (int64_t)l * B.n) : 0.0;
+        vb[l] = (l < kc && two) ? (double)__ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < R; ++q)
-#pragma unroll
-        for (int l = 0; l < 16; ++l) acc[l] = __fma_rn((double)v[q][l], xr[q], acc[l]);
-    }
+      for (int l = 0; l < 16; ++l) acc[l] = __fma_rn(vb[l], xb, __fma_rn(va[l], xa, acc[l]));
     }
     warp_reduce_halving<16>(acc, lane);
     // lane L holds column 8*b4 + 4*b3 + 2*b2 + b1 (two lanes per column)
@@ -405,49 +384,27 @@ __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ 
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    if constexpr (sizeof(E) == 8) {
-      int l = 0;
-      for (; l + 1 < B.k; l += 2) {
-        const double ta = __ldg(tl + l), tb = __ldg(tl + l + 1);
-        const E* Ua = U + (int64_t)l * B.m;
-        const E* Ub = Ua + B.m;
-        double ua[8], ub[8];
+    int l = 0;
+    for (; l + 1 < B.k; l += 2) {
+      const double ta = __ldg(tl + l), tb = __ldg(tl + l + 1);
+      const E* Ua = U + (int64_t)l * B.m;
+      const E* Ub = Ua + B.m;
+      double ua[8], ub[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const bool ok = lane + 32 * q < rows;
-          ua[q] = ok ? (double)__ldg(Ua + 32 * q) : 0.0;
-          ub[q] = ok ? (double)__ldg(Ub + 32 * q) : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] = __fma_rn(ub[q], tb, __fma_rn(ua[q], ta, acc[q]));
-      }
-      if (l < B.k) {
-        const double ta = __ldg(tl + l);
-        const E* Ua = U + (int64_t)l * B.m;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (lane + 32 * q < rows) acc[q] = __fma_rn((double)__ldg(Ua + 32 * q), ta, acc[q]);
-      }
-    } else {
-    // binary32 factors: 4 columns per pass, 32 loads in flight per lane (the bytes in flight of
-    // the FP64 path)
-    constexpr int CP = 4;
-    for (int l = 0; l < B.k; l += CP) {
-      double tc[CP];
-      E u[CP][8];
-#pragma unroll
-      for (int c = 0; c < CP; ++c) {
-        const bool okc = l + c < B.k;
-        tc[c] = okc ? __ldg(tl + l + c) : 0.0;
-        const E* Uc = U + (int64_t)(l + c) * B.m;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) u[c][q] = (okc && lane + 32 * q < rows) ? __ldg(Uc + 32 * q) : E(0);
+      for (int q = 0; q < 8; ++q) {
+        const bool ok = lane + 32 * q < rows;
+        ua[q] = ok ? (double)__ldg(Ua + 32 * q) : 0.0;
+        ub[q] = ok ? (double)__ldg(Ub + 32 * q) : 0.0;
       }
 #pragma unroll
-      for (int c = 0; c < CP; ++c)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] = __fma_rn((double)u[c][q], tc[c], acc[q]);
+      for (int q = 0; q < 8; ++q) acc[q] = __fma_rn(ub[q], tb, __fma_rn(ua[q], ta, acc[q]));
     }
+    if (l < B.k) {
+      const double ta = __ldg(tl + l);
+      const E* Ua = U + (int64_t)l * B.m;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (lane + 32 * q < rows) acc[q] = __fma_rn((double)__ldg(Ua + 32 * q), ta, acc[q]);
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q)

@@ -46,9 +46,7 @@ struct NearMap {
     s = Q.rlo + r.idx / ncol;
     t = Q.clo + r.idx % ncol;
   }
-  __device__ double put(EntryRef r, double a) const { store[off[r.seg] + r.idx] = a; return a; }
-  __device__ void cross(EntryRef, bool, double, int) const {}
-  __device__ void prefetch_next(EntryRef) const {}
+  __device__ void put(EntryRef r, double a) const { store[off[r.seg] + r.idx] = a; }
 };
 
 // bad[0] = number of non-finite entries, bad[1] = smallest offset of one (if any)
