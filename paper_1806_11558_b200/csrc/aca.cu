@@ -129,6 +129,28 @@ struct AcaMap {
     s = ROW ? b.q.rlo + st.i : b.q.rlo + r.idx;
     t = ROW ? b.q.clo + r.idx : b.q.clo + st.js;
   }
+  // Prefetch (option aca_prefetch, A/B) of the residual-correction operands this entry's put()
+  // will load after the quadrature: PF 1 = into L1, 2 = into L2; PF 3 = the panel and operands
+  // of the entry 32 positions further along (the warp's next group), into L2
+  template <int PF>
+  __device__ __forceinline__ void prefetch(EntryRef r) const {
+    if (PF == 0) return;
+    const AcaBlk& b = B[r.seg];
+    const AcaState& st = S[r.seg];
+    const int64_t ld = ROW ? b.n : b.m;
+    int idx = r.idx;
+    if (PF == 3) {
+      idx += 32;
+      if (idx >= ld) return;
+      const Panel* pn = P + (ROW ? b.q.clo + idx : b.q.rlo + idx);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pn));
+    }
+    const double* w = ROW ? Vw + b.voff + idx : Uw + b.uoff + idx;
+    for (int l = 0; l < st.k; ++l) {
+      if (PF == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(w + l * ld));
+      else asm volatile("prefetch.global.L2 [%0];" ::"l"(w + l * ld));
+    }
+  }
   __device__ void put(EntryRef r, double a) const {
     const AcaBlk& b = B[r.seg];
     const AcaState st = S[r.seg];
@@ -513,7 +535,12 @@ void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWor
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 3 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4);   // one wave, persistent
-  k_eval_class3<M><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
+  switch (C.aca_prefetch) {
+    case 1: k_eval_class3<M, 1><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
+    case 2: k_eval_class3<M, 2><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
+    case 3: k_eval_class3<M, 3><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
+    default: k_eval_class3<M, 0><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
+  }
   HM_CHECK_LAUNCH();
   const unsigned g4 = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 16);
   k_eval_list<4, M><<<g4, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
 //   k_eval_rest     persistent, the remaining few (orders 5, 6, touching pairs).
 // one 32-entry group of a warp (lanes e = e0 + lane): classify, append non-order-3 entries,
 // evaluate order 3 in place
-template <class M>
+template <int PF, class M>
 __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t total, int lane, EntryRef* __restrict__ lists,
                                              unsigned long long* __restrict__ cnt, unsigned long long& ev) {
   EntryRef r;
@@ -176,6 +176,7 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
     int s, t;
     m.pair(r, s, t);
     cls = map_class(m, s, t, xs, ys);
+    m.template prefetch<PF>(r);
   }
   const unsigned below = (1u << lane) - 1u;
   const unsigned b4 = __ballot_sync(0xffffffffu, cls == 4), br = __ballot_sync(0xffffffffu, cls >= 0 && cls != 3 && cls != 4);
@@ -199,7 +200,7 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
 // one thread per entry leave SMs idle at the tail: C4 ACA evaluation 1.85 s resp. 1.75 s vs
 // 1.61 s, profiles/r02_setup_ab1.jsonl)
 constexpr int kDynGroups = 4;
-template <class M>
+template <class M, int PF = 0>
 __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __restrict__ dtot,
                                                      EntryRef* __restrict__ lists,
                                                      unsigned long long* __restrict__ cnt /* [n4, nrest, next] */,
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __re
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     if ((int64_t)b0 >= total) break;
 #pragma unroll 1
-    for (int g = 0; g < kDynGroups; ++g) class3_group(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
+    for (int g = 0; g < kDynGroups; ++g) class3_group<PF>(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);

@@ -47,6 +47,8 @@ struct NearMap {
     t = Q.clo + r.idx % ncol;
   }
   __device__ void put(EntryRef r, double a) const { store[off[r.seg] + r.idx] = a; }
+  template <int PF>
+  __device__ void prefetch(EntryRef) const {}
 };
 
 // bad[0] = number of non-finite entries, bad[1] = smallest offset of one (if any)
