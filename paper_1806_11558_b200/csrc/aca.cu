@@ -129,26 +129,39 @@ struct AcaMap {
     s = ROW ? b.q.rlo + st.i : b.q.rlo + r.idx;
     t = ROW ? b.q.clo + r.idx : b.q.clo + st.js;
   }
-  // Prefetch (option aca_prefetch, A/B) of the residual-correction operands this entry's put()
-  // will load after the quadrature: PF 1 = into L1, 2 = into L2; PF 3 = the panel and operands
-  // of the entry 32 positions further along (the warp's next group), into L2
-  template <int PF>
-  __device__ __forceinline__ void prefetch(EntryRef r) const {
-    if (PF == 0) return;
+  // Early residual-correction operands (option aca_early = KE): the first min(k, KE) pairs
+  // (U[i, l], V[j, l]) are loaded before the quadrature, so their latency hides behind it;
+  // put_early() then applies a = a - U V in the same order and rounding as put().
+  template <int KE>
+  __device__ __forceinline__ int early(EntryRef r, double (&eu)[KE > 0 ? KE : 1], double (&ev)[KE > 0 ? KE : 1]) const {
+    if (KE == 0) return 0;
     const AcaBlk& b = B[r.seg];
     const AcaState& st = S[r.seg];
-    const int64_t ld = ROW ? b.n : b.m;
-    int idx = r.idx;
-    if (PF == 3) {
-      idx += 32;
-      if (idx >= ld) return;
-      const Panel* pn = P + (ROW ? b.q.clo + idx : b.q.rlo + idx);
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(pn));
-    }
-    const double* w = ROW ? Vw + b.voff + idx : Uw + b.uoff + idx;
-    for (int l = 0; l < st.k; ++l) {
-      if (PF == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(w + l * ld));
-      else asm volatile("prefetch.global.L2 [%0];" ::"l"(w + l * ld));
+    const int ke = min(st.k, KE);
+#pragma unroll
+    for (int l = 0; l < KE; ++l)
+      if (l < ke) {
+        eu[l] = ROW ? Uw[b.uoff + st.i + (int64_t)l * b.m] : Uw[b.uoff + r.idx + (int64_t)l * b.m];
+        ev[l] = ROW ? Vw[b.voff + r.idx + (int64_t)l * b.n] : Vw[b.voff + st.js + (int64_t)l * b.n];
+      }
+    return ke;
+  }
+  template <int KE>
+  __device__ __forceinline__ void put_early(EntryRef r, double a, int ke, const double (&eu)[KE > 0 ? KE : 1],
+                                            const double (&ev)[KE > 0 ? KE : 1]) const {
+    const AcaBlk& b = B[r.seg];
+    const AcaState st = S[r.seg];
+#pragma unroll
+    for (int l = 0; l < KE; ++l)
+      if (l < ke) a = dsub(a, dmul(eu[l], ev[l]));
+    const double* U = Uw + b.uoff;
+    const double* V = Vw + b.voff;
+    if (ROW) {
+      for (int l = ke; l < st.k; ++l) a = dsub(a, dmul(U[st.i + (int64_t)l * b.m], V[r.idx + (int64_t)l * b.n]));
+      Vw[b.voff + (int64_t)st.k * b.n + r.idx] = a;
+    } else {
+      for (int l = ke; l < st.k; ++l) a = dsub(a, dmul(U[r.idx + (int64_t)l * b.m], V[st.js + (int64_t)l * b.n]));
+      Uw[b.uoff + (int64_t)st.k * b.m + r.idx] = a;
     }
   }
   __device__ void put(EntryRef r, double a) const {
@@ -535,10 +548,10 @@ void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWor
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 3 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4);   // one wave, persistent
-  switch (C.aca_prefetch) {
-    case 1: k_eval_class3<M, 1><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
+  switch (C.aca_early) {
     case 2: k_eval_class3<M, 2><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
-    case 3: k_eval_class3<M, 3><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
+    case 4: k_eval_class3<M, 4><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
+    case 8: k_eval_class3<M, 8><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
     default: k_eval_class3<M, 0><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
   }
   HM_CHECK_LAUNCH();

@@ -349,7 +349,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
     else if (k == "aca_kws") { if (v < 1 || v > 256) bad(); C.aca_kws = v; }
     else if (k == "lr_f32") { if (v != 0 && v != 1) bad(); C.lr_f32 = (int)v; }
-    else if (k == "aca_prefetch") { if (v < 0 || v > 3) bad(); C.aca_prefetch = (int)v; }
+    else if (k == "aca_early") { if (v != 0 && v != 2 && v != 4 && v != 8) bad(); C.aca_early = (int)v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
     else if (k == "mv_kernel") { if (v != 0 && v != 1) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_profile") {
@@ -383,7 +383,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "aca_chunk_mb") *v = C.aca_chunk_mb;
     else if (k == "aca_kws") *v = C.aca_kws;
     else if (k == "lr_f32") *v = C.lr_f32;
-    else if (k == "aca_prefetch") *v = C.aca_prefetch;
+    else if (k == "aca_early") *v = C.aca_early;
     else if (k == "record_pivots") *v = C.record_pivots;
     else if (k == "kernel_timing") *v = C.kt.on ? 1 : 0;
     else if (k == "mv_kernel") *v = C.mv_kind;
