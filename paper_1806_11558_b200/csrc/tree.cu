@@ -325,11 +325,41 @@ __global__ void k_block_level(const int2* __restrict__ fr, const uint64_t* __res
   }
 }
 
-__global__ void k_leaf_cost(const Quad* __restrict__ q, int64_t n, int kind, int64_t* __restrict__ cost) {
+// Per-leaf setup cost for the partition (A18).  model 0 (round 1): dense |t||s|, admissible
+// (|t|+|s|) 10.  model 1 (default): the evaluations the leaf will cost —
+//   dense: |t||s| x (mean rule evaluations per entry of its kind, oracle-measured at C4 on 400
+//          leaves each: diagonal t = s 1542, boxes touching 360, separated 140 -> weights
+//          110 / 26 / 10; boxes over the node centroids, the same boxes as admissibility)
+//   admissible: (|t|+|s|) x 10 k^, k^ = 8.2 + 0.3 log2((|t|+|s|)/40): the mean ACA rank at
+//          eps 1e-6 grows slowly with the block size (oracle at C3: 8.2 at m+n = 40 ... 10.0 at
+//          ~5900)
+__global__ void k_leaf_cost(const Quad* __restrict__ q, int64_t n, int kind, int model, const double* __restrict__ cen,
+                            int cstride, int64_t* __restrict__ cost) {
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= n) return;
-  int64_t m = q[b].rhi - q[b].rlo, nn = q[b].chi - q[b].clo;
-  cost[b] = kind == 1 ? m * nn : (m + nn) * 10;   // A18: dense |t||s|, admissible (|t|+|s|) k_est
+  const Quad Q = q[b];
+  const int64_t m = Q.rhi - Q.rlo, nn = Q.chi - Q.clo;
+  if (model == 0) { cost[b] = kind == 1 ? m * nn : (m + nn) * 10; return; }
+  if (kind == 0) {
+    const double kh = 8.2 + 0.3 * log2((double)(m + nn) / 40.0);
+    cost[b] = (m + nn) * (int64_t)llrint(10.0 * fmax(kh, 7.0));
+    return;
+  }
+  int64_t w = 10;
+  if (Q.rlo == Q.clo && Q.rhi == Q.chi) {
+    w = 110;
+  } else {
+    double bt[6], bs[6];
+    for (int a = 0; a < 3; ++a) { bt[a] = bs[a] = 1e300; bt[3 + a] = bs[3 + a] = -1e300; }
+    for (int s = Q.rlo; s < Q.rhi; ++s)
+      for (int a = 0; a < 3; ++a) { const double c = cen[(int64_t)s * cstride + a]; bt[a] = fmin(bt[a], c); bt[3 + a] = fmax(bt[3 + a], c); }
+    for (int s = Q.clo; s < Q.chi; ++s)
+      for (int a = 0; a < 3; ++a) { const double c = cen[(int64_t)s * cstride + a]; bs[a] = fmin(bs[a], c); bs[3 + a] = fmax(bs[3 + a], c); }
+    bool touch = true;
+    for (int a = 0; a < 3; ++a) touch &= bs[a] <= bt[3 + a] && bt[a] <= bs[3 + a];
+    if (touch) w = 26;
+  }
+  cost[b] = m * nn * w;
 }
 
 template <class F>
@@ -368,10 +398,16 @@ __global__ void k_prefix_bounds(const int64_t* __restrict__ pref, int64_t n, con
 
 void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_t& begin, int64_t& end,
                     DBuf<char>& tmp) {
-  if (C.world == 1 || n == 0) { begin = 0; end = n; return; }
+  // diagnostic options part_ranks / part_rank (one process, world 1): take rank r's share of a
+  // p-way partition, to measure every rank's setup of a p-GPU run one after the other on one GPU
+  const int P = C.world > 1 ? C.world : C.part_ranks, R = C.world > 1 ? C.rank : C.part_rank;
+  if (P <= 1 || n == 0) { begin = 0; end = n; return; }
   DBuf<int64_t>& cost = C.tws.cost; DBuf<int64_t>& pref = C.tws.pref;
   cost.alloc(n); pref.alloc(n);
-  k_leaf_cost<<<grid_for(n, 256), 256, 0, C.stream>>>(q.get(), n, kind, cost.get());
+  const Panel* nodes = C.quad ? C.qnode.get() : C.panel.get();
+  const double* cen = reinterpret_cast<const double*>(reinterpret_cast<const char*>(nodes) + offsetof(Panel, c));
+  k_leaf_cost<<<grid_for(n, 256), 256, 0, C.stream>>>(q.get(), n, kind, C.cost_model, cen,
+                                                       (int)(sizeof(Panel) / sizeof(double)), cost.get());
   HM_CHECK_LAUNCH();
   cub_call(tmp, [&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, cost.get(), pref.get(), n, C.stream);
@@ -381,9 +417,9 @@ void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_
   HM_CUDA(cudaMemcpyAsync(&h[1], cost.get() + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
   HM_CUDA(cudaStreamSynchronize(C.stream));
   const int64_t total = h[0] + h[1];
-  auto bound_of = [&](int r) -> int64_t { return (int64_t)(((__int128)r * total) / C.world); };
+  auto bound_of = [&](int r) -> int64_t { return (int64_t)(((__int128)r * total) / P); };
   // rank r owns the leaves whose exclusive prefix lies in [floor(rC/p), floor((r+1)C/p)) (A18)
-  int64_t hb[2] = {bound_of(C.rank), bound_of(C.rank + 1)};
+  int64_t hb[2] = {bound_of(R), bound_of(R + 1)};
   unsigned long long ho[2] = {(unsigned long long)n, (unsigned long long)n};
   C.tws.bounds.alloc(2);
   C.tws.bout.alloc(2);
@@ -393,8 +429,8 @@ void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_
   HM_CHECK_LAUNCH();
   HM_CUDA(cudaMemcpyAsync(ho, C.tws.bout.get(), sizeof(ho), cudaMemcpyDeviceToHost, C.stream));
   HM_CUDA(cudaStreamSynchronize(C.stream));
-  begin = C.rank == 0 ? 0 : (int64_t)ho[0];
-  end = C.rank + 1 >= C.world ? n : (int64_t)ho[1];
+  begin = R == 0 ? 0 : (int64_t)ho[0];
+  end = R + 1 >= P ? n : (int64_t)ho[1];
 }
 
 }  // namespace
