@@ -267,6 +267,7 @@ def _run_gpu(args, rank, world, local, dev, stream):
     mv_kern_ms = max_over_ranks(kt["matvec_ms"] / max(1, kt["matvec_n"]), world)
     mv_kern_ms_step = max_over_ranks(kt["matvec_ms"] / K, world)
     krylov_ms_step = max_over_ranks(kt.get("krylov_ms", 0.0) / K, world)
+    comm_ms_step = max_over_ranks(kt.get("comm_ms", 0.0) / K, world)      # NCCL calls (p > 1)
     per_rank = None
     if world > 1:                      # per-rank phase times (load balance of the leaf partition)
         import torch.distributed as dist
@@ -401,7 +402,9 @@ def _run_gpu(args, rank, world, local, dev, stream):
                           "eval_rate_phase_Gps": round(eval_rate_phase / 1e9, 2),
                           "kernel_ms_per_step": {"eval": round(eval_ms, 3), "aca_other": round(aca_other_ms, 3),
                                                  "matvec": round(mv_kern_ms_step, 3),
-                                                 "krylov_blas1": round(krylov_ms_step, 3)},
+                                                 "krylov_blas1": round(krylov_ms_step, 3),
+                                                 "nccl": round(comm_ms_step, 3)},
+                          "nccl_us_per_iteration": round(1e3 * comm_ms_step / max(1, iters), 2) if world > 1 else None,
                           "per_rank_near_aca_setup_solve_ms_storedGB": per_rank, "accuracy": accuracy},
             "roofline": roof, "matvec_roofline": matvec_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,

@@ -190,6 +190,7 @@ KTimer::~KTimer() {
 
 // ---- NCCL ---------------------------------------------------------------------------------
 void allreduce_sum(Context& C, double* buf, int64_t n) {
+  KScope ks(C, KF_COMM);
   HM_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, C.comm, C.stream));
 }
 
@@ -350,7 +351,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "aca_kws") { if (v < 1 || v > 256) bad(); C.aca_kws = v; }
     else if (k == "lr_f32") { if (v != 0 && v != 1) bad(); C.lr_f32 = (int)v; }
     else if (k == "aca_early") { if (v != 0 && v != 2 && v != 4 && v != 8) bad(); C.aca_early = (int)v; }
-    else if (k == "cost_model") { if (v != 0 && v != 1) bad(); C.cost_model = (int)v; }
+    else if (k == "cost_model") { if (v != 0 && v != 1 && v != 2) bad(); C.cost_model = (int)v; }
     else if (k == "part_ranks") { if (v < 1 || v > 4096) bad(); C.part_ranks = (int)v; }
     else if (k == "part_rank") { if (v < 0 || v > 4095) bad(); C.part_rank = (int)v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
@@ -751,7 +752,7 @@ hm_status hm_get_stats(hm_ctx ctx, char* buf, int64_t len) {
       o << ",\"mv_prof_cycles\":[" << pr[0] << "," << pr[1] << "," << pr[2] << "]";
     }
     o << ",\"kt\":{\"on\":" << (C.kt.on ? 1 : 0);
-    const char* fam[hm::KF_NUM] = {"eval_near", "eval_aca", "aca_other", "matvec", "krylov"};
+    const char* fam[hm::KF_NUM] = {"eval_near", "eval_aca", "aca_other", "matvec", "krylov", "comm"};
     for (int f = 0; f < hm::KF_NUM; ++f)
       o << ",\"" << fam[f] << "_ms\":" << C.kt.ms[f] << ",\"" << fam[f] << "_n\":" << C.kt.n[f];
     o << ",\"eval_union_ms\":" << C.kt.eval_union_ms << "}}";

@@ -197,15 +197,15 @@ struct PhaseTimes {
 // When the near field runs beside ACA (option setup_overlap) the two evaluation families
 // overlap in time; eval_union_ms is the length of the union of their intervals, measured
 // against a reference event recorded before the streams fork (mark()).
-enum KFam { KF_EVAL_NEAR = 0, KF_EVAL_ACA = 1, KF_ACA_OTHER = 2, KF_MATVEC = 3, KF_KRYLOV = 4, KF_NUM = 5 };
+enum KFam { KF_EVAL_NEAR = 0, KF_EVAL_ACA = 1, KF_ACA_OTHER = 2, KF_MATVEC = 3, KF_KRYLOV = 4, KF_COMM = 5, KF_NUM = 6 };
 struct KTimer {
   bool on = false;
   std::vector<cudaEvent_t> pool;
   struct P { int fam; cudaEvent_t a, b; };
   std::vector<P> pend;
   cudaEvent_t ref = nullptr;   // set by mark(): intervals of this batch measured from it
-  double ms[KF_NUM] = {0, 0, 0, 0, 0};
-  int64_t n[KF_NUM] = {0, 0, 0, 0, 0};
+  double ms[KF_NUM] = {0, 0, 0, 0, 0, 0};
+  int64_t n[KF_NUM] = {0, 0, 0, 0, 0, 0};
   double eval_union_ms = 0;
   cudaEvent_t get();
   void mark(cudaStream_t st);

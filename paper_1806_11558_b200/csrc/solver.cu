@@ -152,9 +152,13 @@ unsigned vgrid(int64_t n) { return std::min<unsigned>(grid_for(n, 256), 148 * 16
 
 void apply(Context& C, const Layout& L, const double* x, double* y) {
   if (!L.sharded) { matvec_internal(C, x, y); return; }
+  { KScope ks_(C, KF_COMM);
   HM_NCCL(ncclAllGather(x, C.sh_x.get(), (size_t)L.S, ncclDouble, C.comm, C.stream));
+  }
   matvec_internal(C, C.sh_x.get(), C.sh_y.get(), /*reduce=*/false);
+  { KScope ks_(C, KF_COMM);
   HM_NCCL(ncclReduceScatter(C.sh_y.get(), y, (size_t)L.S, ncclDouble, ncclSum, C.comm, C.stream));
+  }
 }
 
 double true_relres(Context& C, const Layout& L, Red& R, const double* b, const double* x, double bn, double* tmp) {
@@ -320,7 +324,9 @@ void solve(Context& C, const double* rhs_int, double* sol_int, double tol, int* 
   if (C.solver == 1) cg(C, L, rhs_int + L.off, C.sh_sol.get(), tol, iters, relres);
   else gmres(C, L, rhs_int + L.off, C.sh_sol.get(), tol, iters, relres);
   // the full solution on every rank
+  { KScope ks_(C, KF_COMM);
   HM_NCCL(ncclAllGather(C.sh_sol.get(), C.sh_x.get(), (size_t)L.S, ncclDouble, C.comm, C.stream));
+  }
   HM_CUDA(cudaMemcpyAsync(sol_int, C.sh_x.get(), C.N * sizeof(double), cudaMemcpyDeviceToDevice, C.stream));
   HM_CUDA(cudaStreamSynchronize(C.stream));
 }

@@ -333,6 +333,10 @@ __global__ void k_block_level(const int2* __restrict__ fr, const uint64_t* __res
 //   admissible: (|t|+|s|) x 10 k^, k^ = 8.2 + 0.3 log2((|t|+|s|)/40): the mean ACA rank at
 //          eps 1e-6 grows slowly with the block size (oracle at C3: 8.2 at m+n = 40 ... 10.0 at
 //          ~5900)
+// model 2: the dense weights of model 1, admissible (|t|+|s| + 21) x 10: a fixed per-block
+//          cost (the per-step pivot / update / bookkeeping of a block, fitted on the one-GPU
+//          emulation of 4- and 8-rank partitions at C4, profiles/r02_partition_emulate_c4.jsonl:
+//          per rank ~21.7 us per block vs 1.0 us per unit of m + n)
 __global__ void k_leaf_cost(const Quad* __restrict__ q, int64_t n, int kind, int model, const double* __restrict__ cen,
                             int cstride, int64_t* __restrict__ cost) {
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -341,6 +345,7 @@ __global__ void k_leaf_cost(const Quad* __restrict__ q, int64_t n, int kind, int
   const int64_t m = Q.rhi - Q.rlo, nn = Q.chi - Q.clo;
   if (model == 0) { cost[b] = kind == 1 ? m * nn : (m + nn) * 10; return; }
   if (kind == 0) {
+    if (model == 2) { cost[b] = (m + nn + 21) * 10; return; }
     const double kh = 8.2 + 0.3 * log2((double)(m + nn) / 40.0);
     cost[b] = (m + nn) * (int64_t)llrint(10.0 * fmax(kh, 7.0));
     return;
