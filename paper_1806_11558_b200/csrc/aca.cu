@@ -12,12 +12,12 @@
 // (which feed the stop test alone) are tree-reduced.  Workspace per block holds KWS
 // columns; blocks that reach KWS without stopping are re-run with k_max columns.
 // Finished blocks are packed into the factor pool as [U (m x k) | V (n x k)], col-major.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <chrono>
 
 #include "entry_batch.cuh"
+#include "primitives.cuh"
 
 namespace hm {
 
@@ -529,13 +529,6 @@ __global__ void __launch_bounds__(256) k_aca_store(const AcaBlk* __restrict__ B,
   }
 }
 
-template <class F>
-void cub_call(DBuf<char>& tmp, F&& f) {
-  size_t bytes = 0;
-  HM_CUDA(f(nullptr, bytes));
-  tmp.alloc(bytes);
-  HM_CUDA(f(tmp.get(), bytes));
-}
 
 
 
@@ -634,18 +627,12 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     std::unique_ptr<KScope> ks(new KScope(C, KF_ACA_OTHER));
     k_step_flags<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.state.get(), nb, W.flag.get());
     HM_CHECK_LAUNCH();
-    cub_call(W.tmp, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, W.flag.get(), W.pos.get(), nb + 1, st);
-    });
+    prim::exclusive_scan<int32_t>(W.flag.get(), W.pos.get(), nb + 1, W.tmp, st);
     k_step_compact<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.flag.get(), W.pos.get(), nb, W.act.get(),
                                                           W.rsz.get(), W.csz.get());
     HM_CHECK_LAUNCH();
-    cub_call(W.tmp, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, W.rsz.get(), W.rpre.get(), nb + 1, st);
-    });
-    cub_call(W.tmp, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, W.csz.get(), W.cpre.get(), nb + 1, st);
-    });
+    prim::exclusive_scan<int64_t>(W.rsz.get(), W.rpre.get(), nb + 1, W.tmp, st);
+    prim::exclusive_scan<int64_t>(W.csz.get(), W.cpre.get(), nb + 1, W.tmp, st);
     k_step_totals<<<1, 1, 0, st>>>(W.rpre.get(), W.cpre.get(), W.pos.get(), nb, W.tot.get());
     HM_CHECK_LAUNCH();
     const int slot = step % (kLag + 1);
@@ -708,9 +695,7 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   k_final_sizes<<<grid_for(nb + 1, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.rsz.get(), W.owned.get(),
                                                        W.ovf.get(), W.novf.get());
   HM_CHECK_LAUNCH();
-  cub_call(W.tmp, [&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, W.rsz.get(), W.rpre.get(), nb + 1, st);
-  });
+  prim::exclusive_scan<int64_t>(W.rsz.get(), W.rpre.get(), nb + 1, W.tmp, st);
   k_store_totals<<<1, 1, 0, st>>>(W.rpre.get() + nb, W.novf.get(), W.tot.get());
   HM_CHECK_LAUNCH();
   int64_t* ht = W.h_tot.data();

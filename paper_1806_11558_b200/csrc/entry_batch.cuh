@@ -15,9 +15,9 @@
 //                                                    quads (four triangle pairs over PT), classes
 //                                                    3..6 = separated quads, tensor rule on P
 #pragma once
-#include <cub/cub.cuh>
 
 #include "entry.cuh"
+#include "primitives.cuh"
 
 namespace hm {
 
@@ -314,12 +314,8 @@ double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t s
       for (int b = 0; b < 2; ++b) { W.qkey[b].alloc(c0); W.qref[b].alloc(c0); }
       k_quad_sig<M><<<grid_for(c0, 256), 256, 0, st>>>(m, L + base[0], c0, W.qkey[0].get(), W.qref[0].get());
       HM_CHECK_LAUNCH();
-      size_t tb = 0;
-      HM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, W.qkey[0].get(), W.qkey[1].get(), W.qref[0].get(),
-                                              W.qref[1].get(), (int)c0, 0, 12, st));
-      W.qtmp.alloc(tb);
-      HM_CUDA(cub::DeviceRadixSort::SortPairs(W.qtmp.get(), tb, W.qkey[0].get(), W.qkey[1].get(), W.qref[0].get(),
-                                              W.qref[1].get(), (int)c0, 0, 12, st));
+      prim::radix_sort_pairs<uint16_t, unsigned long long>(W.qkey[0].get(), W.qkey[1].get(), W.qref[0].get(),
+                                                           W.qref[1].get(), c0, 0, 12, W.qtmp, st);
       const EntryRef* Ls = reinterpret_cast<const EntryRef*>(W.qref[1].get());
       k_eval_touching<0, M><<<grid_for(c0, 64), 64, 0, st>>>(m, Ls, c0, W.qev.get());
       HM_CHECK_LAUNCH();

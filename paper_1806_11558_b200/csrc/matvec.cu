@@ -18,7 +18,6 @@
 //                  one atomic per column into t) then k_mv_large_u (y += U t, 256-row tiles,
 //                  8 rows per lane in registers).
 //   dense blocks too big for a stage (only with large leaf_size): k_mv_dense_direct.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <chrono>

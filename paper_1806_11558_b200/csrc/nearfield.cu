@@ -2,11 +2,11 @@
 // every entry of every owned dense leaf, stored contiguously without padding, row-major per
 // block, offsets = exclusive scan of |tau||sigma|.  Entries are evaluated by the
 // class-bucketed batch machinery (entry_batch.cuh) in chunks of at most 2^26 entries.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 
 #include "entry_batch.cuh"
+#include "primitives.cuh"
 
 namespace hm {
 
@@ -82,10 +82,7 @@ void near_prepare(Context& C) {
     HM_CHECK_LAUNCH();
   }
   DBuf<char>& tmp = C.near_tmp;
-  size_t bytes = 0;
-  HM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sz.get(), C.doff.get(), nb + 1, st));
-  tmp.alloc(bytes);
-  HM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, sz.get(), C.doff.get(), nb + 1, st));
+  prim::exclusive_scan<int64_t>(sz.get(), C.doff.get(), nb + 1, tmp, st);
   std::vector<int64_t>& hoff = C.near_hoff;
   hoff.assign(nb + 1, 0);
   HM_CUDA(cudaMemcpyAsync(hoff.data(), C.doff.get(), (nb + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));

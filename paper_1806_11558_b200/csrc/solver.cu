@@ -8,7 +8,6 @@
 // paper's replicated vector + global sum; dot products are local fixed-grid tree
 // reductions followed by an ncclAllReduce of the partials, so every rank sees bit-identical
 // scalars and takes identical convergence decisions.  x0 = 0; stop at ||r|| <= tol ||b||.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>

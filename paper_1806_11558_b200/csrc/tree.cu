@@ -5,9 +5,9 @@
 //   (A18).
 // All floating-point decisions use explicitly rounded intrinsics so that codes, clusters and
 // leaf lists are bit-identical to the definition (A4-A10).
-#include <cub/cub.cuh>
 
 #include "entry.cuh"
+#include "primitives.cuh"
 
 namespace hm {
 
@@ -367,14 +367,6 @@ __global__ void k_leaf_cost(const Quad* __restrict__ q, int64_t n, int kind, int
   cost[b] = m * nn * w;
 }
 
-template <class F>
-void cub_call(DBuf<char>& tmp, F&& f) {
-  size_t bytes = 0;
-  HM_CUDA(f(nullptr, bytes));
-  tmp.alloc(bytes);
-  HM_CUDA(f(tmp.get(), bytes));
-}
-
 void grow_copy(DBuf<Quad>& q, DBuf<uint64_t>& k, int64_t used, int64_t need, cudaStream_t st) {
   if ((int64_t)q.n >= need) return;
   int64_t cap = std::max<int64_t>(need, 2 * (int64_t)q.n);
@@ -414,9 +406,7 @@ void partition_list(Context& C, const DBuf<Quad>& q, int64_t n, int kind, int64_
   k_leaf_cost<<<grid_for(n, 256), 256, 0, C.stream>>>(q.get(), n, kind, C.cost_model, cen,
                                                        (int)(sizeof(Panel) / sizeof(double)), cost.get());
   HM_CHECK_LAUNCH();
-  cub_call(tmp, [&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, cost.get(), pref.get(), n, C.stream);
-  });
+  prim::exclusive_scan<int64_t>(cost.get(), pref.get(), n, tmp, C.stream);
   int64_t h[2];
   HM_CUDA(cudaMemcpyAsync(&h[0], pref.get() + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
   HM_CUDA(cudaMemcpyAsync(&h[1], cost.get() + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, C.stream));
@@ -496,10 +486,9 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   k_morton<<<grid_for(N, 256), 256, 0, st>>>(cen.get(), N, gbox.get(), C.codes_app.get(), idx.get());
   HM_CHECK_LAUNCH();
   DBuf<char>& tmp = ws.tmp;
-  cub_call(tmp, [&](void* t, size_t& b) {   // LSD radix sort: stable, ties keep ascending index (A7)
-    return cub::DeviceRadixSort::SortPairs(t, b, C.codes_app.get(), code_sorted.get(), idx.get(),
-                                           C.perm.get(), (int)N, 0, 63, st);
-  });
+  // LSD radix sort: stable, ties keep ascending index (A7)
+  prim::radix_sort_pairs<uint64_t, int32_t>(C.codes_app.get(), code_sorted.get(), idx.get(), C.perm.get(), N, 0, 63,
+                                            tmp, st);
   C.panel.alloc(C.npanel);
   if (C.quad) {
     C.qnode.alloc(N);
@@ -529,9 +518,7 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
     int64_t b = lev[level], e = lev[level + 1], n = e - b;
     k_split_flags<<<grid_for(n, 256), 256, 0, st>>>(C.cl_lo.get(), C.cl_hi.get(), b, e, leaf_size, flag.get());
     HM_CHECK_LAUNCH();
-    cub_call(tmp, [&](void* t, size_t& bytes) {
-      return cub::DeviceScan::ExclusiveSum(t, bytes, flag.get(), scan.get(), (int)n, st);
-    });
+    prim::exclusive_scan<int32_t>(flag.get(), scan.get(), n, tmp, st);
     k_split_emit<<<grid_for(n, 256), 256, 0, st>>>(C.cl_lo.get(), C.cl_hi.get(), C.cl_child.get(),
                                                     C.cl_depth.get(), b, e, flag.get(), scan.get(), level);
     HM_CHECK_LAUNCH();
@@ -594,16 +581,8 @@ void build_tree(Context& C, const hm_mesh& mesh, int leaf_size, double eta) {
   C.adm.alloc(nadm); C.dense.alloc(nden);
   DBuf<uint64_t>& ksorted = ws.ksorted;
   ksorted.alloc(std::max(nadm, nden));
-  if (nadm)
-    cub_call(tmp, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, admk.get(), ksorted.get(), admq.get(), C.adm.get(), (int)nadm,
-                                             0, 64, st);
-    });
-  if (nden)
-    cub_call(tmp, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, denk.get(), ksorted.get(), denq.get(), C.dense.get(), (int)nden,
-                                             0, 64, st);
-    });
+  if (nadm) prim::radix_sort_pairs<uint64_t, Quad>(admk.get(), ksorted.get(), admq.get(), C.adm.get(), nadm, 0, 64, tmp, st);
+  if (nden) prim::radix_sort_pairs<uint64_t, Quad>(denk.get(), ksorted.get(), denq.get(), C.dense.get(), nden, 0, 64, tmp, st);
   HM_CUDA(cudaEventRecord(ev[5], st));
   // ---- leaf partition over ranks (A18)
   partition_list(C, C.adm, nadm, 0, C.adm_begin, C.adm_end, tmp);
