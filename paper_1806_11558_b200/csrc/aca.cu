@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <type_traits>
 
 #include "entry_batch.cuh"
 #include "primitives.cuh"
@@ -502,9 +503,29 @@ __global__ void k_final_sizes(const AcaBlk* __restrict__ B, const AcaState* __re
   if (st.status == 2) ovf[atomicAdd(novf, 1ull)] = owned[c];
 }
 // pack finished blocks: [U (m x k) | V (n x k)] column-major, straight copies of the
-// first k workspace columns (T = float: option lr_f32, each entry rounded to binary32 once);
-// one CTA per block.  The copy also checks every factor entry for finiteness (hm.h:
-// HM_ERR_NUMERIC names the first offending block): bad = min owned index.
+// first k workspace columns (T = float: option lr_f32, each entry rounded to binary32 once).
+// The copy also checks every factor entry for finiteness (hm.h: HM_ERR_NUMERIC names the first
+// offending block): bad = min owned index.  G threads per block: a warp per small block
+// (k_aca_store<.., 32>, 8 blocks per CTA), a CTA per big block (m + n >= kBigMN, list `big`).
+template <class T, int G>
+__device__ __forceinline__ void aca_store_block(const AcaBlk& b, const AcaState& st, int64_t c,
+                                                const int32_t* __restrict__ owned, const int64_t* __restrict__ fpre,
+                                                int64_t base, const double* __restrict__ Uw,
+                                                const double* __restrict__ Vw, T* __restrict__ pool,
+                                                int64_t* __restrict__ foff, int32_t* __restrict__ frank,
+                                                int32_t* __restrict__ bad, int tid) {
+  const int64_t o = base + fpre[c];
+  const int64_t mu = (int64_t)st.k * b.m, nv = (int64_t)st.k * b.n;
+  bool fin = true;
+  for (int64_t x = tid; x < mu; x += G) { const T a = (T)Uw[b.uoff + x]; fin &= isfinite(a); pool[o + x] = a; }
+  for (int64_t x = tid; x < nv; x += G) { const T a = (T)Vw[b.voff + x]; fin &= isfinite(a); pool[o + mu + x] = a; }
+  if (!fin) atomicMin(bad, owned[c]);
+  if (tid == 0) {
+    foff[owned[c]] = o;
+    frank[owned[c]] = st.k;
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) k_aca_store(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S,
                                                    int64_t nb, const int32_t* __restrict__ owned,
@@ -512,25 +533,26 @@ __global__ void __launch_bounds__(256) k_aca_store(const AcaBlk* __restrict__ B,
                                                    const double* __restrict__ Uw, const double* __restrict__ Vw,
                                                    T* __restrict__ pool, int64_t* __restrict__ foff,
                                                    int32_t* __restrict__ frank, int32_t* __restrict__ bad) {
-  const int64_t c = blockIdx.x;
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (c >= nb) return;
   const AcaState st = S[c];
-  if (st.status != 1) return;
   const AcaBlk b = B[c];
-  const int64_t o = base + fpre[c];
-  const int64_t mu = (int64_t)st.k * b.m, nv = (int64_t)st.k * b.n;
-  bool fin = true;
-  for (int64_t x = threadIdx.x; x < mu; x += blockDim.x) { const T a = (T)Uw[b.uoff + x]; fin &= isfinite(a); pool[o + x] = a; }
-  for (int64_t x = threadIdx.x; x < nv; x += blockDim.x) { const T a = (T)Vw[b.voff + x]; fin &= isfinite(a); pool[o + mu + x] = a; }
-  if (!fin) atomicMin(bad, owned[c]);
-  if (threadIdx.x == 0) {
-    foff[owned[c]] = o;
-    frank[owned[c]] = st.k;
-  }
+  if (st.status != 1 || b.m + b.n >= kBigMN) return;
+  aca_store_block<T, 32>(b, st, c, owned, fpre, base, Uw, Vw, pool, foff, frank, bad, threadIdx.x & 31);
 }
 
-
-
+template <class T>
+__global__ void __launch_bounds__(256) k_aca_store_big(const AcaBlk* __restrict__ B, const AcaState* __restrict__ S,
+                                                       const int32_t* __restrict__ big, const int32_t* __restrict__ owned,
+                                                       const int64_t* __restrict__ fpre, int64_t base,
+                                                       const double* __restrict__ Uw, const double* __restrict__ Vw,
+                                                       T* __restrict__ pool, int64_t* __restrict__ foff,
+                                                       int32_t* __restrict__ frank, int32_t* __restrict__ bad) {
+  const int64_t c = big[blockIdx.x];
+  const AcaState st = S[c];
+  if (st.status != 1) return;
+  aca_store_block<T, 256>(B[c], st, c, owned, fpre, base, Uw, Vw, pool, foff, frank, bad, threadIdx.x);
+}
 
 // one batch of residual entries (row or column step): order-3 in place, then the order-4
 // list, then the rest; the batch size *dtot lives on the device, `upper` bounds it (grid size)
@@ -707,14 +729,18 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   const int64_t base = (int64_t)(C.fpool.used / esz);
   C.fpool.ensure((base + add) * esz + 64);
   C.fpool.used = (base + add) * esz;
-  if (esz == 4)
-    k_aca_store<float><<<(unsigned)nb, 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(), base,
-                                                     Uw, Vw, (float*)C.fpool.base, C.foff.get(), C.frank.get(),
-                                                     W.bad.get());
-  else
-    k_aca_store<double><<<(unsigned)nb, 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(),
-                                                      base, Uw, Vw, (double*)C.fpool.base, C.foff.get(), C.frank.get(),
-                                                      W.bad.get());
+  auto store = [&](auto* pool) {
+    using T = std::remove_pointer_t<decltype(pool)>;
+    k_aca_store<T><<<grid_for(nb * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), nb, W.owned.get(), W.rpre.get(),
+                                                           base, Uw, Vw, pool, C.foff.get(), C.frank.get(), W.bad.get());
+    HM_CHECK_LAUNCH();
+    if (nbig)
+      k_aca_store_big<T><<<(unsigned)nbig, 256, 0, st>>>(W.blk.get(), W.state.get(), W.big.get(), W.owned.get(),
+                                                         W.rpre.get(), base, Uw, Vw, pool, C.foff.get(), C.frank.get(),
+                                                         W.bad.get());
+  };
+  if (esz == 4) store((float*)C.fpool.base);
+  else store((double*)C.fpool.base);
   HM_CHECK_LAUNCH();
   if (nov) {
     const size_t o0 = overflow.size();

@@ -17,6 +17,8 @@ V, T = config_mesh(cfg)
 H = HMatrix(device=0)
 H.build_tree(V, T, 32, 1.0)
 H.set_option("lr_f32", f32)
+if len(sys.argv) > 4:
+    H.set_option("mv_concurrent", int(sys.argv[4]))
 H.setup(1e-6)
 x = torch.randn(T.shape[0], dtype=torch.float64, device="cuda")
 ts = []

@@ -51,6 +51,9 @@ def main():
         out["near_rate_Gps"] = round(st["evals_near"] / (out["eval_near_ms"] * 1e-3) / 1e9, 2)
         out["aca_rate_Gps"] = round(st["evals_aca"] / (out["eval_aca_ms"] * 1e-3) / 1e9, 2)
         out["k_mean"] = st["k_mean"]
+        for k in ("aca_phase_ms", "plan_phase_ms", "plan_ms", "aca_steps", "aca_chunks", "aca_overflow", "tree_ms"):
+            if k in st:
+                out[k] = st[k]
         print(json.dumps(out), flush=True)
     H.close()
 
