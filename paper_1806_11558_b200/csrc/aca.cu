@@ -114,6 +114,7 @@ struct AcaMap {
   int64_t nb;
   double* Uw;
   double* Vw;
+  int raw;              // option aca_split: store the raw entry, k_aca_correct applies the corrections
   __device__ bool locate(int64_t e, bool valid, EntryRef& r) const {
     if (!valid) return false;
     int64_t a = tab[e >> 5];
@@ -130,44 +131,14 @@ struct AcaMap {
     s = ROW ? b.q.rlo + st.i : b.q.rlo + r.idx;
     t = ROW ? b.q.clo + r.idx : b.q.clo + st.js;
   }
-  // Early residual-correction operands (option aca_early = KE): the first min(k, KE) pairs
-  // (U[i, l], V[j, l]) are loaded before the quadrature, so their latency hides behind it;
-  // put_early() then applies a = a - U V in the same order and rounding as put().
-  template <int KE>
-  __device__ __forceinline__ int early(EntryRef r, double (&eu)[KE > 0 ? KE : 1], double (&ev)[KE > 0 ? KE : 1]) const {
-    if (KE == 0) return 0;
-    const AcaBlk& b = B[r.seg];
-    const AcaState& st = S[r.seg];
-    const int ke = min(st.k, KE);
-#pragma unroll
-    for (int l = 0; l < KE; ++l)
-      if (l < ke) {
-        eu[l] = ROW ? Uw[b.uoff + st.i + (int64_t)l * b.m] : Uw[b.uoff + r.idx + (int64_t)l * b.m];
-        ev[l] = ROW ? Vw[b.voff + r.idx + (int64_t)l * b.n] : Vw[b.voff + st.js + (int64_t)l * b.n];
-      }
-    return ke;
-  }
-  template <int KE>
-  __device__ __forceinline__ void put_early(EntryRef r, double a, int ke, const double (&eu)[KE > 0 ? KE : 1],
-                                            const double (&ev)[KE > 0 ? KE : 1]) const {
-    const AcaBlk& b = B[r.seg];
-    const AcaState st = S[r.seg];
-#pragma unroll
-    for (int l = 0; l < KE; ++l)
-      if (l < ke) a = dsub(a, dmul(eu[l], ev[l]));
-    const double* U = Uw + b.uoff;
-    const double* V = Vw + b.voff;
-    if (ROW) {
-      for (int l = ke; l < st.k; ++l) a = dsub(a, dmul(U[st.i + (int64_t)l * b.m], V[r.idx + (int64_t)l * b.n]));
-      Vw[b.voff + (int64_t)st.k * b.n + r.idx] = a;
-    } else {
-      for (int l = ke; l < st.k; ++l) a = dsub(a, dmul(U[r.idx + (int64_t)l * b.m], V[st.js + (int64_t)l * b.n]));
-      Uw[b.uoff + (int64_t)st.k * b.m + r.idx] = a;
-    }
-  }
   __device__ void put(EntryRef r, double a) const {
     const AcaBlk& b = B[r.seg];
     const AcaState st = S[r.seg];
+    if (raw) {
+      if (ROW) Vw[b.voff + (int64_t)st.k * b.n + r.idx] = a;
+      else Uw[b.uoff + (int64_t)st.k * b.m + r.idx] = a;
+      return;
+    }
     const double* U = Uw + b.uoff;
     const double* V = Vw + b.voff;
     if (ROW) {
@@ -179,6 +150,30 @@ struct AcaMap {
     }
   }
 };
+
+// option aca_split: the residual corrections r = a - sum_l U V (l ascending, A15) of a step's
+// raw entries as a separate streaming pass, one thread per entry (grid-stride over the
+// step's device-side total), instead of inside the FP64-bound evaluation kernels
+template <bool ROW>
+__global__ void __launch_bounds__(256) k_aca_correct(AcaMap<ROW> m, const int64_t* __restrict__ dtot) {
+  const int64_t total = *dtot;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    EntryRef r;
+    if (!m.locate(e, true, r)) continue;
+    const AcaBlk& b = m.B[r.seg];
+    const AcaState st = m.S[r.seg];
+    if (st.k == 0) continue;
+    double* dst = ROW ? m.Vw + b.voff + (int64_t)st.k * b.n + r.idx : m.Uw + b.uoff + (int64_t)st.k * b.m + r.idx;
+    double a = *dst;
+    const double* U = m.Uw + b.uoff;
+    const double* V = m.Vw + b.voff;
+    if (ROW)
+      for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[st.i + (int64_t)l * b.m], V[r.idx + (int64_t)l * b.n]));
+    else
+      for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[r.idx + (int64_t)l * b.m], V[st.js + (int64_t)l * b.n]));
+    *dst = a;
+  }
+}
 
 __device__ __forceinline__ void warp_argmax(double& v, int& idx) {
 #pragma unroll
@@ -563,12 +558,7 @@ void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWor
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 3 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4);   // one wave, persistent
-  switch (C.aca_early) {
-    case 2: k_eval_class3<M, 2><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
-    case 4: k_eval_class3<M, 4><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
-    case 8: k_eval_class3<M, 8><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
-    default: k_eval_class3<M, 0><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get()); break;
-  }
+  k_eval_class3<M><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
   const unsigned g4 = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 16);
   k_eval_list<4, M><<<g4, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
@@ -668,10 +658,18 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     ks.reset();
     if (C.quad)
       aca_eval(C, AcaMap<true, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(),
-                                     nb, Uw, Vw}, drow, rmax, W);
+                                     nb, Uw, Vw, 0}, drow, rmax, W);
     else
-      aca_eval(C, AcaMap<true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
-                               W.rtab.get(), nb, Uw, Vw}, drow, rmax, W);
+    {
+      const AcaMap<true> mr{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
+                            W.rtab.get(), nb, Uw, Vw, C.aca_split};
+      aca_eval(C, mr, drow, rmax, W);
+      if (C.aca_split) {
+        KScope kc(C, KF_ACA_OTHER);
+        k_aca_correct<true><<<(unsigned)std::min<int64_t>(grid_for(rmax, 256), 148 * 8), 256, 0, st>>>(mr, drow);
+        HM_CHECK_LAUNCH();
+      }
+    }
     ks.reset(new KScope(C, KF_ACA_OTHER));
     k_aca_pivot<<<grid_for(nact_ub * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Vw,
                                                              W.bmap.get());
@@ -683,10 +681,18 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     ks.reset();
     if (C.quad)
       aca_eval(C, AcaMap<false, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(),
-                                      nb, Uw, Vw}, dcol, cmax, W);
+                                      nb, Uw, Vw, 0}, dcol, cmax, W);
     else
-      aca_eval(C, AcaMap<false>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(),
-                                W.ctab.get(), nb, Uw, Vw}, dcol, cmax, W);
+    {
+      const AcaMap<false> mc{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(),
+                             W.ctab.get(), nb, Uw, Vw, C.aca_split};
+      aca_eval(C, mc, dcol, cmax, W);
+      if (C.aca_split) {
+        KScope kc(C, KF_ACA_OTHER);
+        k_aca_correct<false><<<(unsigned)std::min<int64_t>(grid_for(cmax, 256), 148 * 8), 256, 0, st>>>(mc, dcol);
+        HM_CHECK_LAUNCH();
+      }
+    }
     ks.reset(new KScope(C, KF_ACA_OTHER));
     k_aca_update<<<grid_for(nact_ub * 32, 64), 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Uw, Vw,
                                                             W.bmap.get(), W.piv.get(), kws, C.eps_aca);

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
 //   k_eval_rest     persistent, the remaining few (orders 5, 6, touching pairs).
 // one 32-entry group of a warp (lanes e = e0 + lane): classify, append non-order-3 entries,
 // evaluate order 3 in place
-template <int KE, class M>
+template <class M>
 __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t total, int lane, EntryRef* __restrict__ lists,
                                              unsigned long long* __restrict__ cnt, unsigned long long& ev) {
   EntryRef r;
@@ -189,9 +189,7 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
   if (cls == 4) lists[base4 + __popc(b4 & below)] = r;
   else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
   if (cls == 3) {
-    double eu[KE > 0 ? KE : 1], evv[KE > 0 ? KE : 1];
-    const int ke = m.template early<KE>(r, eu, evv);      // correction operands, loaded ahead
-    m.template put_early<KE>(r, map_regular<3>(m, xs, ys), ke, eu, evv);
+    m.put(r, map_regular<3>(m, xs, ys));
     ev += M::kQuad ? 81 : tri_rule_points(3) * tri_rule_points(3);
   }
 }
@@ -201,7 +199,7 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
 // one thread per entry leave SMs idle at the tail: C4 ACA evaluation 1.85 s resp. 1.75 s vs
 // 1.61 s, profiles/r02_setup_ab1.jsonl)
 constexpr int kDynGroups = 4;
-template <class M, int KE = 0>
+template <class M>
 __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __restrict__ dtot,
                                                      EntryRef* __restrict__ lists,
                                                      unsigned long long* __restrict__ cnt /* [n4, nrest, next] */,
@@ -215,7 +213,7 @@ __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __re
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     if ((int64_t)b0 >= total) break;
 #pragma unroll 1
-    for (int g = 0; g < kDynGroups; ++g) class3_group<KE>(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
+    for (int g = 0; g < kDynGroups; ++g) class3_group(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);

@@ -47,11 +47,7 @@ struct NearMap {
     t = Q.clo + r.idx % ncol;
   }
   __device__ void put(EntryRef r, double a) const { store[off[r.seg] + r.idx] = a; }
-  template <int KE>
-  __device__ int early(EntryRef, double (&)[KE > 0 ? KE : 1], double (&)[KE > 0 ? KE : 1]) const { return 0; }
-  template <int KE>
-  __device__ void put_early(EntryRef r, double a, int, const double (&)[KE > 0 ? KE : 1],
-                            const double (&)[KE > 0 ? KE : 1]) const { put(r, a); }
+
 };
 
 // bad[0] = number of non-finite entries, bad[1] = smallest offset of one (if any)
