@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <type_traits>
 
 #include "entry_batch.cuh"
@@ -581,21 +582,52 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
   std::vector<int32_t>& hbig = W.h_big;
   hbig.clear();
   int64_t uo = 0, vo = 0, bo = 0, rmax = 0, cmax = 0;   // rmax / cmax: entries of the first row / column step
-  for (int64_t c = 0; c < nb; ++c) {
-    const Quad& q = C.h_adm[C.adm_begin + ids[c]];
-    AcaBlk& b = hb[c];
-    b.q = q;
-    b.m = q.rhi - q.rlo;
-    b.n = q.chi - q.clo;
-    b.kmax = std::min(std::min(b.m, b.n), C.k_max);
-    b.pad = 0;
-    b.uoff = uo; b.voff = vo; b.boff = bo;
-    uo += (int64_t)b.m * kws;
-    vo += (int64_t)b.n * kws;
-    bo += (b.m + 31) / 32;
-    rmax += b.n;
-    cmax += b.m;
-    if (b.m + b.n >= kBigMN) hbig.push_back((int32_t)c);
+  {
+    // block records and workspace offsets on host threads over contiguous slices (two passes:
+    // per-slice sizes, then the slices' offsets), the big-block list in slice order
+    const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency() / std::max(1, C.world));
+    const int T = (int)std::max<int64_t>(1, std::min<int64_t>({hw, 8, nb / 50000 + 1}));
+    struct Part { int64_t u = 0, v = 0, b = 0, r = 0, c = 0; std::vector<int32_t> big; };
+    std::vector<Part> part(T);
+    auto slice = [&](int t, bool fill, const Part& off) {
+      const int64_t c0 = nb * t / T, c1 = nb * (t + 1) / T;
+      Part acc = off;
+      for (int64_t c = c0; c < c1; ++c) {
+        const Quad& q = C.h_adm[C.adm_begin + ids[c]];
+        const int32_t m = q.rhi - q.rlo, n = q.chi - q.clo;
+        if (fill) {
+          AcaBlk& b = hb[c];
+          b.q = q;
+          b.m = m;
+          b.n = n;
+          b.kmax = std::min(std::min(m, n), C.k_max);
+          b.pad = 0;
+          b.uoff = acc.u; b.voff = acc.v; b.boff = acc.b;
+        } else if (m + n >= kBigMN) {
+          part[t].big.push_back((int32_t)c);
+        }
+        acc.u += (int64_t)m * kws;
+        acc.v += (int64_t)n * kws;
+        acc.b += (m + 31) / 32;
+        acc.r += n;
+        acc.c += m;
+      }
+      if (!fill) { part[t].u = acc.u; part[t].v = acc.v; part[t].b = acc.b; part[t].r = acc.r; part[t].c = acc.c; }
+    };
+    auto run = [&](auto&& f) {
+      std::vector<std::thread> th;
+      for (int t = 1; t < T; ++t) th.emplace_back([&, t]() { f(t); });
+      f(0);
+      for (auto& x : th) x.join();
+    };
+    run([&](int t) { part[t].big.clear(); slice(t, false, Part{}); });
+    std::vector<Part> off(T);
+    for (int t = 0; t < T; ++t) {
+      off[t].u = uo; off[t].v = vo; off[t].b = bo;
+      uo += part[t].u; vo += part[t].v; bo += part[t].b; rmax += part[t].r; cmax += part[t].c;
+      hbig.insert(hbig.end(), part[t].big.begin(), part[t].big.end());
+    }
+    run([&](int t) { slice(t, true, off[t]); });
   }
   const int64_t nbig = (int64_t)hbig.size();
   W.blk.alloc(nb); W.state.alloc(nb); W.owned.alloc(nb); W.piv.alloc(nb * 2 * kws);

@@ -114,8 +114,11 @@ struct PinnedVec {
     n = m;
   }
   T* data() { return p; }
+  const T* data() const { return p; }
   size_t size() const { return n; }
+  void clear() { n = 0; }
   T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
 };
 
 // Growable device pool backed by CUDA virtual memory management: one reserved VA range,
@@ -249,7 +252,7 @@ struct Context {
   // leaves (canonical DFS order)
   int64_t nadm = 0, ndense = 0;
   DBuf<Quad> adm, dense;
-  std::vector<Quad> h_adm, h_dense;
+  PinnedVec<Quad> h_adm, h_dense;   // host copies of the leaf lists (pinned: fast D2H each setup)
   int64_t adm_begin = 0, adm_end = 0, dense_begin = 0, dense_end = 0;
 
   // setup state
