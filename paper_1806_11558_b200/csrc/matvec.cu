@@ -30,6 +30,9 @@
 namespace hm {
 
 constexpr int kMvStageBytes = 48 * 1024;   // one k_mv_batched pipeline stage (= one batch)
+// stage bytes of option mv_kernel: 0 two CTAs x 2 x 48 KiB (default), 1 one CTA x 4 x 48 KiB,
+// 2 two CTAs x 3 x 36 KiB, 3 two CTAs x 2 x 56 KiB
+inline int64_t mv_stage_bytes(const Context& C) { return C.mv_kind == 2 ? 36 * 1024 : C.mv_kind == 3 ? 56 * 1024 : kMvStageBytes; }
 constexpr int kMaxX = 12;         // x_sigma ranges (bulk copies) per batch
 constexpr int64_t kXGap = 64;     // doubles: merge x ranges closer than this
 
@@ -547,7 +550,7 @@ namespace {
 void plan_dense_part(Context& C, PlanWs& W, PlanPart& P, int64_t i0, int64_t i1) {
   P.clear();
   P.items.reserve(i1 - i0);
-  const int64_t cap = kMvStageBytes;
+  const int64_t cap = mv_stage_bytes(C);
   const int64_t* hoff = W.hoff.data();
   for (int64_t b = i0; b < i1; ++b) {
     const Quad& q = C.h_dense[C.dense_begin + b];
@@ -564,7 +567,7 @@ void plan_lowrank_part(Context& C, PlanWs& W, PlanPart& P, int64_t i0, int64_t i
   P.clear();
   P.items.reserve(i1 - i0);
   P.lr_esz = C.lr_esz;
-  const int64_t cap = kMvStageBytes, esz = C.lr_esz;
+  const int64_t cap = mv_stage_bytes(C), esz = C.lr_esz;
   for (int64_t i = i0; i < i1; ++i) {
     const int64_t b = W.lr_order[i];
     const Quad& q = C.h_adm[C.adm_begin + b];
@@ -700,7 +703,7 @@ void plan_matvec(Context& C) {
   // byte-balanced contiguous batch ranges, one per persistent CTA (two or one per SM)
   int sms = 148;
   HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, C.device));
-  const int G = std::max(1, std::min<int>(C.mv_kind == 0 ? 2 * sms : sms, (int)nbat));
+  const int G = std::max(1, std::min<int>(C.mv_kind == 1 ? sms : 2 * sms, (int)nbat));
   W.cta.resize(G + 1);
   {
     double tot = 0;
@@ -769,6 +772,10 @@ void plan_matvec(Context& C) {
                                  256 + 2 * kMvStageBytes));
     HM_CUDA(cudaFuncSetAttribute(k_mv_batched<4, kMvStageBytes, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  256 + 4 * kMvStageBytes));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<3, 36 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 3 * 36 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<2, 56 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 2 * 56 * 1024));
     attr = true;
   }
 }
@@ -834,6 +841,14 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
     const int64_t scramble = C.mv_scramble ? C.N - 4096 : 0;
     if (C.mv_kind == 0)      // two CTA rings per SM, 2 x 48 KiB stages, 7 consumer warps each
       k_mv_batched<2, kMvStageBytes, 256, 2><<<C.mv_grid, 256, 256 + 2 * kMvStageBytes, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
+    else if (C.mv_kind == 2)
+      k_mv_batched<3, 36 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 3 * 36 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
+    else if (C.mv_kind == 3)
+      k_mv_batched<2, 56 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 2 * 56 * 1024, st>>>(
           C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
           (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
     else                     // one CTA ring per SM, 4 x 48 KiB stages, 15 consumer warps
