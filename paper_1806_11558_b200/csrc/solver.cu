@@ -21,9 +21,10 @@ namespace {
 constexpr int kRedBlocks = 296;
 constexpr int kRedThreads = 256;
 
-// partial dot products of w against nv vectors V[i] (stride ld), for i < nv; partial[b*nv + i]
+// partial dot products of w against nv vectors V[i] (stride ld), for i < nv; partial[b*nv + i];
+// extra != nullptr: the last one (i = nv - 1) is extra^T w instead of V[nv-1]^T w
 __global__ void k_mdot(const double* __restrict__ Vb, int64_t ld, int nv, const double* __restrict__ w, int64_t n,
-                       double* __restrict__ partial) {
+                       double* __restrict__ partial, const double* __restrict__ extra) {
   __shared__ double sh[kRedThreads / 32][33];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   for (int i0 = 0; i0 < nv; i0 += 32) {
@@ -35,7 +36,7 @@ __global__ void k_mdot(const double* __restrict__ Vb, int64_t ld, int nv, const 
       const double wt = w[t];
 #pragma unroll
       for (int q = 0; q < 32; ++q)
-        if (q < cnt) acc[q] += Vb[(int64_t)(i0 + q) * ld + t] * wt;
+        if (q < cnt) acc[q] += (extra && i0 + q == nv - 1 ? extra[t] : Vb[(int64_t)(i0 + q) * ld + t]) * wt;
     }
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
@@ -125,11 +126,11 @@ struct Red {
   DBuf<double> part, out;
   Red(Context& c, const Layout& l) : C(c), L(l) {}
   // out[0..nv) = V[i]^T w (global) on the device; returns device pointer
-  double* mdot(const double* Vb, int64_t ld, int nv, const double* w) {
+  double* mdot(const double* Vb, int64_t ld, int nv, const double* w, const double* extra = nullptr) {
     part.alloc((size_t)kRedBlocks * nv);
     out.alloc(nv + 8);
     { KScope ks_(C, KF_KRYLOV);
-    k_mdot<<<kRedBlocks, kRedThreads, 0, C.stream>>>(Vb, ld, nv, w, L.n, part.get());
+    k_mdot<<<kRedBlocks, kRedThreads, 0, C.stream>>>(Vb, ld, nv, w, L.n, part.get(), extra);
     }
     { KScope ks_(C, KF_KRYLOV);
     k_mdot_final<<<(nv + 127) / 128, 128, 0, C.stream>>>(part.get(), kRedBlocks, nv, out.get());
@@ -217,7 +218,7 @@ void gmres(Context& C, const Layout& L, const double* b, double* x, double tol, 
   Red R(C, L);
   DBuf<double> hdev, hsum;
   hdev.alloc(m + 8);
-  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), h(m + 1), h2(m + 1), y(m);
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), h(m + 1), h2(m + 2), y(m);
   HM_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st));
   const double bn = std::sqrt(R.dot(b, b));
   int total = 0;
@@ -249,15 +250,19 @@ void gmres(Context& C, const Layout& L, const double* b, double* x, double tol, 
       }
       HM_CHECK_LAUNCH();
       HM_CUDA(cudaMemcpyAsync(h.data(), d1, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
-      double* d2 = R.mdot(Vb, ld, j + 1, w);
+      // second projection and ||w'||^2 in one reduction (one all-reduce, one host sync per
+      // iteration): ||w' - V h2||^2 = ||w'||^2 - ||h2||^2 for orthonormal V, and h2 is ~1e-8
+      // ||w'|| after the first projection, so the difference does not cancel
+      double* d2 = R.mdot(Vb, ld, j + 2, w, w);
       { KScope ks_(C, KF_KRYLOV);
       k_msub<<<vgrid(N), 256, 0, st>>>(Vb, ld, j + 1, d2, w, N);
       }
       HM_CHECK_LAUNCH();
-      HM_CUDA(cudaMemcpyAsync(h2.data(), d2, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+      HM_CUDA(cudaMemcpyAsync(h2.data(), d2, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
       HM_CUDA(cudaStreamSynchronize(st));
-      for (int i = 0; i <= j; ++i) h[i] += h2[i];
-      const double hn = std::sqrt(R.dot(w, w));
+      double hh2 = 0.0;
+      for (int i = 0; i <= j; ++i) { h[i] += h2[i]; hh2 += h2[i] * h2[i]; }
+      const double hn = std::sqrt(std::max(0.0, h2[j + 1] - hh2));
       for (int i = 0; i < j; ++i) {
         const double t1 = cs[i] * h[i] + sn[i] * h[i + 1];
         const double t2 = -sn[i] * h[i] + cs[i] * h[i + 1];
