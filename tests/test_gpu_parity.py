@@ -338,3 +338,46 @@ def test_lobed_surface_full_path(O, torch_cuda):
     xo = R.gmres(f, tol=1e-10)[0]
     assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-5 * np.linalg.norm(xo)
     H.close()
+
+
+@pytest.mark.parametrize("case", ["one_panel", "two_panels", "below_one_leaf", "leaf_size_1"])
+def test_degenerate_sizes(O, torch_cuda, case):
+    """Degenerate cases of the method: a single panel (the whole H is one 1 x 1 dense leaf: the
+    closed-form self term), two panels, a mesh smaller than one leaf (N <= C_leaf: one dense
+    leaf, no admissible block), and C_leaf = 1 (a tree down to single panels, admissible blocks
+    of 1 x 1).  Tree bit-exact, every stored entry equal to the oracle's, H-matvec equal to the
+    oracle's and GMRES solution equal to the oracle's."""
+    V, T = icosphere(1)                                       # 80 triangles
+    leaf = 32
+    if case == "one_panel":
+        T = T[:1].copy()
+    elif case == "two_panels":
+        T = T[:2].copy()
+    elif case == "below_one_leaf":
+        T = T[:20].copy()
+    else:
+        leaf = 1
+    N = T.shape[0]
+    H = _gpu(V, T, leaf=leaf)
+    H.set_option("record_pivots", 1)
+    R = _compare_tree(O, H, V, T, leaf=leaf)
+    H.setup(EPS)
+    R.assemble(EPS)
+    # a box of zero diameter is admissible against itself (A4/A5: min(D, D) <= eta^2 G with
+    # D = G = 0): one panel gives one 1 x 1 ACA block, C_leaf = 1 only 1 x 1 ACA blocks (the
+    # singular classes then go through ACA); the others have only dense leaves
+    nadm = {"one_panel": 1, "two_panels": 0, "below_one_leaf": 0}.get(case)
+    if nadm is not None:
+        assert H.stats()["adm_leaves"] == nadm
+    else:
+        assert H.stats()["dense_leaves"] == 0
+    _check_blocks(H, R)
+    x = seeded_vector(N, 5)
+    yg = H.matvec(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+    yo = R.matvec(x)
+    assert np.linalg.norm(yg - yo) <= 1e-12 * np.linalg.norm(yo)
+    f = R.rhs(1) if case != "one_panel" else R.rhs(0)
+    sol, it, rr = H.solve(torch_cuda.from_numpy(f).cuda(), tol=1e-10)
+    xo = R.gmres(f, tol=1e-10)[0]
+    assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-10 * np.linalg.norm(xo)
+    H.close()
