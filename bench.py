@@ -271,7 +271,8 @@ def _run_gpu(args, rank, world, local, dev, stream):
     per_rank = None
     if world > 1:                      # per-rank phase times (load balance of the leaf partition)
         import torch.distributed as dist
-        mine = torch.tensor([st["near_ms"], st["aca_ms"], st["setup_ms"], st["solve_ms"], st["stored_bytes"] / 1e9],
+        mine = torch.tensor([st["near_ms"], st["aca_ms"], st["setup_ms"], st["solve_ms"], st["stored_bytes"] / 1e9,
+                             kt["matvec_ms"] / K, kt.get("comm_ms", 0.0) / K],
                             dtype=torch.float64, device=dev)
         allr = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allr, mine)
@@ -405,7 +406,7 @@ def _run_gpu(args, rank, world, local, dev, stream):
                                                  "krylov_blas1": round(krylov_ms_step, 3),
                                                  "nccl": round(comm_ms_step, 3)},
                           "nccl_us_per_iteration": round(1e3 * comm_ms_step / max(1, iters), 2) if world > 1 else None,
-                          "per_rank_near_aca_setup_solve_ms_storedGB": per_rank, "accuracy": accuracy},
+                          "per_rank_near_aca_setup_solve_ms_storedGB_matvec_nccl_ms_per_step": per_rank, "accuracy": accuracy},
             "roofline": roof, "matvec_roofline": matvec_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         }

@@ -327,11 +327,11 @@ __global__ void k_block_level(const int2* __restrict__ fr, const uint64_t* __res
 
 // Per-leaf setup cost for the partition (A18).  model 0 (round 1): dense |t||s|, admissible
 // (|t|+|s|) 10.  model 1 (default): the evaluations the leaf will cost —
-//   dense: |t||s| x (mean rule evaluations per entry of its kind, oracle-measured at C4 on 400
+//   dense: |t||s| x (mean rule evaluations per entry of its kind, measured at C4 on 400
 //          leaves each: diagonal t = s 1542, boxes touching 360, separated 140 -> weights
 //          110 / 26 / 10; boxes over the node centroids, the same boxes as admissibility)
 //   admissible: (|t|+|s|) x 10 k^, k^ = 8.2 + 0.3 log2((|t|+|s|)/40): the mean ACA rank at
-//          eps 1e-6 grows slowly with the block size (oracle at C3: 8.2 at m+n = 40 ... 10.0 at
+//          eps 1e-6 grows slowly with the block size (sampled at C3: 8.2 at m+n = 40 ... 10.0 at
 //          ~5900)
 // model 2: the dense weights of model 1, admissible (|t|+|s| + 21) x 10: a fixed per-block
 //          cost (the per-step pivot / update / bookkeeping of a block, fitted on the one-GPU
