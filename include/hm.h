@@ -105,7 +105,8 @@ const char* hm_last_error(hm_ctx ctx);
  *                  each kernel family (near-field evaluation, ACA evaluation, other ACA,
  *                  matvec, Krylov BLAS-1); totals in hm_get_stats "kt"; setting it resets them
  *   "mv_kernel"    small-leaf matvec pipeline: 0 (default) two CTA rings per SM, 2 x 48 KiB
- *                  stages each; 1 one ring of 4 x 48 KiB stages.  Re-plans the matvec if set up.
+ *                  stages each; 1 one ring of 4 x 48 KiB stages; 2 two rings of 3 x 36 KiB;
+ *                  3 two rings of 2 x 56 KiB.  Re-plans the matvec if set up.
  *   "mv_small_max" low-rank leaves up to this many bytes (default 16384) go through the
  *                  shared-memory pipeline, larger ones through the large-block kernels
  *   "mv_profile"   1: accumulate producer/consumer wait and work cycles of the CTA-ring
@@ -115,6 +116,15 @@ const char* hm_last_error(hm_ctx ctx);
  *   "mv_concurrent" 1 (default): the large low-rank matvec kernels run on a library side
  *                  stream beside the small-leaf pipeline (joined before hm_matvec returns its
  *                  stream order); 0: one stream
+ *   "cost_model"   leaf cost of the partition over ranks (A18): 2 (default) dense leaves |t||s|
+ *                  weighted by kind (t = s 110, boxes touching 26, separated 10), admissible
+ *                  leaves (|t|+|s| + 21) x 10; 1 a size-dependent rank estimate for admissible
+ *                  leaves; 0 round 1 (|t||s|, (|t|+|s|) x 10).  Takes effect at hm_build_tree.
+ *   "part_ranks", "part_rank"  DIAGNOSTIC (world_size 1 only): build rank part_rank's share of a
+ *                  part_ranks-way partition (no collectives), to measure every rank's setup of
+ *                  a p-GPU run on one GPU.  Takes effect at hm_build_tree.
+ *   "aca_split"    DIAGNOSTIC: 1 = the ACA evaluation kernels store raw entries and a separate
+ *                  pass applies the residual corrections (same results; slower)
  *   "lr_f32"       1: hm_setup stores the ACA factors U, V in binary32 (each entry rounded once;
  *                  dense blocks, ACA itself and all matvec / Krylov arithmetic stay FP64: the
  *                  matvec widens the factors exactly before every FMA).  Halves the low-rank bytes
