@@ -32,15 +32,19 @@ __global__ void k_mdot(const double* __restrict__ Vb, int64_t ld, int nv, const 
     double acc[32];
 #pragma unroll
     for (int q = 0; q < 32; ++q) acc[q] = 0.0;
+    // the basis vectors of this pass; an extra vector (i = nv - 1, slot nb) is read from `extra`
+    const int nb = (extra && i0 + cnt == nv) ? cnt - 1 : cnt;
+    double accx = 0.0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
       const double wt = w[t];
 #pragma unroll
       for (int q = 0; q < 32; ++q)
-        if (q < cnt) acc[q] += (extra && i0 + q == nv - 1 ? extra[t] : Vb[(int64_t)(i0 + q) * ld + t]) * wt;
+        if (q < nb) acc[q] += Vb[(int64_t)(i0 + q) * ld + t] * wt;
+      if (nb < cnt) accx += extra[t] * wt;
     }
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
-      double a = acc[q];
+      double a = (q == nb) ? accx : acc[q];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
       if (lane == 0) sh[wib][q] = a;
