@@ -184,3 +184,28 @@ def test_lr_f32_c2_matvec_and_solution(O, torch_cuda):
     xo = R.gmres(f, tol=1e-10)[0]
     assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-5 * np.linalg.norm(xo)
     H.close(); G.close()
+
+
+def test_c5_matvec_sampled_exact_rows(O, torch_cuda):
+    """configs[4] (lobed surface on geodesic nu = 244, N = 1,190,720, the gearwheel stand-in):
+    ||(Hx)_R - (Ax)_R|| <= 10 eps_aca ||(Ax)_R|| on 128 seeded exact Galerkin rows for x = 1, the
+    paper's f and a seeded N(0,1) vector, and the tree (perm, both leaf lists) bit-exact."""
+    import torch
+    from inputs.meshes import lobed
+    V, T = lobed(244)
+    N = T.shape[0]
+    H = _gpu(V, T)
+    R = O.Problem(V, T)
+    assert np.array_equal(H.perm(), R.perm())
+    for kind in (0, 1):
+        assert np.array_equal(H.leaves(kind)[0], R.leaves(kind))
+    H.setup(EPS)
+    rows = np.random.default_rng(7).permutation(N)[:128]
+    Arows = R.dense_rows(rows)
+    fbar = H.assemble_rhs(1)
+    for x in (np.ones(N), fbar, seeded_vector(N, 0)):
+        yg = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        ye = Arows @ x
+        err = np.linalg.norm(yg[rows] - ye) / np.linalg.norm(ye)
+        assert err <= 10 * EPS, err
+    H.close()
