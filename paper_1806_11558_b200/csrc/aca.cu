@@ -126,6 +126,38 @@ struct AcaMap {
     r.idx = (int32_t)(e - pre[a]);
     return true;
   }
+  // Warp-collective locate with a per-warp cache of the last segment seen (shared memory):
+  // consecutive 32-entry groups of a warp mostly stay in one block, and then the entry ->
+  // block lookup (tab, pre, act and, for columns, the block state) is one shared-memory read
+  // instead of a chain of dependent global loads.  Misses take the plain path and the warp's
+  // last valid lane publishes its segment.
+  __device__ bool locate_warp(int64_t e, bool valid, EntryRef& r, SegCache& sc, int lane) const {
+    const int64_t lo = sc.lo, hi = sc.hi;
+    if (__all_sync(0xffffffffu, !valid || (e >= lo && e < hi))) {
+      if (!valid || !sc.ok) return false;
+      r.seg = sc.c;
+      r.idx = (int32_t)(e - lo);
+      return true;
+    }
+    int64_t plo = 0, phi = 0;
+    int32_t c = 0;
+    bool ok = false;
+    if (valid) {
+      int64_t a = tab[e >> 5];
+      while (pre[a + 1] <= e) ++a;
+      c = act[a];
+      plo = pre[a];
+      phi = pre[a + 1];
+      ok = ROW || !(S[c].skip || S[c].status != 0);
+      r.seg = c;
+      r.idx = (int32_t)(e - plo);
+    }
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    __syncwarp();
+    if (vm && lane == 31 - __clz(vm)) { sc.lo = plo; sc.hi = phi; sc.c = c; sc.ok = ok ? 1 : 0; }
+    __syncwarp();
+    return valid && ok;
+  }
   __device__ void pair(EntryRef r, int& s, int& t) const {
     const AcaBlk& b = B[r.seg];
     const AcaState& st = S[r.seg];
@@ -559,7 +591,8 @@ void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWor
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 3 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4);   // one wave, persistent
-  k_eval_class3<M><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
+  if (C.aca_segcache) k_eval_class3<M, true><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
+  else k_eval_class3<M, false><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
   const unsigned g4 = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 16);
   k_eval_list<4, M><<<g4, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
