@@ -40,7 +40,7 @@ __global__ void k_mdot(const double* __restrict__ Vb, int64_t ld, int nv, const 
 #pragma unroll
       for (int q = 0; q < 32; ++q)
         if (q < nb) acc[q] += Vb[(int64_t)(i0 + q) * ld + t] * wt;
-      if (nb < cnt) accx += extra[t] * wt;
+      if (nb < cnt) accx += (extra == w ? wt : extra[t]) * wt;
     }
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
