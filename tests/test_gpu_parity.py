@@ -381,3 +381,23 @@ def test_degenerate_sizes(O, torch_cuda, case):
     xo = R.gmres(f, tol=1e-10)[0]
     assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-10 * np.linalg.norm(xo)
     H.close()
+
+
+def test_potential_beyond_one_launch_of_point_tiles(O, torch_cuda):
+    """hm_potential with m = 600,000 points (more than the 65,535 x 8 point tiles one launch
+    covers: the point slices are launched one after another): every 1000th point equal to the
+    oracle's potential to 1e-12."""
+    V, T = icosphere(3)
+    H = _gpu(V, T)
+    R = O.Problem(V, T)
+    rng = np.random.default_rng(11)
+    M = 600_000
+    X = rng.standard_normal((M, 3)); X /= np.linalg.norm(X, axis=1)[:, None]
+    X *= rng.uniform(0.0, 0.7, size=(M, 1))
+    a = seeded_vector(T.shape[0], 8)
+    ug = H.potential(torch_cuda.from_numpy(a).cuda(), torch_cuda.from_numpy(X).cuda()).cpu().numpy()
+    sel = np.arange(0, M, 1000)
+    sel = np.concatenate([sel, [M - 1]])
+    uo = R.potential(a, X[sel])
+    assert np.abs(ug[sel] - uo).max() <= 1e-12 * np.abs(uo).max()
+    H.close()
