@@ -479,7 +479,8 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
 
 // G = 1: one warp per active block (small blocks; big ones are skipped), act[] = compact list;
 // the active count *dnact is read on the device (grid: a host-side upper bound, see k_aca_pivot)
-__global__ void __launch_bounds__(64, 16) k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
+template <int MINB>
+__global__ void __launch_bounds__(64, MINB) k_aca_update(const AcaBlk* __restrict__ B, AcaState* __restrict__ S,
                                                     const int32_t* __restrict__ act, const int64_t* __restrict__ dnact,
                                                     const double* __restrict__ Uw, const double* __restrict__ Vw,
                                                     const uint32_t* __restrict__ bmap, int32_t* __restrict__ piv,
@@ -759,7 +760,8 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
       }
     }
     ks.reset(new KScope(C, KF_ACA_OTHER));
-    k_aca_update<<<grid_for(nact_ub * 32, 64), 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Uw, Vw,
+    auto upd = C.aca_upd_occ == 2 ? k_aca_update<32> : C.aca_upd_occ == 1 ? k_aca_update<24> : k_aca_update<16>;
+    upd<<<grid_for(nact_ub * 32, 64), 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Uw, Vw,
                                                             W.bmap.get(), W.piv.get(), kws, C.eps_aca);
     HM_CHECK_LAUNCH();
     if (nbig) {

@@ -352,6 +352,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "lr_f32") { if (v != 0 && v != 1) bad(); C.lr_f32 = (int)v; }
     else if (k == "aca_split") { if (v != 0 && v != 1) bad(); C.aca_split = (int)v; }
     else if (k == "aca_segcache") { if (v != 0 && v != 1) bad(); C.aca_segcache = (int)v; }
+    else if (k == "aca_upd_occ") { if (v < 0 || v > 2) bad(); C.aca_upd_occ = (int)v; }
     else if (k == "cost_model") { if (v != 0 && v != 1 && v != 2) bad(); C.cost_model = (int)v; }
     else if (k == "part_ranks") { if (v < 1 || v > 4096) bad(); C.part_ranks = (int)v; }
     else if (k == "part_rank") { if (v < 0 || v > 4095) bad(); C.part_rank = (int)v; }
@@ -390,6 +391,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "lr_f32") *v = C.lr_f32;
     else if (k == "aca_split") *v = C.aca_split;
     else if (k == "aca_segcache") *v = C.aca_segcache;
+    else if (k == "aca_upd_occ") *v = C.aca_upd_occ;
     else if (k == "cost_model") *v = C.cost_model;
     else if (k == "part_ranks") *v = C.part_ranks;
     else if (k == "part_rank") *v = C.part_rank;
