@@ -123,6 +123,8 @@ const char* hm_last_error(hm_ctx ctx);
  *   "part_ranks", "part_rank"  DIAGNOSTIC (world_size 1 only): build rank part_rank's share of a
  *                  part_ranks-way partition (no collectives), to measure every rank's setup of
  *                  a p-GPU run on one GPU.  Takes effect at hm_build_tree.
+ *   "aca_upd_occ"  CTAs per SM of the warp-per-block Frobenius-update kernel: 0 = 16 (64 registers),
+ *                  1 = 24 (default, 40 registers), 2 = 32 (32 registers)
  *   "aca_segcache" DIAGNOSTIC: 1 = per-warp shared-memory cache of the last entry segment in the
  *                  ACA order-3 kernel (same results; slower)
  *   "aca_split"    DIAGNOSTIC: 1 = the ACA evaluation kernels store raw entries and a separate

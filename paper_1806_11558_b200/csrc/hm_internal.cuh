@@ -276,7 +276,7 @@ struct Context {
   int part_ranks = 1, part_rank = 0;   // diagnostic options: emulate rank part_rank of a part_ranks-way partition (world 1)
   int cost_model = 2;          // option "cost_model": leaf cost of the partition (A18): 0 round-1 proxy, 1 evaluation model, 2 (default) kind weights + per-block ACA cost
   int aca_split = 0;           // option "aca_split": ACA residual corrections in a separate streaming pass (A/B)
-  int aca_upd_occ = 0;         // diagnostic option "aca_upd_occ": CTAs per SM of k_aca_update (0: 16, 1: 24, 2: 32)
+  int aca_upd_occ = 1;         // option "aca_upd_occ": CTAs per SM of k_aca_update (0: 16, 1: 24 default, 2: 32)
   int aca_segcache = 0;        // diagnostic option "aca_segcache": per-warp segment cache in the ACA order-3 kernel (A/B: slower)
   int lr_f32 = 0;              // option "lr_f32": store the ACA factors U, V in binary32 (dense blocks stay FP64)
   int lr_esz = 8;              // bytes per stored factor entry of the current setup (8, or 4 with lr_f32)
