@@ -394,41 +394,28 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
   const double* V = Vw + b.voff;
   const double* u = U + (int64_t)st.k * b.m;
   const double* v = V + (int64_t)st.k * b.n;
-  const uint32_t* bm = bmap + b.boff;
   const int t0 = gw * 32 + lane, stride = G * 32;
-  const int mn = max(b.m, b.n);
   double uu = 0.0;   // ||u_k||^2, accumulated in the first pass over u (one pass also when k = 0)
   double cross = 0.0;
-  // the next-row argmax over unused rows (A12) rides along the first pass over u; it is used
-  // only if the stop test below does not fire
-  double best = -1.0;
-  int bt = INT_MAX;
   for (int l0 = 0; l0 < max(st.k, 1); l0 += 8) {
     const int kc = min(8, st.k - l0);
     double acc[16];
 #pragma unroll
     for (int l = 0; l < 16; ++l) acc[l] = 0.0;
-    // one loop over rows of U and V together: a pass's loads (u, 8 columns of U, v, 8 of V)
-    // are issued at once, one memory latency per pass instead of two
-    for (int t = t0; t < mn; t += stride) {
-      if (t < b.m) {
-        const double ut = u[t];
-        if (l0 == 0) {
-          uu = fma(ut, ut, uu);
-          if (!is_used(bm, t) && fabs(ut) > best) { best = fabs(ut); bt = t; }
-        }
+    for (int t = t0; t < b.m; t += stride) {
+      const double ut = u[t];
+      if (l0 == 0) uu = fma(ut, ut, uu);
 #pragma unroll
-        for (int l = 0; l < 8; ++l)
-          if (l < kc) acc[l] = fma(ut, U[t + (int64_t)(l0 + l) * b.m], acc[l]);
-      }
-      if (t < b.n && kc > 0) {
-        const double vj = v[t];
-#pragma unroll
-        for (int l = 0; l < 8; ++l)
-          if (l < kc) acc[8 + l] = fma(V[t + (int64_t)(l0 + l) * b.n], vj, acc[8 + l]);
-      }
+      for (int l = 0; l < 8; ++l)
+        if (l < kc) acc[l] = fma(ut, U[t + (int64_t)(l0 + l) * b.m], acc[l]);
     }
     if (kc <= 0) break;
+    for (int j = t0; j < b.n; j += stride) {
+      const double vj = v[j];
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < kc) acc[8 + l] = fma(V[j + (int64_t)(l0 + l) * b.n], vj, acc[8 + l]);
+    }
     warp_reduce16(acc, lane);   // lane L: total of index reduce16_index(L); du_l at bit4 = 0, dv_l at L ^ 16
     if (G > 1) {
       if ((lane & 1) == 0) red[gw * 17 + reduce16_index(lane)] = acc[0];
@@ -465,6 +452,14 @@ __device__ __forceinline__ void aca_update_block(const AcaBlk& b, AcaState& st, 
   else if (st.k >= b.kmax) st.status = 1;                              // rank budget
   else if (st.k >= kws) st.status = 2;                                 // workspace full: re-run
   if (st.status == 0) {                                                // next row pivot (A12)
+    const uint32_t* bm = bmap + b.boff;
+    double best = -1.0;
+    int bt = INT_MAX;
+    for (int t = t0; t < b.m; t += stride) {
+      if (is_used(bm, t)) continue;
+      const double a = fabs(u[t]);
+      if (a > best) { best = a; bt = t; }
+    }
     warp_argmax(best, bt);
     if (G > 1) {
       int* ri = reinterpret_cast<int*>(red + G * 17);
