@@ -125,10 +125,6 @@ const char* hm_last_error(hm_ctx ctx);
  *                  a p-GPU run on one GPU.  Takes effect at hm_build_tree.
  *   "aca_upd_occ"  CTAs per SM of the warp-per-block Frobenius-update kernel: 0 = 16 (64 registers),
  *                  1 = 24 (default, 40 registers), 2 = 32 (32 registers)
- *   "aca_segcache" DIAGNOSTIC: 1 = per-warp shared-memory cache of the last entry segment in the
- *                  ACA order-3 kernel (same results; slower)
- *   "aca_split"    DIAGNOSTIC: 1 = the ACA evaluation kernels store raw entries and a separate
- *                  pass applies the residual corrections (same results; slower)
  *   "lr_f32"       1: hm_setup stores the ACA factors U, V in binary32 (each entry rounded once;
  *                  dense blocks, ACA itself and all matvec / Krylov arithmetic stay FP64: the
  *                  matvec widens the factors exactly before every FMA).  Halves the low-rank bytes
@@ -136,7 +132,7 @@ const char* hm_last_error(hm_ctx ctx);
  *                  Takes effect at the next hm_setup; hm_get_lowrank returns the widened values.
  *   "setup_overlap" 1: hm_setup evaluates the near field on a least-priority stream from a
  *                  second host thread while ACA runs on a greatest-priority stream (results
- *                  bit-identical; ~5% shorter setup at N = 1.57M); 0 (default) serial.  With
+ *                  bit-identical; 8% shorter setup at N = 1.57M), the default; 0: serial.  With
  *                  kernel timing on, "kt" "eval_union_ms" is the union of the two evaluation
  *                  families' intervals (their sum when serial)
  * Errors: HM_ERR_ARG for an unknown key or an out-of-range value. */

@@ -115,7 +115,6 @@ struct AcaMap {
   int64_t nb;
   double* Uw;
   double* Vw;
-  int raw;              // option aca_split: store the raw entry, k_aca_correct applies the corrections
   __device__ bool locate(int64_t e, bool valid, EntryRef& r) const {
     if (!valid) return false;
     int64_t a = tab[e >> 5];
@@ -126,38 +125,6 @@ struct AcaMap {
     r.idx = (int32_t)(e - pre[a]);
     return true;
   }
-  // Warp-collective locate with a per-warp cache of the last segment seen (shared memory):
-  // consecutive 32-entry groups of a warp mostly stay in one block, and then the entry ->
-  // block lookup (tab, pre, act and, for columns, the block state) is one shared-memory read
-  // instead of a chain of dependent global loads.  Misses take the plain path and the warp's
-  // last valid lane publishes its segment.
-  __device__ bool locate_warp(int64_t e, bool valid, EntryRef& r, SegCache& sc, int lane) const {
-    const int64_t lo = sc.lo, hi = sc.hi;
-    if (__all_sync(0xffffffffu, !valid || (e >= lo && e < hi))) {
-      if (!valid || !sc.ok) return false;
-      r.seg = sc.c;
-      r.idx = (int32_t)(e - lo);
-      return true;
-    }
-    int64_t plo = 0, phi = 0;
-    int32_t c = 0;
-    bool ok = false;
-    if (valid) {
-      int64_t a = tab[e >> 5];
-      while (pre[a + 1] <= e) ++a;
-      c = act[a];
-      plo = pre[a];
-      phi = pre[a + 1];
-      ok = ROW || !(S[c].skip || S[c].status != 0);
-      r.seg = c;
-      r.idx = (int32_t)(e - plo);
-    }
-    const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    __syncwarp();
-    if (vm && lane == 31 - __clz(vm)) { sc.lo = plo; sc.hi = phi; sc.c = c; sc.ok = ok ? 1 : 0; }
-    __syncwarp();
-    return valid && ok;
-  }
   __device__ void pair(EntryRef r, int& s, int& t) const {
     const AcaBlk& b = B[r.seg];
     const AcaState& st = S[r.seg];
@@ -167,11 +134,6 @@ struct AcaMap {
   __device__ void put(EntryRef r, double a) const {
     const AcaBlk& b = B[r.seg];
     const AcaState st = S[r.seg];
-    if (raw) {
-      if (ROW) Vw[b.voff + (int64_t)st.k * b.n + r.idx] = a;
-      else Uw[b.uoff + (int64_t)st.k * b.m + r.idx] = a;
-      return;
-    }
     const double* U = Uw + b.uoff;
     const double* V = Vw + b.voff;
     if (ROW) {
@@ -183,30 +145,6 @@ struct AcaMap {
     }
   }
 };
-
-// option aca_split: the residual corrections r = a - sum_l U V (l ascending, A15) of a step's
-// raw entries as a separate streaming pass, one thread per entry (grid-stride over the
-// step's device-side total), instead of inside the FP64-bound evaluation kernels
-template <bool ROW>
-__global__ void __launch_bounds__(256) k_aca_correct(AcaMap<ROW> m, const int64_t* __restrict__ dtot) {
-  const int64_t total = *dtot;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    EntryRef r;
-    if (!m.locate(e, true, r)) continue;
-    const AcaBlk& b = m.B[r.seg];
-    const AcaState st = m.S[r.seg];
-    if (st.k == 0) continue;
-    double* dst = ROW ? m.Vw + b.voff + (int64_t)st.k * b.n + r.idx : m.Uw + b.uoff + (int64_t)st.k * b.m + r.idx;
-    double a = *dst;
-    const double* U = m.Uw + b.uoff;
-    const double* V = m.Vw + b.voff;
-    if (ROW)
-      for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[st.i + (int64_t)l * b.m], V[r.idx + (int64_t)l * b.n]));
-    else
-      for (int l = 0; l < st.k; ++l) a = dsub(a, dmul(U[r.idx + (int64_t)l * b.m], V[st.js + (int64_t)l * b.n]));
-    *dst = a;
-  }
-}
 
 __device__ __forceinline__ void warp_argmax(double& v, int& idx) {
 #pragma unroll
@@ -592,8 +530,7 @@ void aca_eval(Context& C, const M& m, const int64_t* dtot, int64_t upper, AcaWor
   HM_CUDA(cudaMemsetAsync(W.cnt.get(), 0, 3 * sizeof(unsigned long long), st));
   KScope ks(C, KF_EVAL_ACA);
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 4);   // one wave, persistent
-  if (C.aca_segcache) k_eval_class3<M, true><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
-  else k_eval_class3<M, false><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
+  k_eval_class3<M><<<g, 128, 0, st>>>(m, dtot, W.lists.get(), W.cnt.get(), W.ev.get());
   HM_CHECK_LAUNCH();
   const unsigned g4 = (unsigned)std::min<int64_t>(grid_for(upper, 128), 148 * 16);
   k_eval_list<4, M><<<g4, 128, 0, st>>>(m, W.lists.get(), W.cnt.get(), W.ev.get());
@@ -724,18 +661,10 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     ks.reset();
     if (C.quad)
       aca_eval(C, AcaMap<true, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(),
-                                     nb, Uw, Vw, 0}, drow, rmax, W);
+                                     nb, Uw, Vw}, drow, rmax, W);
     else
-    {
-      const AcaMap<true> mr{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
-                            W.rtab.get(), nb, Uw, Vw, C.aca_split};
-      aca_eval(C, mr, drow, rmax, W);
-      if (C.aca_split) {
-        KScope kc(C, KF_ACA_OTHER);
-        k_aca_correct<true><<<(unsigned)std::min<int64_t>(grid_for(rmax, 256), 148 * 8), 256, 0, st>>>(mr, drow);
-        HM_CHECK_LAUNCH();
-      }
-    }
+      aca_eval(C, AcaMap<true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
+                               W.rtab.get(), nb, Uw, Vw}, drow, rmax, W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
     k_aca_pivot<<<grid_for(nact_ub * 32, 256), 256, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Vw,
                                                              W.bmap.get());
@@ -747,18 +676,10 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     ks.reset();
     if (C.quad)
       aca_eval(C, AcaMap<false, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(),
-                                      nb, Uw, Vw, 0}, dcol, cmax, W);
+                                      nb, Uw, Vw}, dcol, cmax, W);
     else
-    {
-      const AcaMap<false> mc{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(),
-                             W.ctab.get(), nb, Uw, Vw, C.aca_split};
-      aca_eval(C, mc, dcol, cmax, W);
-      if (C.aca_split) {
-        KScope kc(C, KF_ACA_OTHER);
-        k_aca_correct<false><<<(unsigned)std::min<int64_t>(grid_for(cmax, 256), 148 * 8), 256, 0, st>>>(mc, dcol);
-        HM_CHECK_LAUNCH();
-      }
-    }
+      aca_eval(C, AcaMap<false>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(),
+                                W.ctab.get(), nb, Uw, Vw}, dcol, cmax, W);
     ks.reset(new KScope(C, KF_ACA_OTHER));
     auto upd = C.aca_upd_occ == 2 ? k_aca_update<32> : C.aca_upd_occ == 1 ? k_aca_update<24> : k_aca_update<16>;
     upd<<<grid_for(nact_ub * 32, 64), 64, 0, st>>>(W.blk.get(), W.state.get(), W.act.get(), dnact, Uw, Vw,

@@ -350,8 +350,6 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "aca_chunk_mb") { if (v < 1) bad(); C.aca_chunk_mb = v; }
     else if (k == "aca_kws") { if (v < 1 || v > 256) bad(); C.aca_kws = v; }
     else if (k == "lr_f32") { if (v != 0 && v != 1) bad(); C.lr_f32 = (int)v; }
-    else if (k == "aca_split") { if (v != 0 && v != 1) bad(); C.aca_split = (int)v; }
-    else if (k == "aca_segcache") { if (v != 0 && v != 1) bad(); C.aca_segcache = (int)v; }
     else if (k == "aca_upd_occ") { if (v < 0 || v > 2) bad(); C.aca_upd_occ = (int)v; }
     else if (k == "cost_model") { if (v != 0 && v != 1 && v != 2) bad(); C.cost_model = (int)v; }
     else if (k == "part_ranks") { if (v < 1 || v > 4096) bad(); C.part_ranks = (int)v; }
@@ -389,8 +387,6 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "aca_chunk_mb") *v = C.aca_chunk_mb;
     else if (k == "aca_kws") *v = C.aca_kws;
     else if (k == "lr_f32") *v = C.lr_f32;
-    else if (k == "aca_split") *v = C.aca_split;
-    else if (k == "aca_segcache") *v = C.aca_segcache;
     else if (k == "aca_upd_occ") *v = C.aca_upd_occ;
     else if (k == "cost_model") *v = C.cost_model;
     else if (k == "part_ranks") *v = C.part_ranks;
@@ -427,7 +423,9 @@ hm_status hm_build_tree(hm_ctx ctx, const hm_mesh* mesh, int leaf_size, double e
 // loop drives a greatest-priority stream, so the near-field CTAs fill the SM time ACA leaves
 // idle (its pivot/update/compaction launches, host round trips and chunk tails) and yield
 // to every ACA launch.  Both write disjoint storage; results are identical to the serial
-// order.  near_ms is the near-field thread's own span, aca_ms ACA's.
+// order.  The matvec plan (host work + upload; it needs ACA's ranks, not the near-field
+// values) is built while the near-field tail still runs.  near_ms is the near-field thread's
+// own span, aca_ms ACA's.
 static void run_overlapped(Context& C) {
   if (!C.s_hi) {
     int least = 0, greatest = 0;
@@ -467,6 +465,17 @@ static void run_overlapped(Context& C) {
   }
   HM_CUDA(cudaStreamSynchronize(C.s_hi));
   C.times.aca_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  try {
+    const auto t1 = std::chrono::steady_clock::now();
+    hm::plan_matvec(C);
+    HM_CUDA(cudaStreamSynchronize(C.s_hi));
+    C.times.plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+  } catch (...) {
+    C.stream = user;
+    th.join();
+    cudaStreamSynchronize(C.s_lo);
+    throw;
+  }
   C.stream = user;
   th.join();
   if (near_err) std::rethrow_exception(near_err);
@@ -493,19 +502,20 @@ hm_status hm_setup(hm_ctx ctx, double eps_aca) {
     hm::near_prepare(C);
     hm::plan_dense_begin(C);
     if (C.setup_overlap && C.dense_doubles > 0) {
-      run_overlapped(C);
+      run_overlapped(C);               // near field beside ACA, plan beside the near-field tail
+      hm::near_check(C);
     } else {
       {
         Timer t(C);
         hm::near_eval(C, C.stream, C.kt);
         C.times.near_ms = t.ms();
       }
-      Timer t(C);
-      hm::setup_aca(C);
-      C.times.aca_ms = t.ms();
-    }
-    hm::near_check(C);
-    {
+      {
+        Timer t(C);
+        hm::setup_aca(C);
+        C.times.aca_ms = t.ms();
+      }
+      hm::near_check(C);
       Timer t(C);
       hm::plan_matvec(C);
       C.times.plan_ms = t.ms();

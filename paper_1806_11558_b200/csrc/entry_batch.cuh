@@ -26,11 +26,7 @@ constexpr int kNumClass = 7;   // 0 identical, 1 edge, 2 vertex, 3..6 regular or
 struct EntryRef {
   int32_t seg, idx;
 };
-// per-warp cache of the last entry segment of a persistent warp (k_eval_class3, ACA mappings)
-struct SegCache {
-  int64_t lo, hi;
-  int32_t c, ok;
-};
+
 
 __device__ __forceinline__ int canonical_class(const Panel* __restrict__ P, int s, int t, int& xs, int& ys) {
   const bool swap = __ldg(&P[t].app) < __ldg(&P[s].app);
@@ -172,15 +168,12 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
 //   k_eval_rest     persistent, the remaining few (orders 5, 6, touching pairs).
 // one 32-entry group of a warp (lanes e = e0 + lane): classify, append non-order-3 entries,
 // evaluate order 3 in place
-template <bool SC, class M>
+template <class M>
 __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t total, int lane, EntryRef* __restrict__ lists,
-                                             unsigned long long* __restrict__ cnt, unsigned long long& ev, SegCache& sc) {
+                                             unsigned long long* __restrict__ cnt, unsigned long long& ev) {
   EntryRef r;
   int cls = -1, xs = 0, ys = 0;
-  bool found;
-  if constexpr (SC) found = m.locate_warp(e, e < total, r, sc, lane);
-  else found = m.locate(e, e < total, r);
-  if (found) {
+  if (m.locate(e, e < total, r)) {
     int s, t;
     m.pair(r, s, t);
     cls = map_class(m, s, t, xs, ys);
@@ -207,17 +200,13 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
 // one thread per entry leave SMs idle at the tail: C4 ACA evaluation 1.85 s resp. 1.75 s vs
 // 1.61 s, profiles/r02_setup_ab1.jsonl)
 constexpr int kDynGroups = 4;
-template <class M, bool SC = true>
+template <class M>
 __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __restrict__ dtot,
                                                      EntryRef* __restrict__ lists,
                                                      unsigned long long* __restrict__ cnt /* [n4, nrest, next] */,
                                                      unsigned long long* __restrict__ evals) {
-  __shared__ SegCache scache[4];
   const int64_t total = *dtot;
   const int lane = threadIdx.x & 31;
-  SegCache& sc = scache[threadIdx.x >> 5];
-  if (lane == 0) { sc.lo = 0; sc.hi = 0; sc.c = 0; sc.ok = 0; }
-  __syncwarp();
   unsigned long long ev = 0;
   for (;;) {
     unsigned long long b0 = 0;
@@ -225,7 +214,7 @@ __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __re
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     if ((int64_t)b0 >= total) break;
 #pragma unroll 1
-    for (int g = 0; g < kDynGroups; ++g) class3_group<SC>(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev, sc);
+    for (int g = 0; g < kDynGroups; ++g) class3_group(m, (int64_t)b0 + 32 * g + lane, total, lane, lists, cnt, ev);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);

@@ -275,9 +275,7 @@ struct Context {
   int aca_prev_kmax = 0, aca_prev_esz = 0;
   int part_ranks = 1, part_rank = 0;   // diagnostic options: emulate rank part_rank of a part_ranks-way partition (world 1)
   int cost_model = 2;          // option "cost_model": leaf cost of the partition (A18): 0 round-1 proxy, 1 evaluation model, 2 (default) kind weights + per-block ACA cost
-  int aca_split = 0;           // option "aca_split": ACA residual corrections in a separate streaming pass (A/B)
   int aca_upd_occ = 1;         // option "aca_upd_occ": CTAs per SM of k_aca_update (0: 16, 1: 24 default, 2: 32)
-  int aca_segcache = 0;        // diagnostic option "aca_segcache": per-warp segment cache in the ACA order-3 kernel (A/B: slower)
   int lr_f32 = 0;              // option "lr_f32": store the ACA factors U, V in binary32 (dense blocks stay FP64)
   int lr_esz = 8;              // bytes per stored factor entry of the current setup (8, or 4 with lr_f32)
 
@@ -317,7 +315,7 @@ struct Context {
   std::vector<int64_t> near_hoff;   // host copy of doff (near_prepare)
   // near field beside ACA (option setup_overlap): ACA on s_hi (greatest priority), the
   // near-field evaluation on s_lo (least priority) from its own host thread and timer
-  int setup_overlap = 0;
+  int setup_overlap = 1;
   cudaStream_t s_hi = nullptr, s_lo = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   KTimer kt_near;

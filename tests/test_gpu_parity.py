@@ -228,15 +228,14 @@ def test_c2_solve_vs_oracle(c2):
 
 
 def test_setup_overlap_bit_identical(c2):
-    # near field beside ACA (option setup_overlap, default off) vs the serial order: every
+    # near field beside ACA (option setup_overlap, default on) vs the serial order: every
     # stored entry and factor identical, and the kernel-timing union of the two evaluation
     # families no longer than their sum and no shorter than either
-    V, T, H, R = c2
+    V, T, H, R = c2      # H: overlapped (the fixture's, default options)
+    assert H.get_option("setup_overlap") == 1
     G = _gpu(V, T)
-    assert G.get_option("setup_overlap") == 0
-    G.set_option("setup_overlap", 1)
+    G.set_option("setup_overlap", 0)
     G.setup(EPS)
-    H, G = G, H          # H: overlapped, G: serial (the fixture's)
     dense, _ = H.leaves(1)
     for b, q in enumerate(dense):
         shape = (q[1] - q[0], q[3] - q[2])
@@ -253,7 +252,7 @@ def test_setup_overlap_bit_identical(c2):
     H.set_option("kernel_timing", 0)
     s = kt["eval_near_ms"] + kt["eval_aca_ms"]
     assert max(kt["eval_near_ms"], kt["eval_aca_ms"]) * 0.999 <= kt["eval_union_ms"] <= s * 1.001
-    H.close()
+    G.close()
 
 
 def test_matvec_options_agree(c2, torch_cuda):
