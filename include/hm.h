@@ -56,6 +56,7 @@ typedef enum {
 } hm_status;
 
 #define HM_NCCL_UNIQUE_ID_BYTES 128
+#define HM_P2P_HANDLE_BYTES 64   /* a CUDA IPC memory handle */
 
 /* Surface mesh of flat panels (nodes = element centres).
  * vertices: n_vertices*3 doubles, xyz row-major.  triangles: n_triangles*panel_vertices
@@ -130,6 +131,8 @@ const char* hm_last_error(hm_ctx ctx);
  *                  matvec widens the factors exactly before every FMA).  Halves the low-rank bytes
  *                  the matvec streams.  0 (default): FP64 factors.
  *                  Takes effect at the next hm_setup; hm_get_lowrank returns the widened values.
+ *   "solve_comm"   sharded solve collectives: 0 NCCL (default), 1 libhm P2P kernels (requires
+ *                  hm_p2p_import, which selects it).
  *   "setup_overlap" 1: hm_setup evaluates the near field on a least-priority stream from a
  *                  second host thread while ACA runs on a greatest-priority stream (results
  *                  bit-identical; 8% shorter setup at N = 1.57M), the default; 0: serial.  With
@@ -176,8 +179,10 @@ hm_status hm_matvec(hm_ctx ctx, const double* x, double* y);
  * each matvec all-gathers x (ncclAllGather) and reduce-scatters the partial products
  * (ncclReduceScatter) — the volume of the paper's replicated vector + global sum, P:578-587 —
  * and dot products are all-reduced (ncclAllReduce), so all ranks take identical decisions;
- * rhs and sol are full-length on every rank (sol is all-gathered at the end).  COLLECTIVE.
- * Synchronous.
+ * rhs and sol are full-length on every rank (sol is all-gathered at the end).  After
+ * hm_p2p_import (option "solve_comm" 1) the three collectives run as libhm kernels over NVLink
+ * peer memory instead of NCCL (sums in rank order: identical scalars on all ranks).
+ * COLLECTIVE.  Synchronous.
  * iters_out: matvecs performed (may be NULL); rel_residual_out: true relative residual
  * ||rhs - H sol|| / ||rhs|| after the last iteration (may be NULL).
  * Non-convergence within max_iter is NOT an error: HM_OK with *rel_residual_out > tol.
@@ -185,6 +190,25 @@ hm_status hm_matvec(hm_ctx ctx, const double* x, double* y);
  * HM_ERR_NCCL. */
 hm_status hm_solve(hm_ctx ctx, const double* rhs, double* sol, double tol,
                    int* iters_out, double* rel_residual_out);
+
+/* Peer-memory collectives for the sharded solve (the paper's per-product
+ * global sum, and the solver's dot-product reductions).
+ * hm_p2p_export: allocates this rank's exchange buffer (gathered x, partial y, dot-product
+ * slots and flags; ~16 n_max bytes) for solves of up to n_max unknowns and writes its CUDA
+ * IPC handle (HM_P2P_HANDLE_BYTES) to handle_out (host memory, caller-owned).  Once per
+ * context.  Errors: HM_ERR_STATE (world_size < 2 or > 8, or already exported), HM_ERR_ARG
+ * (n_max < 1 or NULL handle_out), HM_ERR_OOM, HM_ERR_CUDA.
+ * hm_p2p_import: handles = world_size consecutive handles in rank order (host memory, as
+ * exported by every rank and gathered by the caller, e.g. over the torch process group);
+ * maps every peer's buffer (cudaIpcOpenMemHandle) and sets option "solve_comm" to 1: from now
+ * on hm_solve's x all-gather, y reduce-scatter and dot-product all-reduce are libhm kernels
+ * (P2P stores / loads over NVLink, flags with system-scope release / acquire) instead of
+ * NCCL calls.  COLLECTIVE in the sense that every rank must import before any rank solves.
+ * A solve with N > n_max fails with HM_ERR_STATE.  The buffers are unmapped / freed by
+ * hm_destroy.  Errors: HM_ERR_STATE (not exported, or already imported), HM_ERR_ARG (NULL),
+ * HM_ERR_CUDA (a peer buffer could not be mapped). */
+hm_status hm_p2p_export(hm_ctx ctx, int64_t n_max, void* handle_out);
+hm_status hm_p2p_import(hm_ctx ctx, const void* handles);
 
 /* Right-hand side f_i = int_{T_i} f: kind 0 -> f = 1 (f_i = |T_i|);
  * kind 1 -> the paper's f(x) = 4x1^2 - 3x2^2 - x3^2, edge-midpoint rule (exact for

@@ -317,10 +317,25 @@ hm_status hm_create(hm_ctx* out, int device, int rank, int world_size, const voi
   return HM_OK;
 }
 
+hm_status hm_p2p_export(hm_ctx ctx, int64_t n_max, void* handle_out) {
+  return guarded(ctx, [&](Context& C) {
+    if (!handle_out) hm::fail(HM_ERR_ARG, "hm_p2p_export: NULL handle_out");
+    hm::p2p_export(C, n_max, handle_out);
+  });
+}
+
+hm_status hm_p2p_import(hm_ctx ctx, const void* handles) {
+  return guarded(ctx, [&](Context& C) {
+    if (!handles) hm::fail(HM_ERR_ARG, "hm_p2p_import: NULL handles");
+    hm::p2p_import(C, handles);
+  });
+}
+
 hm_status hm_destroy(hm_ctx ctx) {
   if (!ctx) return HM_OK;
   cudaSetDevice(ctx->C.device);
   if (ctx->C.stream) cudaStreamSynchronize(ctx->C.stream);
+  hm::p2p_release(ctx->C);
   if (ctx->C.comm) ncclCommDestroy(ctx->C.comm);
   bool own = ctx->C.own_stream;
   cudaStream_t st = ctx->C.stream;
@@ -364,6 +379,11 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "mv_small_max") { if (v < 0 || v > 49152) bad(); C.mv_small_max = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_scramble") { if (v != 0 && v != 1) bad(); C.mv_scramble = (int)v; }
     else if (k == "setup_overlap") { if (v != 0 && v != 1) bad(); C.setup_overlap = (int)v; }
+    else if (k == "solve_comm") {
+      if (v != 0 && v != 1) bad();
+      if (v == 1 && !C.p2p.ready) hm::fail(HM_ERR_STATE, "option solve_comm = 1 needs hm_p2p_import");
+      C.solve_comm = (int)v;
+    }
     else if (k == "mv_concurrent") { if (v != 0 && v != 1) bad(); C.mv_concurrent = (int)v; }
     else if (k == "kernel_timing") {
       if (v != 0 && v != 1) bad();
@@ -395,6 +415,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "kernel_timing") *v = C.kt.on ? 1 : 0;
     else if (k == "mv_kernel") *v = C.mv_kind;
     else if (k == "setup_overlap") *v = C.setup_overlap;
+    else if (k == "solve_comm") *v = C.solve_comm;
     else if (k == "mv_concurrent") *v = C.mv_concurrent;
     else hm::fail(HM_ERR_ARG, "hm_get_option: unknown key '" + k + "'");
   });

@@ -218,6 +218,17 @@ struct KTimer {
   ~KTimer();
 };
 
+// P2P exchange buffers of the sharded solve (p2p.cu; hm_p2p_export / hm_p2p_import)
+constexpr int kMaxPeers = 8;
+struct P2PState {
+  char* own = nullptr;               // this rank's exchange buffer (cudaMalloc, IPC-exported)
+  char* peer[kMaxPeers] = {};        // every rank's buffer mapped into this process (own at rank)
+  bool opened[kMaxPeers] = {};
+  int64_t F = 0, n_max = 0;          // doubles per vector region; largest N it serves
+  unsigned long long ep_ag = 0, ep_rs = 0, ep_ar = 0;   // epochs per collective kind
+  bool ready = false;
+};
+
 // Context ---------------------------------------------------------------------------------
 struct Context {
   int device = 0, rank = 0, world = 1;
@@ -302,6 +313,8 @@ struct Context {
   // work vectors (internal order)
   DBuf<double> xin, yin, xapp, yapp, work, pot_x, pot_out;
   DBuf<double> sh_x, sh_y, sh_sol;   // sharded Krylov (p > 1): gathered x, partial y, local solution
+  P2PState p2p;
+  int solve_comm = 0;          // option "solve_comm": 0 NCCL, 1 libhm P2P kernels (after hm_p2p_import)
   DBuf<double> krylov;         // GMRES basis / CG vectors
   DBuf<double> red;            // reduction scratch
   double* h_red = nullptr;     // pinned host scratch for scalar read-back
@@ -368,6 +381,17 @@ void solve(Context& C, const double* rhs_int, double* sol_int, double tol, int* 
            double* relres);
 // comm
 void allreduce_sum(Context& C, double* buf, int64_t n);
+// p2p.cu
+bool p2p_on(const Context& C);
+double* p2p_xfull(Context& C);
+double* p2p_ypart(Context& C);
+void p2p_export(Context& C, int64_t n_max, void* handle_out);
+void p2p_import(Context& C, const void* handles);
+void p2p_release(Context& C);
+void p2p_check_capacity(Context& C, int64_t S);
+void p2p_allgather(Context& C, const double* x, int64_t n, int64_t S, bool into_ypart = false);
+void p2p_reduce_scatter(Context& C, double* y, int64_t n, int64_t S);
+void p2p_allreduce(Context& C, double* buf, int64_t n);
 // entries (entry.cu)
 void eval_entries(Context& C, int64_t n, const int64_t* d_pairs, double* d_out);
 void assemble_rhs(Context& C, int kind, double* f_app);

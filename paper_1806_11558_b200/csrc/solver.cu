@@ -140,7 +140,10 @@ struct Red {
     k_mdot_final<<<(nv + 127) / 128, 128, 0, C.stream>>>(part.get(), kRedBlocks, nv, out.get());
     }
     HM_CHECK_LAUNCH();
-    if (L.sharded) allreduce_sum(C, out.get(), nv);
+    if (L.sharded) {
+      if (p2p_on(C)) p2p_allreduce(C, out.get(), nv);
+      else allreduce_sum(C, out.get(), nv);
+    }
     return out.get();
   }
   double dot(const double* a, const double* b) {
@@ -156,6 +159,12 @@ unsigned vgrid(int64_t n) { return std::min<unsigned>(grid_for(n, 256), 148 * 16
 
 void apply(Context& C, const Layout& L, const double* x, double* y) {
   if (!L.sharded) { matvec_internal(C, x, y); return; }
+  if (p2p_on(C)) {             // libhm's own collectives over NVLink peer memory (p2p.cu)
+    p2p_allgather(C, x, L.n, L.S);
+    matvec_internal(C, p2p_xfull(C), p2p_ypart(C), /*reduce=*/false);
+    p2p_reduce_scatter(C, y, L.n, L.S);
+    return;
+  }
   { KScope ks_(C, KF_COMM);
   HM_NCCL(ncclAllGather(x, C.sh_x.get(), (size_t)L.S, ncclDouble, C.comm, C.stream));
   }
@@ -329,13 +338,25 @@ void solve(Context& C, const double* rhs_int, double* sol_int, double tol, int* 
   }
   C.sh_sol.alloc(L.S + 32);
   HM_CUDA(cudaMemsetAsync(C.sh_sol.get(), 0, (L.S + 32) * sizeof(double), C.stream));
+  const bool p2p = p2p_on(C);
+  if (p2p) {
+    // entries past N of the gathered x stay 0 (the staged x ranges may read one past N);
+    // no peer writes there
+    p2p_check_capacity(C, L.S);
+    HM_CUDA(cudaMemsetAsync(p2p_xfull(C) + C.N, 0, (C.p2p.F - C.N) * sizeof(double), C.stream));
+  }
   if (C.solver == 1) cg(C, L, rhs_int + L.off, C.sh_sol.get(), tol, iters, relres);
   else gmres(C, L, rhs_int + L.off, C.sh_sol.get(), tol, iters, relres);
   // the full solution on every rank
-  { KScope ks_(C, KF_COMM);
-  HM_NCCL(ncclAllGather(C.sh_sol.get(), C.sh_x.get(), (size_t)L.S, ncclDouble, C.comm, C.stream));
+  if (p2p) {
+    p2p_allgather(C, C.sh_sol.get(), L.n, L.S, /*into_ypart=*/true);
+    HM_CUDA(cudaMemcpyAsync(sol_int, p2p_ypart(C), C.N * sizeof(double), cudaMemcpyDeviceToDevice, C.stream));
+  } else {
+    { KScope ks_(C, KF_COMM);
+    HM_NCCL(ncclAllGather(C.sh_sol.get(), C.sh_x.get(), (size_t)L.S, ncclDouble, C.comm, C.stream));
+    }
+    HM_CUDA(cudaMemcpyAsync(sol_int, C.sh_x.get(), C.N * sizeof(double), cudaMemcpyDeviceToDevice, C.stream));
   }
-  HM_CUDA(cudaMemcpyAsync(sol_int, C.sh_x.get(), C.N * sizeof(double), cudaMemcpyDeviceToDevice, C.stream));
   HM_CUDA(cudaStreamSynchronize(C.stream));
 }
 

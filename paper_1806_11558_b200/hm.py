@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libhm.so")
 STATUS = {0: "HM_OK", 1: "HM_ERR_ARG", 2: "HM_ERR_STATE", 3: "HM_ERR_OOM", 4: "HM_ERR_CUDA",
           5: "HM_ERR_NCCL", 6: "HM_ERR_NUMERIC", 7: "HM_ERR_BREAKDOWN"}
 NCCL_ID_BYTES = 128
+P2P_HANDLE_BYTES = 64
 
 
 class HMError(RuntimeError):
@@ -67,6 +68,8 @@ def lib():
             "hm_get_lowrank": [vp, i64, C.POINTER(i32), vp, vp, vp],
             "hm_quadrature_table": [i32, vp, vp],
             "hm_get_stats": [vp, C.c_char_p, i64],
+            "hm_p2p_export": [vp, i64, vp],
+            "hm_p2p_import": [vp, vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -156,6 +159,17 @@ def hm_solve(ctx, rhs, sol, tol=1e-8):
     return it.value, rr.value
 
 
+def hm_p2p_export(ctx, n_max: int) -> bytes:
+    buf = (C.c_char * P2P_HANDLE_BYTES)()
+    _check(ctx, lib().hm_p2p_export(ctx, int(n_max), buf))
+    return bytes(buf)
+
+
+def hm_p2p_import(ctx, handles: bytes):
+    buf = (C.c_char * len(handles)).from_buffer_copy(handles)
+    _check(ctx, lib().hm_p2p_import(ctx, buf))
+
+
 def hm_assemble_rhs(ctx, kind, f):
     _check(ctx, lib().hm_assemble_rhs(ctx, int(kind), _ptr(f)))
 
@@ -196,6 +210,16 @@ class HMatrix:
 
     def set_option(self, key, value):
         hm_set_option(self.ctx, key, value)
+
+    def enable_p2p(self, n_max, group=None):
+        """Sharded-solve collectives over NVLink peer memory (hm_p2p_export / hm_p2p_import):
+        every rank exports its exchange buffer, the IPC handles are all-gathered over the torch
+        process group (plumbing only), and every rank maps its peers'."""
+        import torch.distributed as dist
+        h = hm_p2p_export(self.ctx, n_max)
+        allh = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allh, h, group=group)
+        hm_p2p_import(self.ctx, b"".join(allh))
 
     def get_option(self, key):
         return hm_get_option(self.ctx, key)

@@ -5,6 +5,9 @@ lists; the matvec's partial products are all-reduced.  C
   * owned ranges of all ranks are disjoint and cover both lists (gathered to rank 0);
   * the p-rank H-matvec equals a 1-rank H-matvec built on rank 0's GPU to 1e-13 relative
     (same leaves, same factors; only the summation order of the global sum differs, A19);
+  * with libhm's peer-memory collectives (hm_p2p_import) the sharded GMRES and CG solutions
+    equal the NCCL ones to 1e-12 with the same iteration counts (not bitwise: the matvec's
+    FP64 atomics make every product's last bits run-dependent; observed 2.7e-14 at C2);
   * the p-rank GMRES and CG solutions (sharded Krylov vectors) equal the 1-rank ones to 1e-8: both solves stop at
     relres <= 1e-10 with y differing by ~1e-15 per product (A19), so they can differ by up to
     cond(H) * 2e-10 (cond ~ 1e3 at C2, growing like 1/h); observed 4e-14 (C2), 1.3e-10 (C3).
@@ -51,7 +54,16 @@ def main():
     H.set_option("solver", 1)                     # CG on the sharded Krylov vectors too
     sol_cg, it_cg, rr_cg = H.solve(f, 1e-10)
     H.set_option("solver", 0)
+    # the same solves with libhm's peer-memory collectives instead of NCCL (hm_p2p_import)
+    H.enable_p2p(N)
+    assert H.get_option("solve_comm") == 1
+    sol_p, it_p, rr_p = H.solve(f, 1e-10)
+    H.set_option("solver", 1)
+    sol_pcg, it_pcg, _ = H.solve(f, 1e-10)
+    H.set_option("solver", 0)
     torch.cuda.synchronize()
+    dp = (torch.linalg.norm(sol_p - sol) / torch.linalg.norm(sol)).item()
+    dpcg = (torch.linalg.norm(sol_pcg - sol_cg) / torch.linalg.norm(sol_cg)).item()
     own = torch.tensor(st["adm_owned"] + st["dense_owned"], dtype=torch.int64, device="cuda")
     allown = [torch.zeros_like(own) for _ in range(world)]
     dist.all_gather(allown, own)
@@ -80,7 +92,10 @@ def main():
         res.update({"matvec_rel_diff": dy, "solve_rel_diff": ds, "cg_rel_diff": dcg, "cg_iters": it_cg,
                     "cg_iters_1rank": it1cg, "iters": it, "iters_1rank": it1,
                     "setup_ms_max": setup_ms.item(), "setup_ms_1rank": R.stats()["setup_ms"]})
+        res.update({"p2p_vs_nccl_gmres": dp, "p2p_vs_nccl_cg": dpcg, "p2p_iters": [it_p, it_pcg],
+                    "p2p_bit_identical": bool(torch.equal(sol_p, sol) and torch.equal(sol_pcg, sol_cg))})
         ok &= dy <= 1e-13 and ds <= 1e-8 and dcg <= 1e-8
+        ok &= dp <= 1e-12 and dpcg <= 1e-12 and it_p == it and it_pcg == it_cg
         res["ok"] = bool(ok)
         print(json.dumps(res), flush=True)
         R.close()
