@@ -107,7 +107,8 @@ const char* hm_last_error(hm_ctx ctx);
  *                  matvec, Krylov BLAS-1); totals in hm_get_stats "kt"; setting it resets them
  *   "mv_kernel"    small-leaf matvec pipeline: 0 (default) two CTA rings per SM, 2 x 48 KiB
  *                  stages each; 1 one ring of 4 x 48 KiB stages; 2 two rings of 3 x 36 KiB;
- *                  3 two rings of 2 x 56 KiB.  Re-plans the matvec if set up.
+ *                  3 two rings of 2 x 56 KiB; 4 two rings of 4 x 24 KiB; 5 two rings of
+ *                  3 x 32 KiB.  Re-plans the matvec if set up.
  *   "mv_small_max" low-rank leaves up to this many bytes (default 16384) go through the
  *                  shared-memory pipeline, larger ones through the large-block kernels
  *   "mv_profile"   1: accumulate producer/consumer wait and work cycles of the CTA-ring

@@ -370,7 +370,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "part_ranks") { if (v < 1 || v > 4096) bad(); C.part_ranks = (int)v; }
     else if (k == "part_rank") { if (v < 0 || v > 4095) bad(); C.part_rank = (int)v; }
     else if (k == "record_pivots") { if (v != 0 && v != 1 && v != -1) bad(); C.record_pivots = (int)v; }
-    else if (k == "mv_kernel") { if (v < 0 || v > 3) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
+    else if (k == "mv_kernel") { if (v < 0 || v > 5) bad(); C.mv_kind = (int)v; if (C.have_setup) hm::plan_matvec(C); }
     else if (k == "mv_profile") {
       if (v != 0 && v != 1) bad();
       if (v == 1) { C.mv_prof.alloc(4); HM_CUDA(cudaMemsetAsync(C.mv_prof.get(), 0, 32, C.stream)); }

@@ -32,7 +32,16 @@ namespace hm {
 constexpr int kMvStageBytes = 48 * 1024;   // one k_mv_batched pipeline stage (= one batch)
 // stage bytes of option mv_kernel: 0 two CTAs x 2 x 48 KiB (default), 1 one CTA x 4 x 48 KiB,
 // 2 two CTAs x 3 x 36 KiB, 3 two CTAs x 2 x 56 KiB
-inline int64_t mv_stage_bytes(const Context& C) { return C.mv_kind == 2 ? 36 * 1024 : C.mv_kind == 3 ? 56 * 1024 : kMvStageBytes; }
+// 4 two CTAs x 4 x 24 KiB, 5 two CTAs x 3 x 32 KiB
+inline int64_t mv_stage_bytes(const Context& C) {
+  switch (C.mv_kind) {
+    case 2: return 36 * 1024;
+    case 3: return 56 * 1024;
+    case 4: return 24 * 1024;
+    case 5: return 32 * 1024;
+    default: return kMvStageBytes;
+  }
+}
 constexpr int kMaxX = 12;         // x_sigma ranges (bulk copies) per batch
 constexpr int64_t kXGap = 64;     // doubles: merge x ranges closer than this
 
@@ -333,10 +342,30 @@ __device__ __forceinline__ void warp_reduce_halving(double (&v)[KB], int lane) {
   for (int o = 16 >> LV; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
 }
 
+// binary32 factors: every widening must wait for the LAST raw load, else ptxas issues each
+// F2F right behind its load and the in-order warp stalls once per load (measured 1.8 TB/s).
+// zmask is 0 at run time but opaque to the compiler: OR-ing (all raw bits & zmask) into each
+// value makes every widening depend on every load, so all loads issue first.
+template <int K>
+__device__ __forceinline__ void order_after_all_loads(float (&a)[K], float (&b)[K], unsigned zmask) {
+  unsigned z = 0;
+#pragma unroll
+  for (int l = 0; l < K; ++l) z |= __float_as_uint(a[l]) | __float_as_uint(b[l]);
+  z &= zmask;
+#pragma unroll
+  for (int l = 0; l < K; ++l) {
+    a[l] = __uint_as_float(__float_as_uint(a[l]) | z);
+    b[l] = __uint_as_float(__float_as_uint(b[l]) | z);
+  }
+}
+template <int K>
+__device__ __forceinline__ void order_after_all_loads(double (&)[K], double (&)[K], unsigned) {}
+
 template <class E>
 __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ tiles, int64_t ntiles,
                                                       const MvLarge* __restrict__ L, const E* __restrict__ pool,
-                                                      const double* __restrict__ x, double* __restrict__ tbuf) {
+                                                      const double* __restrict__ x, double* __restrict__ tbuf,
+                                                      unsigned zmask) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -352,14 +381,17 @@ __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ 
     for (int j = T.j0 + lane; j < T.j1; j += 64) {
       const bool two = j + 32 < T.j1;
       const double xa = __ldg(xs + j), xb = two ? __ldg(xs + j + 32) : 0.0;
-      double va[16], vb[16];
+      // the raw factor loads all issue before the first use (binary32: widening each load
+      // right after it would stall the warp on every load)
+      E va[16], vb[16];
 #pragma unroll
       for (int l = 0; l < 16; ++l) {
-        va[l] = l < kc ? (double)__ldg(V + j + (int64_t)l * B.n) : 0.0;
-        vb[l] = (l < kc && two) ? (double)__ldg(V + j + 32 + (int64_t)l * B.n) : 0.0;
+        va[l] = l < kc ? __ldg(V + j + (int64_t)l * B.n) : E(0);
+        vb[l] = (l < kc && two) ? __ldg(V + j + 32 + (int64_t)l * B.n) : E(0);
       }
+      order_after_all_loads<16>(va, vb, zmask);
 #pragma unroll
-      for (int l = 0; l < 16; ++l) acc[l] = __fma_rn(vb[l], xb, __fma_rn(va[l], xa, acc[l]));
+      for (int l = 0; l < 16; ++l) acc[l] = __fma_rn((double)vb[l], xb, __fma_rn((double)va[l], xa, acc[l]));
     }
     warp_reduce_halving<16>(acc, lane);
     // lane L holds column 8*b4 + 4*b3 + 2*b2 + b1 (two lanes per column)
@@ -373,7 +405,8 @@ __global__ void __launch_bounds__(256) k_mv_large_v(const MvTileV* __restrict__ 
 template <class E>
 __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ tiles, int64_t ntiles,
                                                      const MvLarge* __restrict__ L, const E* __restrict__ pool,
-                                                     const double* __restrict__ tbuf, double* __restrict__ y) {
+                                                     const double* __restrict__ tbuf, double* __restrict__ y,
+                                                     unsigned zmask) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -391,15 +424,16 @@ __global__ void __launch_bounds__(256) k_mv_large_u(const MvTileU* __restrict__ 
       const double ta = __ldg(tl + l), tb = __ldg(tl + l + 1);
       const E* Ua = U + (int64_t)l * B.m;
       const E* Ub = Ua + B.m;
-      double ua[8], ub[8];
+      E ua[8], ub[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const bool ok = lane + 32 * q < rows;
-        ua[q] = ok ? (double)__ldg(Ua + 32 * q) : 0.0;
-        ub[q] = ok ? (double)__ldg(Ub + 32 * q) : 0.0;
+        ua[q] = ok ? __ldg(Ua + 32 * q) : E(0);
+        ub[q] = ok ? __ldg(Ub + 32 * q) : E(0);
       }
+      order_after_all_loads<8>(ua, ub, zmask);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = __fma_rn(ub[q], tb, __fma_rn(ua[q], ta, acc[q]));
+      for (int q = 0; q < 8; ++q) acc[q] = __fma_rn((double)ub[q], tb, __fma_rn((double)ua[q], ta, acc[q]));
     }
     if (l < B.k) {
       const double ta = __ldg(tl + l);
@@ -776,6 +810,10 @@ void plan_matvec(Context& C) {
                                  256 + 3 * 36 * 1024));
     HM_CUDA(cudaFuncSetAttribute(k_mv_batched<2, 56 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  256 + 2 * 56 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<4, 24 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 4 * 24 * 1024));
+    HM_CUDA(cudaFuncSetAttribute(k_mv_batched<3, 32 * 1024, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 256 + 3 * 32 * 1024));
     attr = true;
   }
 }
@@ -808,16 +846,16 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
   const bool f32 = C.lr_esz == 4;
   auto large_v = [&](cudaStream_t s) {
     if (f32) k_mv_large_v<float><<<148 * 8, 256, 0, s>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool32,
-                                                          x_int, C.mv_tbuf.get());
+                                                          x_int, C.mv_tbuf.get(), 0u);
     else k_mv_large_v<double><<<148 * 8, 256, 0, s>>>(C.mv_tiles_v.get(), C.mv_n_tiles_v, C.mv_large.get(), pool,
-                                                       x_int, C.mv_tbuf.get());
+                                                       x_int, C.mv_tbuf.get(), 0u);
     HM_CHECK_LAUNCH();
   };
   auto large_u = [&](cudaStream_t s) {
     if (f32) k_mv_large_u<float><<<148 * 8, 256, 0, s>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool32,
-                                                          C.mv_tbuf.get(), y_int);
+                                                          C.mv_tbuf.get(), y_int, 0u);
     else k_mv_large_u<double><<<148 * 8, 256, 0, s>>>(C.mv_tiles_u.get(), C.mv_n_tiles_u, C.mv_large.get(), pool,
-                                                       C.mv_tbuf.get(), y_int);
+                                                       C.mv_tbuf.get(), y_int, 0u);
     HM_CHECK_LAUNCH();
   };
   // option mv_concurrent (default on): the large low-rank blocks (V^T x, then U z) stream on
@@ -849,6 +887,14 @@ void matvec_internal(Context& C, const double* x_int, double* y_int, bool reduce
           (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
     else if (C.mv_kind == 3)
       k_mv_batched<2, 56 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 2 * 56 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
+    else if (C.mv_kind == 4)
+      k_mv_batched<4, 24 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 4 * 24 * 1024, st>>>(
+          C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
+          (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
+    else if (C.mv_kind == 5)
+      k_mv_batched<3, 32 * 1024, 256, 2><<<C.mv_grid, 256, 256 + 3 * 32 * 1024, st>>>(
           C.mv_batches.get(), C.mv_segs.get(), C.mv_nsegs, C.mv_cta.get(), (const char*)C.dstore.get(), (const char*)pool,
           (const char*)C.mv_tasks.get(), x_int, y_int, scramble, prof, f32 ? 1 : 0);
     else                     // one CTA ring per SM, 4 x 48 KiB stages, 15 consumer warps
