@@ -96,6 +96,15 @@ def test_error_codes_and_state_machine():
         H.set_option("nope", 1)
     with pytest.raises(HMError):
         H.set_option("k_max", 0)
+    # peer-memory collectives: single-rank contexts cannot export, solve_comm 1 needs an import
+    from paper_1806_11558_b200 import hm
+    with pytest.raises(HMError) as e:
+        hm.hm_p2p_export(H.ctx, 320)
+    assert e.value.status == 2
+    with pytest.raises(HMError) as e:
+        H.set_option("solve_comm", 1)
+    assert e.value.status == 2
+    assert H.get_option("solve_comm") == 0
     H.setup(1e-6)
     st = H.stats()
     assert st["N"] == 320 and st["adm_leaves"] == 0 and st["dense_leaves"] == 256
