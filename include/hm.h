@@ -118,10 +118,12 @@ const char* hm_last_error(hm_ctx ctx);
  *   "mv_concurrent" 1 (default): the large low-rank matvec kernels run on a library side
  *                  stream beside the small-leaf pipeline (joined before hm_matvec returns its
  *                  stream order); 0: one stream
- *   "cost_model"   leaf cost of the partition over ranks (A18): 2 (default) dense leaves |t||s|
+ *   "cost_model"   leaf cost of the partition over ranks (A18): 0 (default) dense leaves
+ *                  |t||s|, admissible leaves (|t|+|s|) x 10 (~ stored bytes: balances the
+ *                  matvec and, with the near field beside ACA, the setup); 2 dense leaves
  *                  weighted by kind (t = s 110, boxes touching 26, separated 10), admissible
- *                  leaves (|t|+|s| + 21) x 10; 1 a size-dependent rank estimate for admissible
- *                  leaves; 0 round 1 (|t||s|, (|t|+|s|) x 10).  Takes effect at hm_build_tree.
+ *                  leaves (|t|+|s| + 21) x 10 (best for a serial setup); 1 a size-dependent
+ *                  rank estimate for admissible leaves.  Takes effect at hm_build_tree.
  *   "part_ranks", "part_rank"  DIAGNOSTIC (world_size 1 only): build rank part_rank's share of a
  *                  part_ranks-way partition (no collectives), to measure every rank's setup of
  *                  a p-GPU run on one GPU.  Takes effect at hm_build_tree.

@@ -285,7 +285,7 @@ struct Context {
   double aca_prev_bytes = 0, aca_prev_eps = -1;
   int aca_prev_kmax = 0, aca_prev_esz = 0;
   int part_ranks = 1, part_rank = 0;   // diagnostic options: emulate rank part_rank of a part_ranks-way partition (world 1)
-  int cost_model = 2;          // option "cost_model": leaf cost of the partition (A18): 0 round-1 proxy, 1 evaluation model, 2 (default) kind weights + per-block ACA cost
+  int cost_model = 0;          // option "cost_model": leaf cost of the partition (A18): 0 (default) size proxy, 1 evaluation model, 2 kind weights + per-block ACA cost
   int aca_upd_occ = 1;         // option "aca_upd_occ": CTAs per SM of k_aca_update (0: 16, 1: 24 default, 2: 32)
   int lr_f32 = 0;              // option "lr_f32": store the ACA factors U, V in binary32 (dense blocks stay FP64)
   int lr_esz = 8;              // bytes per stored factor entry of the current setup (8, or 4 with lr_f32)
