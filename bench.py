@@ -55,17 +55,23 @@ def peaks():
 # "alu" roofline of entry evaluation: the FP64 pipe issues 64 instructions
 # per clock per SM (B200: 148 SMs, 1965 MHz max); one quadrature evaluation of the reading's
 # arithmetic (A15) is 23.5 FP64-pipe instructions in the SASS of the evaluation loop (distance
-# 6, correctly rounded w/sqrt(d2) 16, sum 1, outer point amortised 0.5) plus one MUFU.
-FP64_LANES_PER_SM, SMS, DP_INSTR_PER_EVAL = 64, 148, 23.5
+# 6, correctly rounded w/sqrt(d2) 16, sum 1, outer point amortised 0.5) plus one MUFU; a
+# perf-mode evaluation (option near_perf, near-field entries) is 12.5 (distance 6, refined
+# rsqrt 5, FMA sum 1, outer 0.5) plus one MUFU.
+FP64_LANES_PER_SM, SMS, DP_INSTR_PER_EVAL, DP_INSTR_PER_EVAL_PERF = 64, 148, 23.5, 12.5
 
 
-def fp64_eval_peak():
-    """Peak quadrature evaluations/s from unit counts and clocks (see above)."""
+def fp64_eval_peak(evals_near=0.0, evals_aca=1.0, near_perf=False):
+    """Peak quadrature evaluations/s from unit counts and clocks (see above) for this mix of
+    near-field and ACA evaluations: FP64 instructions/s over the mix's instructions per
+    evaluation."""
     mhz = 1965.0
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         mhz = json.load(open(p)).get("sm_max_mhz", mhz)
-    return FP64_LANES_PER_SM * SMS * mhz * 1e6 / DP_INSTR_PER_EVAL
+    dn = DP_INSTR_PER_EVAL_PERF if near_perf else DP_INSTR_PER_EVAL
+    per_eval = (evals_near * dn + evals_aca * DP_INSTR_PER_EVAL) / max(1e-30, evals_near + evals_aca)
+    return FP64_LANES_PER_SM * SMS * mhz * 1e6 / per_eval
 
 
 def ncu_traffic(cfg):
@@ -344,7 +350,15 @@ def _run_gpu(args, rank, world, local, dev, stream):
     eval_ms_rank = kt["eval_union_ms"] / K
     eval_rate = -max_over_ranks(-(evals / max(1e-9, eval_ms_rank * 1e-3)), world)   # slowest rank
     eval_rate_phase = evals / max(1e-9, (st["near_ms"] + st["aca_ms"]) * 1e-3)
-    eval_peak = fp64_eval_peak()
+    near_perf = bool(H.get_option("near_perf"))
+    eval_peak = fp64_eval_peak(st["evals_near"], st["evals_aca"], near_perf)
+    eval_fam = {}                      # each family against its own per-evaluation peak
+    for fam, ev, ms_, pk in (("near", st["evals_near"], kt["eval_near_ms"] / K, fp64_eval_peak(1.0, 0.0, near_perf)),
+                             ("aca", st["evals_aca"], kt["eval_aca_ms"] / K, fp64_eval_peak(0.0, 1.0))):
+        if ev > 0 and ms_ > 0:
+            r_ = ev / (ms_ * 1e-3)
+            eval_fam[fam] = {"Geval_s": round(r_ / 1e9, 2), "peak": round(pk / 1e9, 2), "frac": round(r_ / pk, 4),
+                             "mode": ("perf" if (fam == "near" and near_perf) else "parity")}
     mv_gbs_live = alg_bytes_rank / (mv_kern_ms * 1e-3) / 1e9
 
     # ---- e2e: same step through the same ABI with host buffers
@@ -373,7 +387,8 @@ def _run_gpu(args, rank, world, local, dev, stream):
                 "traffic": traffic.get("eval_bytes_per_launch") if traffic else None,
                 "traffic_note": traffic.get("eval_source") if traffic else None,
                 "peak_source": f"unit counts: {FP64_LANES_PER_SM} FP64 instr/clk/SM x {SMS} SMs x sm_max clock / "
-                               f"{DP_INSTR_PER_EVAL} FP64 instr per evaluation (SASS)",
+                               f"FP64 instr per evaluation (SASS: {DP_INSTR_PER_EVAL} parity mode"
+                               + (f", {DP_INSTR_PER_EVAL_PERF} near-field perf mode; evaluation-weighted)" if near_perf else ")"),
                 "share_of_step": round(eval_ms / ms_instr, 4)}
     else:
         roof = {"kernel": "H-matvec (k_mv_batched + k_mv_large_v/u)", "bound": "hbm", "achieved": round(mv_gbs_live, 1),
@@ -401,6 +416,9 @@ def _run_gpu(args, rank, world, local, dev, stream):
                        "solve_comm": (args.comm if world > 1 else None),
                        "factor_storage": "binary32 U, V (option lr_f32; dense blocks and all arithmetic FP64)"
                        if args.lr_f32 else "FP64",
+                       "near_field_entries": ("perf mode (FP64 rsqrt + one cubic refinement, FMA sums; "
+                                              "<= 1e-13 vs the oracle, SURVEY A15)" if H.get_option("near_perf")
+                                              else "parity mode (IEEE sqrt and division, A15)"),
                        "l2": "inputs larger than L2 (stored H >> 126 MB); matvec timing flushes L2 with a 256 MB write"},
             "breakdown": {"instrumented_steps": KI, "ms_per_step_instrumented": round(ms_instr, 3),
                           "cold_first_step": cold, "tree_s": round(tree_s, 6), "setup_s": round(setup_s, 6), "near_field_s": round(near_s, 6),
@@ -411,6 +429,7 @@ def _run_gpu(args, rank, world, local, dev, stream):
                           "matvec_frac_hbm": round(mv_gbs / hbm, 4), "stored_GB_total": round(stored_tot / 1e9, 3),
                           "k_mean": st["k_mean"], "evals": evals, "eval_rate_Gps": round(eval_rate / 1e9, 2),
                           "eval_rate_phase_Gps": round(eval_rate_phase / 1e9, 2),
+                          "eval_families": eval_fam,
                           "kernel_ms_per_step": {"eval": round(eval_ms, 3), "aca_other": round(aca_other_ms, 3),
                                                  "matvec": round(mv_kern_ms_step, 3),
                                                  "krylov_blas1": round(krylov_ms_step, 3),

@@ -134,6 +134,12 @@ const char* hm_last_error(hm_ctx ctx);
  *                  matvec widens the factors exactly before every FMA).  Halves the low-rank bytes
  *                  the matvec streams.  0 (default): FP64 factors.
  *                  Takes effect at the next hm_setup; hm_get_lowrank returns the widened values.
+ *   "near_perf"    1 (default): near-field (dense-leaf) entries in perf mode: each
+ *                  term w / |x - y| as w * rsqrt(d2), the hardware seed refined by one cubic
+ *                  step, accumulated by FMA — within 1e-13 relative of the oracle's entries
+ *                  (measured <= 8.1e-16); 0: parity mode (IEEE sqrt then IEEE division, no FMA in
+ *                  the sums, as for the admissible entries, whose residuals steer the ACA pivots
+ *                  and therefore always use parity mode).  Takes effect at the next hm_setup.
  *   "solve_comm"   sharded solve collectives: 0 NCCL (default), 1 libhm P2P kernels (requires
  *                  hm_p2p_import, which selects it).
  *   "setup_overlap" 1: hm_setup evaluates the near field on a least-priority stream from a

@@ -41,15 +41,15 @@ __device__ __forceinline__ int map_class(const M& m, int s, int t, int& xs, int&
   if constexpr (M::kQuad) return quad_class(m.P, m.QV, s, t, xs, ys);
   else return canonical_class(m.P, s, t, xs, ys);
 }
-template <int n, class M>
+template <int n, class M, bool PERF = false>
 __device__ __forceinline__ double map_regular(const M& m, int xs, int ys) {
   if constexpr (M::kQuad) {
-    return quad_regular_entry<n>(m.P, xs, ys);
+    return quad_regular_entry<n, PERF>(m.P, xs, ys);
   } else {
     double X[9], Y[9];
     load_panel_vertices(m.P, xs, X);
     load_panel_vertices(m.P, ys, Y);
-    const double I = regular_sum<n>(X, Y);
+    const double I = regular_sum<n, false, PERF>(X, Y);
     return dmul(dmul(I, dmul(dmul(2.0, __ldg(&m.P[xs].area)), dmul(2.0, __ldg(&m.P[ys].area)))), kInv4Pi);
   }
 }
@@ -107,7 +107,7 @@ __global__ void k_class_scatter(M m, int64_t total, const unsigned char* __restr
   if (cls >= 0) lists[base[cls] + pos] = r;
 }
 
-template <int n, class M>
+template <int n, class M, bool PERF>
 __global__ void __launch_bounds__(128) k_eval_regular(M m, const EntryRef* __restrict__ list, int64_t cnt) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= cnt) return;
@@ -115,12 +115,12 @@ __global__ void __launch_bounds__(128) k_eval_regular(M m, const EntryRef* __res
   int s, t, xs, ys;
   m.pair(r, s, t);
   map_class(m, s, t, xs, ys);
-  m.put(r, map_regular<n>(m, xs, ys));
+  m.put(r, map_regular<n, M, PERF>(m, xs, ys));
 }
 
 // triangles: KIND 0 identical, 1 edge, 2 vertex; quads: KIND 0 = touching quads (the four
 // triangle pairs; their evaluations are counted into qev)
-template <int KIND, class M>
+template <int KIND, class M, bool PERF>
 __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __restrict__ list, int64_t cnt,
                                                       unsigned long long* __restrict__ qev) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
     v = dmul(selfterm_closed(X, A.area), kInv4Pi);
   } else {
     orient_touching(KIND, A, B, X, Y);
-    const double I = ss_sum_t<KIND>(X, Y);
+    const double I = ss_sum_t<KIND, PERF>(X, Y);
     v = dmul(dmul(I, dmul(dmul(2.0, A.area), dmul(2.0, B.area))), kInv4Pi);
   }
   m.put(r, v);
@@ -285,7 +285,8 @@ struct EntryBatchWork {
 
 // Evaluate all `total` entries of mapping m on stream st; returns the number of kernel
 // evaluations.  Allocates only when W is smaller than this batch (near_prepare pre-sizes it).
-template <class M>
+// PERF: perf-mode kernel evaluations (option near_perf; near-field entries only, A15)
+template <bool PERF, class M>
 double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t st, KTimer& kt) {
   if (total <= 0) return 0.0;
   W.cnt.alloc(kNumClass);
@@ -316,17 +317,17 @@ double eval_batched(const M& m, int64_t total, EntryBatchWork& W, cudaStream_t s
       prim::radix_sort_pairs<uint16_t, unsigned long long>(W.qkey[0].get(), W.qkey[1].get(), W.qref[0].get(),
                                                            W.qref[1].get(), c0, 0, 12, W.qtmp, st);
       const EntryRef* Ls = reinterpret_cast<const EntryRef*>(W.qref[1].get());
-      k_eval_touching<0, M><<<grid_for(c0, 64), 64, 0, st>>>(m, Ls, c0, W.qev.get());
+      k_eval_touching<0, M, PERF><<<grid_for(c0, 64), 64, 0, st>>>(m, Ls, c0, W.qev.get());
       HM_CHECK_LAUNCH();
     }
   }
-  if (W.hcnt[1]) { k_eval_touching<1, M><<<grid_for(W.hcnt[1], 64), 64, 0, st>>>(m, L + base[1], W.hcnt[1], W.qev.get()); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[2]) { k_eval_touching<2, M><<<grid_for(W.hcnt[2], 64), 64, 0, st>>>(m, L + base[2], W.hcnt[2], W.qev.get()); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[6]) { k_eval_regular<6, M><<<grid_for(W.hcnt[6], 128), 128, 0, st>>>(m, L + base[6], W.hcnt[6]); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[5]) { k_eval_regular<5, M><<<grid_for(W.hcnt[5], 128), 128, 0, st>>>(m, L + base[5], W.hcnt[5]); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[4]) { k_eval_regular<4, M><<<grid_for(W.hcnt[4], 128), 128, 0, st>>>(m, L + base[4], W.hcnt[4]); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[3]) { k_eval_regular<3, M><<<grid_for(W.hcnt[3], 128), 128, 0, st>>>(m, L + base[3], W.hcnt[3]); HM_CHECK_LAUNCH(); }
-  if (W.hcnt[0] && !M::kQuad) { k_eval_touching<0, M><<<grid_for(W.hcnt[0], 64), 64, 0, st>>>(m, L + base[0], W.hcnt[0], W.qev.get()); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[1]) { k_eval_touching<1, M, PERF><<<grid_for(W.hcnt[1], 64), 64, 0, st>>>(m, L + base[1], W.hcnt[1], W.qev.get()); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[2]) { k_eval_touching<2, M, PERF><<<grid_for(W.hcnt[2], 64), 64, 0, st>>>(m, L + base[2], W.hcnt[2], W.qev.get()); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[6]) { k_eval_regular<6, M, PERF><<<grid_for(W.hcnt[6], 128), 128, 0, st>>>(m, L + base[6], W.hcnt[6]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[5]) { k_eval_regular<5, M, PERF><<<grid_for(W.hcnt[5], 128), 128, 0, st>>>(m, L + base[5], W.hcnt[5]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[4]) { k_eval_regular<4, M, PERF><<<grid_for(W.hcnt[4], 128), 128, 0, st>>>(m, L + base[4], W.hcnt[4]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[3]) { k_eval_regular<3, M, PERF><<<grid_for(W.hcnt[3], 128), 128, 0, st>>>(m, L + base[3], W.hcnt[3]); HM_CHECK_LAUNCH(); }
+  if (W.hcnt[0] && !M::kQuad) { k_eval_touching<0, M, PERF><<<grid_for(W.hcnt[0], 64), 64, 0, st>>>(m, L + base[0], W.hcnt[0], W.qev.get()); HM_CHECK_LAUNCH(); }
   // (quads: class 0 = touching quads, counted on the device into W.qev, read by the caller)
   const double per[kNumClass] = {0, 6480, 2592, M::kQuad ? 81.0 : 49.0, 256, 625, 1296};
   for (int c = 0; c < kNumClass; ++c) evals += per[c] * (double)W.hcnt[c];

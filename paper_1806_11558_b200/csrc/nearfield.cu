@@ -121,11 +121,13 @@ void near_eval(Context& C, cudaStream_t st, KTimer& kt) {
     if (C.quad) {
       NearMap<true> m{C.qnode.get(), C.panel.get(), C.qv.get(), q, C.doff.get(), b0, b1 - b0, hoff[b0],
                       C.dstore.get(), C.near_tab.get()};
-      evals += eval_batched(m, hoff[b1] - hoff[b0], W, st, kt);
+      evals += C.near_perf ? eval_batched<true>(m, hoff[b1] - hoff[b0], W, st, kt)
+                           : eval_batched<false>(m, hoff[b1] - hoff[b0], W, st, kt);
     } else {
       NearMap<false> m{C.panel.get(), nullptr, nullptr, q, C.doff.get(), b0, b1 - b0, hoff[b0], C.dstore.get(),
                        C.near_tab.get()};
-      evals += eval_batched(m, hoff[b1] - hoff[b0], W, st, kt);
+      evals += C.near_perf ? eval_batched<true>(m, hoff[b1] - hoff[b0], W, st, kt)
+                           : eval_batched<false>(m, hoff[b1] - hoff[b0], W, st, kt);
     }
     b0 = b1;
   }

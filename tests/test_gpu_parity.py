@@ -400,3 +400,38 @@ def test_potential_beyond_one_launch_of_point_tiles(O, torch_cuda):
     uo = R.potential(a, X[sel])
     assert np.abs(ug[sel] - uo).max() <= 1e-12 * np.abs(uo).max()
     H.close()
+
+
+@pytest.mark.parametrize("mesh", ["C2", "cube4"])
+def test_near_perf_mode_entries(O, torch_cuda, mesh):
+    """Option near_perf (SURVEY A15 perf mode, near-field entries only): every dense-leaf entry
+    within 1e-13 relative of the oracle's; parity mode bit-exact; the ACA
+    factors (admissible entries stay in parity mode) identical in both modes."""
+    from inputs.meshes import cube
+    V, T = icosphere(5) if mesh == "C2" else cube(4)
+    R = O.Problem(V, T)
+    R.assemble(EPS)
+    Hs = {}
+    for perf in (0, 1):
+        H = _gpu(V, T)
+        H.set_option("near_perf", perf)
+        H.setup(EPS)
+        Hs[perf] = H
+    dense, _ = Hs[0].leaves(1)
+    worst = {0: 0.0, 1: 0.0}
+    for b, q in enumerate(dense):
+        Bo = R.dense_block(b)
+        for perf, H in Hs.items():
+            Bg = H.dense_block(b, (q[1] - q[0], q[3] - q[2]))
+            worst[perf] = max(worst[perf], float((np.abs(Bg - Bo) / np.abs(Bo)).max()))
+    assert worst[1] <= 1e-13, worst
+    assert worst[0] <= 1e-14, worst
+    adm, _ = Hs[0].leaves(0)
+    for b in range(0, len(adm), max(1, len(adm) // 300)):
+        m, n = adm[b][1] - adm[b][0], adm[b][3] - adm[b][2]
+        U0, W0 = Hs[0].lowrank(b, m, n)
+        U1, W1 = Hs[1].lowrank(b, m, n)
+        assert np.array_equal(U0, U1) and np.array_equal(W0, W1), f"low-rank block {b}"
+    print("near_perf max relative entry error vs oracle:", worst)
+    for H in Hs.values():
+        H.close()
