@@ -207,6 +207,8 @@ def _run_gpu(args, rank, world, local, dev, stream):
     H.set_option("restart", 100)
     if args.lr_f32:                     # SURVEY §8(f)-4 option: ACA factors stored in binary32
         H.set_option("lr_f32", 1)
+    if args.aca_perf:
+        H.set_option("aca_perf", 1)
     # rhs = the paper's f, assembled by the library
     H.build_tree(Vd, Td, LEAF, ETA)
     if world > 1 and args.comm == "p2p":     # x all-gather / y reduce-scatter / dot all-reduce over NVLink P2P
@@ -416,6 +418,9 @@ def _run_gpu(args, rank, world, local, dev, stream):
                        "solve_comm": (args.comm if world > 1 else None),
                        "factor_storage": "binary32 U, V (option lr_f32; dense blocks and all arithmetic FP64)"
                        if args.lr_f32 else "FP64",
+                       "aca_entries": ("perf mode (option aca_perf; pivots identical to the oracle's on 99.9997% "
+                                       "of blocks at C3)" if H.get_option("aca_perf") else
+                                       "parity mode (bit-identical to the oracle, A15)"),
                        "near_field_entries": ("perf mode (FP64 rsqrt + one cubic refinement, FMA sums; "
                                               "<= 1e-13 vs the oracle, SURVEY A15)" if H.get_option("near_perf")
                                               else "parity mode (IEEE sqrt and division, A15)"),
@@ -619,6 +624,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--instrumented-steps", type=int, default=2)
     ap.add_argument("--lr-f32", action="store_true", help="store the ACA factors in binary32 (option lr_f32)")
+    ap.add_argument("--aca-perf", action="store_true",
+                    help="ACA order-3/4 entries in perf mode too (option aca_perf; deviates from reading A15)")
     ap.add_argument("--comm", default="p2p", choices=["p2p", "nccl"],
                     help="sharded-solve collectives (N > 1): libhm peer-memory kernels or NCCL")
     args = ap.parse_args()

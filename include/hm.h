@@ -140,6 +140,11 @@ const char* hm_last_error(hm_ctx ctx);
  *                  (measured <= 8.1e-16); 0: parity mode (IEEE sqrt then IEEE division, no FMA in
  *                  the sums, as for the admissible entries, whose residuals steer the ACA pivots
  *                  and therefore always use parity mode).  Takes effect at the next hm_setup.
+ *   "aca_perf"     1: the ACA row / column entries of orders 3 and 4 in the same perf mode —
+ *                  NOT reading A15 (which keeps admissible entries bit-identical to the oracle so
+ *                  that the ACA pivots coincide): measured identical rank and pivots on 99.9991%
+ *                  (C2) / 99.9997% (C3) of the blocks, solutions within 6.3e-9 / 1.5e-9 of the
+ *                  oracle's, C4 ACA evaluation -19%.  0 (default): parity mode.  Triangles only.
  *   "solve_comm"   sharded solve collectives: 0 NCCL (default), 1 libhm P2P kernels (requires
  *                  hm_p2p_import, which selects it).
  *   "setup_overlap" 1: hm_setup evaluates the near field on a least-priority stream from a

@@ -101,9 +101,10 @@ __global__ void k_step_totals(const int64_t* __restrict__ rpre, const int64_t* _
 // for entry_batch.cuh.  put() applies the rank-one corrections of the previous k steps in
 // ascending l, each product and difference separately rounded (A15), and stores the residual
 // into column k of the block's V (row step) or U (column step) workspace.
-template <bool ROW, bool QUAD = false>
+template <bool ROW, bool QUAD = false, bool PERF = false>
 struct AcaMap {
   static constexpr bool kQuad = QUAD;
+  static constexpr bool kPerf = PERF;   // option aca_perf: order-3/4 entries in perf mode (A15 deviation, measured)
   const Panel* P;       // triangle panels, or node panels of a quadrilateral mesh (A25)
   const Panel* PT;      // quads: the split triangles
   const int4* QV;       // quads: vertex ids
@@ -662,6 +663,9 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     if (C.quad)
       aca_eval(C, AcaMap<true, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(), W.rtab.get(),
                                      nb, Uw, Vw}, drow, rmax, W);
+    else if (C.aca_perf)
+      aca_eval(C, AcaMap<true, false, true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
+                                            W.rtab.get(), nb, Uw, Vw}, drow, rmax, W);
     else
       aca_eval(C, AcaMap<true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.rpre.get(), W.act.get(),
                                W.rtab.get(), nb, Uw, Vw}, drow, rmax, W);
@@ -677,6 +681,9 @@ void run_chunk(Context& C, AcaWork& W, const std::vector<int32_t>& ids, int kws,
     if (C.quad)
       aca_eval(C, AcaMap<false, true>{Pn, P, QV, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(), W.ctab.get(),
                                       nb, Uw, Vw}, dcol, cmax, W);
+    else if (C.aca_perf)
+      aca_eval(C, AcaMap<false, false, true>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(),
+                                             W.act.get(), W.ctab.get(), nb, Uw, Vw}, dcol, cmax, W);
     else
       aca_eval(C, AcaMap<false>{P, nullptr, nullptr, W.blk.get(), W.state.get(), W.cpre.get(), W.act.get(),
                                 W.ctab.get(), nb, Uw, Vw}, dcol, cmax, W);

@@ -380,6 +380,7 @@ hm_status hm_set_option(hm_ctx ctx, const char* key, double v) {
     else if (k == "mv_scramble") { if (v != 0 && v != 1) bad(); C.mv_scramble = (int)v; }
     else if (k == "setup_overlap") { if (v != 0 && v != 1) bad(); C.setup_overlap = (int)v; }
     else if (k == "near_perf") { if (v != 0 && v != 1) bad(); C.near_perf = (int)v; }
+    else if (k == "aca_perf") { if (v != 0 && v != 1) bad(); C.aca_perf = (int)v; }
     else if (k == "solve_comm") {
       if (v != 0 && v != 1) bad();
       if (v == 1 && !C.p2p.ready) hm::fail(HM_ERR_STATE, "option solve_comm = 1 needs hm_p2p_import");
@@ -418,6 +419,7 @@ hm_status hm_get_option(hm_ctx ctx, const char* key, double* v) {
     else if (k == "setup_overlap") *v = C.setup_overlap;
     else if (k == "solve_comm") *v = C.solve_comm;
     else if (k == "near_perf") *v = C.near_perf;
+    else if (k == "aca_perf") *v = C.aca_perf;
     else if (k == "mv_concurrent") *v = C.mv_concurrent;
     else hm::fail(HM_ERR_ARG, "hm_get_option: unknown key '" + k + "'");
   });

@@ -190,7 +190,7 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
   if (cls == 4) lists[base4 + __popc(b4 & below)] = r;
   else if (cls >= 0 && cls != 3) lists[total - 1 - (baser + __popc(br & below))] = r;
   if (cls == 3) {
-    m.put(r, map_regular<3>(m, xs, ys));
+    m.put(r, map_regular<3, M, M::kPerf>(m, xs, ys));
     ev += M::kQuad ? 81 : tri_rule_points(3) * tri_rule_points(3);
   }
 }
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(128) k_eval_list(M m, const EntryRef* __restri
     int s, t, xs, ys;
     m.pair(r, s, t);
     map_class(m, s, t, xs, ys);
-    m.put(r, map_regular<n>(m, xs, ys));
+    m.put(r, map_regular<n, M, M::kPerf>(m, xs, ys));
   }
   constexpr int np = M::kQuad ? n * n : tri_rule_points(n);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(evals, (unsigned long long)(np * np) * (unsigned long long)c);

