@@ -61,7 +61,7 @@ def peaks():
 FP64_LANES_PER_SM, SMS, DP_INSTR_PER_EVAL, DP_INSTR_PER_EVAL_PERF = 64, 148, 23.5, 12.5
 
 
-def fp64_eval_peak(evals_near=0.0, evals_aca=1.0, near_perf=False):
+def fp64_eval_peak(evals_near=0.0, evals_aca=1.0, near_perf=False, aca_perf=False):
     """Peak quadrature evaluations/s from unit counts and clocks (see above) for this mix of
     near-field and ACA evaluations: FP64 instructions/s over the mix's instructions per
     evaluation."""
@@ -70,7 +70,8 @@ def fp64_eval_peak(evals_near=0.0, evals_aca=1.0, near_perf=False):
     if os.path.exists(p):
         mhz = json.load(open(p)).get("sm_max_mhz", mhz)
     dn = DP_INSTR_PER_EVAL_PERF if near_perf else DP_INSTR_PER_EVAL
-    per_eval = (evals_near * dn + evals_aca * DP_INSTR_PER_EVAL) / max(1e-30, evals_near + evals_aca)
+    da = DP_INSTR_PER_EVAL_PERF if aca_perf else DP_INSTR_PER_EVAL
+    per_eval = (evals_near * dn + evals_aca * da) / max(1e-30, evals_near + evals_aca)
     return FP64_LANES_PER_SM * SMS * mhz * 1e6 / per_eval
 
 
@@ -353,14 +354,16 @@ def _run_gpu(args, rank, world, local, dev, stream):
     eval_rate = -max_over_ranks(-(evals / max(1e-9, eval_ms_rank * 1e-3)), world)   # slowest rank
     eval_rate_phase = evals / max(1e-9, (st["near_ms"] + st["aca_ms"]) * 1e-3)
     near_perf = bool(H.get_option("near_perf"))
-    eval_peak = fp64_eval_peak(st["evals_near"], st["evals_aca"], near_perf)
+    aca_perf = bool(H.get_option("aca_perf"))
+    eval_peak = fp64_eval_peak(st["evals_near"], st["evals_aca"], near_perf, aca_perf)
     eval_fam = {}                      # each family against its own per-evaluation peak
-    for fam, ev, ms_, pk in (("near", st["evals_near"], kt["eval_near_ms"] / K, fp64_eval_peak(1.0, 0.0, near_perf)),
-                             ("aca", st["evals_aca"], kt["eval_aca_ms"] / K, fp64_eval_peak(0.0, 1.0))):
+    for fam, ev, ms_, perf in (("near", st["evals_near"], kt["eval_near_ms"] / K, near_perf),
+                               ("aca", st["evals_aca"], kt["eval_aca_ms"] / K, aca_perf)):
+        pk = fp64_eval_peak(1.0, 0.0, perf) if fam == "near" else fp64_eval_peak(0.0, 1.0, False, perf)
         if ev > 0 and ms_ > 0:
             r_ = ev / (ms_ * 1e-3)
             eval_fam[fam] = {"Geval_s": round(r_ / 1e9, 2), "peak": round(pk / 1e9, 2), "frac": round(r_ / pk, 4),
-                             "mode": ("perf" if (fam == "near" and near_perf) else "parity")}
+                             "mode": "perf" if perf else "parity"}
     mv_gbs_live = alg_bytes_rank / (mv_kern_ms * 1e-3) / 1e9
 
     # ---- e2e: same step through the same ABI with host buffers
@@ -390,7 +393,8 @@ def _run_gpu(args, rank, world, local, dev, stream):
                 "traffic_note": traffic.get("eval_source") if traffic else None,
                 "peak_source": f"unit counts: {FP64_LANES_PER_SM} FP64 instr/clk/SM x {SMS} SMs x sm_max clock / "
                                f"FP64 instr per evaluation (SASS: {DP_INSTR_PER_EVAL} parity mode"
-                               + (f", {DP_INSTR_PER_EVAL_PERF} near-field perf mode; evaluation-weighted)" if near_perf else ")"),
+                               + (f", {DP_INSTR_PER_EVAL_PERF} perf mode; evaluation-weighted)"
+                                  if (near_perf or aca_perf) else ")"),
                 "share_of_step": round(eval_ms / ms_instr, 4)}
     else:
         roof = {"kernel": "H-matvec (k_mv_batched + k_mv_large_v/u)", "bound": "hbm", "achieved": round(mv_gbs_live, 1),
