@@ -54,11 +54,11 @@ def peaks():
 
 # "alu" roofline of entry evaluation: the FP64 pipe issues 64 instructions
 # per clock per SM (B200: 148 SMs, 1965 MHz max); one quadrature evaluation of the reading's
-# arithmetic (A15) is 23.5 FP64-pipe instructions in the SASS of the evaluation loop (distance
-# 6, correctly rounded w/sqrt(d2) 16, sum 1, outer point amortised 0.5) plus one MUFU; a
-# perf-mode evaluation (option near_perf, near-field entries) is 12.5 (distance 6, refined
-# rsqrt 5, FMA sum 1, outer 0.5) plus one MUFU.
-FP64_LANES_PER_SM, SMS, DP_INSTR_PER_EVAL, DP_INSTR_PER_EVAL_PERF = 64, 148, 23.5, 12.5
+# arithmetic (A15) is 21.5 FP64-pipe instructions in the SASS of the evaluation loop (distance
+# 6, correctly rounded w/sqrt(d2) 14, sum 1, outer point amortised 0.5) plus one MUFU (23.5
+# with round 1's two Newton steps); a perf-mode evaluation (option near_perf, near-field
+# entries) is 12.5 (distance 6, refined rsqrt 5, FMA sum 1, outer 0.5) plus one MUFU.
+FP64_LANES_PER_SM, SMS, DP_INSTR_PER_EVAL, DP_INSTR_PER_EVAL_PERF = 64, 148, 21.5, 12.5
 
 
 def fp64_eval_peak(evals_near=0.0, evals_aca=1.0, near_perf=False, aca_perf=False):
