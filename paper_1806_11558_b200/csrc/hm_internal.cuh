@@ -393,6 +393,7 @@ void p2p_release(Context& C);
 void p2p_check_capacity(Context& C, int64_t S);
 void p2p_allgather(Context& C, const double* x, int64_t n, int64_t S, bool into_ypart = false);
 void p2p_reduce_scatter(Context& C, double* y, int64_t n, int64_t S);
+void p2p_scale_publish(Context& C, const double* a, const double* sden, double* out, int64_t n, int64_t S);
 void p2p_allreduce(Context& C, double* buf, int64_t n);
 // entries (entry.cu)
 void eval_entries(Context& C, int64_t n, const int64_t* d_pairs, double* d_out);

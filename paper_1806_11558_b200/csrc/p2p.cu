@@ -86,6 +86,32 @@ __global__ void __launch_bounds__(256) k_p2p_allgather(Peers P, const double* __
   }
 }
 
+// Fused normalisation + all-gather (GMRES: v = w / h for the next product): out[t] = a[t] / *s
+// for this rank's slice, and the same value stored into every rank's xfull at r S + t, then the
+// all-gather's flags — the product that follows reads xfull without a separate all-gather.
+__global__ void __launch_bounds__(256) k_p2p_scale_publish(Peers P, const double* __restrict__ a,
+                                                           const double* __restrict__ sden, double* __restrict__ out,
+                                                           int64_t n, int64_t S, unsigned long long epoch) {
+  __shared__ bool last;
+  const double f = 1.0 / *sden;
+  const int64_t o = (int64_t)P.r * S;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = a[t] * f;
+    out[t] = v;
+    for (int q = 0; q < P.p; ++q) reinterpret_cast<double*>(P.base[q])[o + t] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* ticket = reinterpret_cast<unsigned*>(P.base[P.r] + off_flags(P.F, P.p) + 3 * kMaxPeers * 8);
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (last) {
+      *ticket = 0;
+      signal_and_wait(P, FL_AG, epoch);
+    }
+  }
+}
+
 // reduce-scatter: y[t] = sum_q ypart_q[r S + t] (q ascending) once every rank's ypart is final
 __global__ void __launch_bounds__(256) k_p2p_reduce_scatter(Peers P, double* __restrict__ y, int64_t n, int64_t S,
                                                             unsigned long long epoch) {
@@ -198,6 +224,13 @@ void p2p_allgather(Context& C, const double* x, int64_t n, int64_t S, bool into_
   KScope ks(C, KF_COMM);
   const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n, 256), 148 * 4));
   k_p2p_allgather<<<g, 256, 0, C.stream>>>(peers(C), x, n, S, into_ypart ? C.p2p.F : 0, ++C.p2p.ep_ag);
+  HM_CHECK_LAUNCH();
+}
+
+void p2p_scale_publish(Context& C, const double* a, const double* sden, double* out, int64_t n, int64_t S) {
+  KScope ks(C, KF_COMM);
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n, 256), 148 * 4));
+  k_p2p_scale_publish<<<g, 256, 0, C.stream>>>(peers(C), a, sden, out, n, S, ++C.p2p.ep_ag);
   HM_CHECK_LAUNCH();
 }
 

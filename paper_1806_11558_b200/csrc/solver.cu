@@ -157,10 +157,12 @@ struct Red {
 
 unsigned vgrid(int64_t n) { return std::min<unsigned>(grid_for(n, 256), 148 * 16); }
 
-void apply(Context& C, const Layout& L, const double* x, double* y) {
+// gathered: x was already published into every rank's gathered vector by the kernel that
+// produced it (p2p_scale_publish), so the product starts without an all-gather
+void apply(Context& C, const Layout& L, const double* x, double* y, bool gathered = false) {
   if (!L.sharded) { matvec_internal(C, x, y); return; }
   if (p2p_on(C)) {             // libhm's own collectives over NVLink peer memory (p2p.cu)
-    p2p_allgather(C, x, L.n, L.S);
+    if (!gathered) p2p_allgather(C, x, L.n, L.S);
     matvec_internal(C, p2p_xfull(C), p2p_ypart(C), /*reduce=*/false);
     p2p_reduce_scatter(C, y, L.n, L.S);
     return;
@@ -245,16 +247,22 @@ void gmres(Context& C, const Layout& L, const double* b, double* x, double tol, 
     const double beta = std::sqrt(R.dot(w, w));
     if (beta <= tol * bn || total >= C.max_iter) break;
     HM_CUDA(cudaMemcpyAsync(hdev.get(), &beta, sizeof(double), cudaMemcpyHostToDevice, st));
-    { KScope ks_(C, KF_KRYLOV);
-    k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb, N);
+    // sharded over P2P: the normalisation also publishes the next product's x (fused all-gather)
+    const bool fused = L.sharded && p2p_on(C);
+    if (fused) {
+      p2p_scale_publish(C, w, hdev.get(), Vb, N, L.S);
+    } else {
+      { KScope ks_(C, KF_KRYLOV);
+      k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb, N);
+      }
+      HM_CHECK_LAUNCH();
     }
-    HM_CHECK_LAUNCH();
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
     int jend = 0;
     bool conv = false;
     for (int j = 0; j < m; ++j) {
-      apply(C, L, Vb + (int64_t)j * ld, w);
+      apply(C, L, Vb + (int64_t)j * ld, w, fused);
       ++total;
       // CGS2
       double* d1 = R.mdot(Vb, ld, j + 1, w);
@@ -291,10 +299,14 @@ void gmres(Context& C, const Layout& L, const double* b, double* x, double tol, 
       jend = j + 1;
       if (std::fabs(g[j + 1]) <= tol * bn || total >= C.max_iter || hn == 0.0) { conv = true; break; }
       HM_CUDA(cudaMemcpyAsync(hdev.get(), &hn, sizeof(double), cudaMemcpyHostToDevice, st));
-      { KScope ks_(C, KF_KRYLOV);
-      k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb + (int64_t)(j + 1) * ld, N);
+      if (fused) {
+        p2p_scale_publish(C, w, hdev.get(), Vb + (int64_t)(j + 1) * ld, N, L.S);
+      } else {
+        { KScope ks_(C, KF_KRYLOV);
+        k_scale_to<<<vgrid(N), 256, 0, st>>>(w, hdev.get(), true, Vb + (int64_t)(j + 1) * ld, N);
+        }
+        HM_CHECK_LAUNCH();
       }
-      HM_CHECK_LAUNCH();
     }
     for (int i = jend - 1; i >= 0; --i) {
       double s = g[i];
