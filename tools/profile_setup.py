@@ -16,6 +16,8 @@ if os.environ.get("HM_KWS"):
     H.set_option("aca_kws", int(os.environ["HM_KWS"]))
 if os.environ.get("HM_OVERLAP"):
     H.set_option("setup_overlap", int(os.environ["HM_OVERLAP"]))
+if os.environ.get("HM_NEAR_PERF"):
+    H.set_option("near_perf", int(os.environ["HM_NEAR_PERF"]))
 for _ in range(int(os.environ.get("HM_SETUPS", "1"))):
     H.setup(1e-6)
     st = H.stats()
