@@ -242,6 +242,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + STAGES;
+  // per-stage task counters (dynamic task assignment: a warp takes the next task of the stage
+  // when it is free, so the stage is released one task after the average, not after the
+  // round-robin share of the slowest warp); reset by the producer before it refills the stage
+  int* tctr = reinterpret_cast<int*>(empty + STAGES);
   unsigned char* buf = smem + 256;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = cta_first[blockIdx.x], nb = cta_first[blockIdx.x + 1] - b0;
@@ -269,7 +273,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
       const long long tw0 = prof ? clock64() : 0;
       if (it >= STAGES) mbar_wait(&empty[stage], (unsigned)(((it / STAGES) - 1) & 1));
       if (prof && lane == 0) pw_empty += clock64() - tw0;
-      if (lane == 0) mbar_expect_tx(&full[stage], (unsigned)bytes);
+      if (lane == 0) {
+        tctr[stage] = 0;                       // ordered before the consumers' full-wait by the arrive
+        mbar_expect_tx(&full[stage], (unsigned)bytes);
+      }
       __syncwarp();
       unsigned char* sb = buf + stage * SBYTES;
       for (int s0 = 0; s0 < nseg; s0 += 32) {
@@ -298,7 +305,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const double* sd = reinterpret_cast<const double*>(sb);
     const int4* rec = reinterpret_cast<const int4*>(sb);
     const int count = rec[0].x;
-    for (int t = warp - 1; t < count; t += NC) {
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&tctr[stage], 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= count) break;
       const int4 T = rec[1 + t];
       const uint32_t mnk = (uint32_t)T.w;
       const int m = mnk & 2047, n = (mnk >> 11) & 2047, k = mnk >> 22;
