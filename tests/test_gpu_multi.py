@@ -1,8 +1,10 @@
-"""Multi-GPU parity: p ranks, one process per GPU over NCCL, each owning a
-contiguous cost-balanced slice of both leaf lists, partial products summed by
-ncclAllReduce.  Runs tools/multi_rank_check.py under torchrun when the box has
->= 2 GPUs; skipped on a 1-GPU box.  Bars: owned ranges tile both lists; p-rank matvec vs the
-1-rank matvec <= 1e-13 relative; p-rank GMRES solution vs 1-rank <= 1e-8 (see the script)."""
+"""Multi-GPU parity: p ranks, one process per GPU, each owning a contiguous
+cost-balanced slice of both leaf lists, partial products summed over the ranks
+(P:578-587): NCCL, then libhm's peer-memory collectives (hm_p2p_import; the GMRES
+normalisation publishes the next product's x).  Runs tools/multi_rank_check.py under torchrun
+when the box has >= 2 GPUs; skipped on a 1-GPU box.  Bars: owned ranges tile both lists;
+p-rank matvec vs the 1-rank matvec <= 1e-13 relative; p-rank GMRES / CG solutions vs 1-rank
+<= 1e-8; P2P vs NCCL solutions <= 1e-12 with equal iteration counts (see the script)."""
 import json
 import os
 import socket
