@@ -212,8 +212,10 @@ def _run_gpu(args, rank, world, local, dev, stream):
         H.set_option("aca_perf", 1)
     # rhs = the paper's f, assembled by the library
     H.build_tree(Vd, Td, LEAF, ETA)
+    comm_used = "nccl" if world > 1 else None
     if world > 1 and args.comm == "p2p":     # x all-gather / y reduce-scatter / dot all-reduce over NVLink P2P
-        H.enable_p2p(N)
+        perr = H.enable_p2p(N)
+        comm_used = "p2p" if perr is None else f"nccl (p2p unavailable: {str(perr)[:120]})"
     f = torch.empty(N, dtype=torch.float64, device=dev)
     H.assemble_rhs(1, f)
     sol = torch.empty_like(f)
@@ -419,7 +421,7 @@ def _run_gpu(args, rank, world, local, dev, stream):
             "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "N": N, "leaf_size": LEAF, "eta": ETA,
                        "eps_aca": EPS, "solver": "GMRES(100)", "tol": TOL, "rhs": "paper f=4x^2-3y^2-z^2",
                        "parallelism": f"leaf-partition x{world}",
-                       "solve_comm": (args.comm if world > 1 else None),
+                       "solve_comm": comm_used,
                        "factor_storage": "binary32 U, V (option lr_f32; dense blocks and all arithmetic FP64)"
                        if args.lr_f32 else "FP64",
                        "aca_entries": ("perf mode (option aca_perf; pivots identical to the oracle's on 99.9997% "

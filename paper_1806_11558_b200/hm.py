@@ -214,12 +214,31 @@ class HMatrix:
     def enable_p2p(self, n_max, group=None):
         """Sharded-solve collectives over NVLink peer memory (hm_p2p_export / hm_p2p_import):
         every rank exports its exchange buffer, the IPC handles are all-gathered over the torch
-        process group (plumbing only), and every rank maps its peers'."""
+        process group (plumbing only), and every rank maps its peers'.  All ranks must agree on
+        the transport: if any rank cannot map its peers, every rank keeps NCCL (option
+        solve_comm 0) and the error is returned (None on success)."""
+        import torch
         import torch.distributed as dist
-        h = hm_p2p_export(self.ctx, n_max)
+        err = None
+        try:
+            h = hm_p2p_export(self.ctx, n_max)
+        except HMError as e:
+            h, err = b"", e
         allh = [None] * dist.get_world_size(group)
         dist.all_gather_object(allh, h, group=group)
-        hm_p2p_import(self.ctx, b"".join(allh))
+        if err is None and all(len(x) == P2P_HANDLE_BYTES for x in allh):
+            try:
+                hm_p2p_import(self.ctx, b"".join(allh))
+            except HMError as e:
+                err = e
+        ok = torch.tensor([0 if err is not None or any(len(x) != P2P_HANDLE_BYTES for x in allh) else 1],
+                          dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            if self.get_option("solve_comm") != 0:
+                self.set_option("solve_comm", 0)
+            return err or RuntimeError("a peer rank could not map the P2P buffers")
+        return None
 
     def get_option(self, key):
         return hm_get_option(self.ctx, key)
