@@ -149,7 +149,7 @@ const char* hm_last_error(hm_ctx ctx);
  *                  hm_p2p_import, which selects it).
  *   "setup_overlap" 1: hm_setup evaluates the near field on a least-priority stream from a
  *                  second host thread while ACA runs on a greatest-priority stream (results
- *                  bit-identical; 8% shorter setup at N = 1.57M), the default; 0: serial.  With
+ *                  bit-identical; 10-12% shorter setup at N = 1.57M), the default; 0: serial.  With
  *                  kernel timing on, "kt" "eval_union_ms" is the union of the two evaluation
  *                  families' intervals (their sum when serial)
  * Errors: HM_ERR_ARG for an unknown key or an out-of-range value. */

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(64) k_eval_touching(M m, const EntryRef* __res
       int s, t, xs, ys;
       m.pair(r, s, t);
       map_class(m, s, t, xs, ys);
-      m.put(r, quad_split_entry(m.PT, xs, ys, ev));
+      m.put(r, quad_split_entry<PERF>(m.PT, xs, ys, ev));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
