@@ -198,8 +198,9 @@ __device__ __forceinline__ void class3_group(const M& m, int64_t e, int64_t tota
 // Persistent, dynamically balanced: every warp takes groups of kDynGroups x 32 consecutive
 // entries from the counter cnt[2] until the batch is exhausted (a fixed grid-stride split or
 // one thread per entry leave SMs idle at the tail: C4 ACA evaluation 1.85 s resp. 1.75 s vs
-// 1.61 s, profiles/r02_setup_ab1.jsonl)
-constexpr int kDynGroups = 4;
+// 1.61 s, profiles/r02_setup_ab1.jsonl).  Groups per fetch: 1 / 2 / 4 / 8 / 16 / 32 give
+// 1735 / 1607 / 1579 / 1560 / 1561 / 1581 ms (profiles/r02_setup_ab22/23_dyngroups.jsonl).
+constexpr int kDynGroups = 8;
 template <class M>
 __global__ void __launch_bounds__(128, 4) k_eval_class3(M m, const int64_t* __restrict__ dtot,
                                                      EntryRef* __restrict__ lists,
