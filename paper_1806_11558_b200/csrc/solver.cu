@@ -238,12 +238,17 @@ void gmres(Context& C, const Layout& L, const double* b, double* x, double tol, 
   const double bn = std::sqrt(R.dot(b, b));
   int total = 0;
   if (bn == 0.0) { *iters = 0; *relres = 0.0; return; }
+  bool x_zero = true;          // first cycle: x0 = 0, so r0 = b exactly (no product)
   for (;;) {
-    apply(C, L, x, w);
-    { KScope ks_(C, KF_KRYLOV);
-    k_sub<<<vgrid(N), 256, 0, st>>>(b, w, w, N);
+    if (x_zero) {
+      HM_CUDA(cudaMemcpyAsync(w, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    } else {
+      apply(C, L, x, w);
+      { KScope ks_(C, KF_KRYLOV);
+      k_sub<<<vgrid(N), 256, 0, st>>>(b, w, w, N);
+      }
+      HM_CHECK_LAUNCH();
     }
-    HM_CHECK_LAUNCH();
     const double beta = std::sqrt(R.dot(w, w));
     if (beta <= tol * bn || total >= C.max_iter) break;
     HM_CUDA(cudaMemcpyAsync(hdev.get(), &beta, sizeof(double), cudaMemcpyHostToDevice, st));
@@ -318,6 +323,7 @@ void gmres(Context& C, const Layout& L, const double* b, double* x, double tol, 
     k_madd<<<vgrid(N), 256, 0, st>>>(Vb, ld, jend, hdev.get(), x, N);
     }
     HM_CHECK_LAUNCH();
+    x_zero = false;
     HM_CUDA(cudaStreamSynchronize(st));
     if (conv && (std::fabs(g[jend]) <= tol * bn || total >= C.max_iter)) break;
     if (total >= C.max_iter) break;
